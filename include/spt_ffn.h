@@ -1,0 +1,151 @@
+/*
+ * spt_ffn.h -- C ABI of the B200 (sm_100a) routed-FFN library libspt_ffn.so.
+ *
+ * SPT's routed FFN (arXiv 2312.10365, §4.2 "Dynamic routing", PAPER.md:426-437,
+ * and §5.2 Algorithm 4 "The procedure of BSpMV"):
+ *   - the FFN H = act(X W_I), Y = H W_O (Eq. 4) is split into
+ *     G blocks of bw = D/G adjacent hidden units (rows of W_I^T / rows of W_O,
+ *     Fig. 6a);
+ *   - a route network x_R = x W_R (W_R in R^{d x G}) picks, per token, the k
+ *     blocks with the largest |x_R|;
+ *   - tokens are batched per activated block, each block runs as a dense GEMM
+ *     and the block outputs are accumulated per token (Alg. 4).
+ * The three compute calls map to the paper's problem statement (Alg. 4 inputs:
+ * token sequence X, weights W_I, W_O, Indices of activated blocks; output Y)
+ * plus the route network and the backward pass the router training needs
+ * ("trained along with the FFN").
+ *
+ * Conventions (all calls):
+ *   - Every tensor pointer is a DEVICE pointer (cudaMalloc'd or equivalent),
+ *     row-major and contiguous; 16-byte aligned.  The caller owns all memory;
+ *     the library never allocates device memory and retains no pointer after
+ *     a call returns.
+ *   - `stream` is a cudaStream_t (passed as void*); every call only enqueues
+ *     work on it and never synchronises the host.  NULL = legacy default stream.
+ *   - Argument validation happens before any launch; on error nothing is
+ *     enqueued.  Launch failures return SPT_ERR_CUDA; faults inside kernels
+ *     surface at the caller's next synchronisation.  No C++ exception crosses
+ *     the ABI.
+ *   - NaN / Inf inputs are not checked; IEEE propagation applies.  Routing
+ *     stays total-ordered (see spt_ffn_route).
+ *
+ * Shapes (T tokens, d = d_model, D = d_ff, G blocks, bw = D/G, k = top_k,
+ * m' = 2 for SwiGLU (gate and up projections) else 1):
+ *   x, y, dy, dx : [T, d]        act dtype (fp32 or bf16)
+ *   w1           : [D, d]  (SwiGLU: [2, D, d] = gate rows then up rows)
+ *                  = W_I^T of Eq. 4; block b = rows [b*bw, (b+1)*bw)
+ *   w2           : [D, d]  = W_O; block b = rows [b*bw, (b+1)*bw)
+ *   w_r          : [G, d]  = W_R^T (route network)
+ *   dw1, dw2, dw_r : fp32, shapes of w1, w2, w_r
+ */
+#ifndef SPT_FFN_H_
+#define SPT_FFN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPT_FFN_ABI_VERSION 1
+/* Height of a bucket tile: tile_offsets counts ceil(n_b / SPT_TILE_M) per block. */
+#define SPT_TILE_M 128
+
+typedef enum {
+  SPT_OK = 0,
+  SPT_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, T < 0, k < 1, k > G, D % G != 0, dims <= 0 */
+  SPT_ERR_UNSUPPORTED = 2,      /* G > 256, d % 64, bw % 16, fp32 with bw % 4, non-sm_100 device */
+  SPT_ERR_WORKSPACE_TOO_SMALL = 3,
+  SPT_ERR_CUDA = 4              /* a CUDA launch / API call failed */
+} spt_status;
+
+typedef enum { SPT_F32 = 0, SPT_BF16 = 1 } spt_dtype;
+/* SPT_ACT_RELU: Eq. 4; SPT_ACT_GELU: z*Phi(z) (erf form); SPT_ACT_SWIGLU:
+ * silu(x w_gate) * (x w_up), block b covers the gate and up rows of units in b. */
+typedef enum { SPT_ACT_RELU = 0, SPT_ACT_GELU = 1, SPT_ACT_SWIGLU = 2 } spt_act;
+/* SPT_GATE_SIGMOID: each activated block's output is scaled by sigmoid(x_R[b])
+ * (gives the router a gradient); SPT_GATE_NONE: plain 0/1
+ * masking exactly as Alg. 4, router receives no gradient. */
+typedef enum { SPT_GATE_SIGMOID = 0, SPT_GATE_NONE = 1 } spt_gate;
+
+typedef struct {
+  int64_t n_tokens; /* T >= 0 (batch x sequence flattened) */
+  int32_t d_model;  /* d */
+  int32_t d_ff;     /* D, divisible by n_blocks */
+  int32_t n_blocks; /* G <= 256 */
+  int32_t top_k;    /* k = G' in [1, G] (beta = k/G) */
+  int32_t dtype;    /* spt_dtype: storage dtype of x, y, dy, dx, w1, w2, w_r */
+  int32_t act;      /* spt_act */
+  int32_t gate;     /* spt_gate */
+} spt_ffn_desc;
+
+/* Routing decision and bucket layout (all DEVICE buffers, caller-allocated).
+ * Written by spt_ffn_route, read by spt_ffn_forward / spt_ffn_backward. */
+typedef struct {
+  float* logits;         /* [T, G] fp32: x_R = x W_R.  Output; input if SPT_ROUTE_LOGITS_IN */
+  int32_t* topk_idx;     /* [T, k]: activated block ids of each token, ascending */
+  float* topk_gate;      /* [T, k]: gate g of each (token, block) pair (1.0 for GATE_NONE) */
+  int32_t* block_offsets;/* [G+1]: exclusive prefix sum of bucket sizes n_b; [G] = T*k */
+  int32_t* bucket_token; /* [T*k]: block-major, ascending token id within a block
+                            (the order X[Mask_T] of Alg. 4 line 3 visits tokens) */
+  float* bucket_gate;    /* [T*k]: gate of each bucket entry */
+  int32_t* pair_slot;    /* [T*k]: pair_slot[t*k+j] = bucket position of (t, topk_idx[t,j]) */
+  int32_t* tile_offsets; /* [G+1]: exclusive prefix of ceil(n_b / SPT_TILE_M) (device tile schedule) */
+} spt_route_buf;
+
+#define SPT_ROUTE_LOGITS_IN 1u   /* spt_ffn_route: skip x W_R, route the given r->logits */
+#define SPT_BWD_ACCUMULATE_DW 1u /* spt_ffn_backward: dw1/dw2/dw_r += grads instead of = */
+
+/* Bytes of the stash (forward -> backward activations, must survive unchanged
+ * between the two calls) and of the per-call scratch workspace, for `desc`.
+ * Pure host function; needs no device.  Returns SPT_ERR_INVALID_ARGUMENT on a
+ * bad descriptor or NULL out-pointer. */
+spt_status spt_ffn_sizes(const spt_ffn_desc* desc, size_t* stash_bytes, size_t* workspace_bytes);
+
+/* Route network + per-token top-k + token bucketing (Alg. 4
+ * lines 2-3).  x: [T,d]; w_r: [G,d] (may be NULL with SPT_ROUTE_LOGITS_IN).
+ * Selection: the k blocks with the largest |logit|, compared as the uint32 bit
+ * pattern of |logit| (sign cleared; NaN ranks above +Inf), ties -> lower block
+ * id; ids emitted ascending.  Gate = sigmoid(logit) (fp32) or 1.
+ * Writes every field of *r.  ws: >= workspace_bytes from spt_ffn_sizes. */
+spt_status spt_ffn_route(const spt_ffn_desc* desc, const void* x, const void* w_r,
+                         unsigned flags, const spt_route_buf* r, void* ws, size_t ws_bytes,
+                         void* stream);
+
+/* Routed FFN forward (Alg. 4 with accumulation; Fig. 6a):
+ *   y_t = sum_{b in S_t, ascending b} g_{t,b} * act(x_t W1_b^T) W2_b
+ * Reads r (from spt_ffn_route); writes y [T,d] and stash (pre-activations and
+ * gated hidden activations of every (token, block) pair, for the backward). */
+spt_status spt_ffn_forward(const spt_ffn_desc* desc, const void* x, const void* w1,
+                           const void* w2, const spt_route_buf* r, void* y, void* stash,
+                           void* ws, size_t ws_bytes, void* stream);
+
+/* Backward of spt_ffn_forward (routing held fixed; no gradient through the
+ * top-k selection).  Given dy = dL/dy [T,d]:
+ *   dx   [T,d]   = sum_b dZ_b W1_b + sum_b dlogit_b w_r[b]       (act dtype)
+ *   dw1, dw2     = per-block weight gradients (fp32, rows of inactive blocks 0)
+ *   dw_r [G,d]   = sum over pairs of dlogit * x_t  (fp32; 0 for GATE_NONE)
+ *   dgate [T,k]  = dL/dg per pair (fp32, optional: may be NULL)
+ * with dlogit = dgate * g (1 - g) for GATE_SIGMOID.  stash must be the one the
+ * matching spt_ffn_forward wrote.  flags: SPT_BWD_ACCUMULATE_DW. */
+spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void* w1,
+                            const void* w2, const void* w_r, const spt_route_buf* r,
+                            const void* stash, const void* dy, void* dx, float* dw1, float* dw2,
+                            float* dw_r, float* dgate, unsigned flags, void* ws, size_t ws_bytes,
+                            void* stream);
+
+/* Static string for a status code (never NULL). */
+const char* spt_status_string(spt_status s);
+
+/* SPT_FFN_ABI_VERSION of the loaded library. */
+int spt_ffn_abi_version(void);
+
+/* Number of this library's kernels launched by the calling process so far
+ * (host-side counter, for the benchmark's gpu_launches report). */
+uint64_t spt_ffn_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPT_FFN_H_ */

@@ -1,0 +1,95 @@
+// internal.h -- shared declarations of libspt_ffn (not part of the ABI).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/spt_ffn.h"
+
+namespace spt {
+
+constexpr int kTileM = SPT_TILE_M;   // bucket tile height (rows of a grouped-GEMM M tile)
+constexpr int kRouteChunk = 256;     // tokens per bucketing chunk (one CTA)
+constexpr int kMaxBlocks = 256;      // G limit (routing keeps 8 logits per lane)
+
+// Problem geometry derived from spt_ffn_desc.
+struct Geom {
+  int64_t T;
+  int d, D, G, k, bw, mp;  // mp = m' (2 for SwiGLU)
+  int dtype, act, gate;
+  int64_t pairs;     // T*k
+  int64_t rows_cap;  // padded bucket rows: T*k + G*kTileM (>= sum_b ceil(n_b/128)*128)
+  int64_t n_chunks;  // ceil(T / kRouteChunk)
+  int gpad;          // G rounded up to 16 (router GEMM N, dense dlogit width)
+  int esize;         // bytes per act element
+};
+
+// Device-resident views of the routing decision (= spt_route_buf).
+struct RouteView {
+  float* logits;
+  int32_t* topk_idx;
+  float* topk_gate;
+  int32_t* block_offsets;
+  int32_t* bucket_token;
+  float* bucket_gate;
+  int32_t* pair_slot;
+  int32_t* tile_offsets;
+};
+
+// Carved workspace / stash pointers.
+struct Bufs {
+  // stash (forward -> backward)
+  void* z;        // [rows_cap, mp*bw] act: pre-activations (SwiGLU: gate | up)
+  void* h;        // [rows_cap, bw] act: gated hidden g*act(z) (operand of W2 GEMM)
+  // scratch
+  void* part;     // [rows_cap, d] act: per-pair partial outputs (fwd Y, bwd dX)
+  void* dz;       // [rows_cap, mp*bw] act
+  float* da;      // [rows_cap, bw] f32 (SIMT path only)
+  float* dlogit;  // [rows_cap] f32: dL/dlogit per padded bucket row
+  float* dgate;   // [rows_cap] f32: dL/dgate per padded bucket row
+  void* dlg;      // [2, T, gpad] bf16 (hi, lo) dense dlogits (tcgen05 dW_R GEMM)
+  float* dwr_part;// [n_split, G, d] f32 split-K partials of dW_R
+  int n_split;
+  int32_t* chunk_counts;  // [n_chunks, G]
+  int32_t* chunk_base;    // [n_chunks, G]
+  int32_t* n_b;           // [G]
+};
+
+void count_launch(int n = 1);
+
+// routing (route.cu)
+cudaError_t launch_router_simt(const Geom& g, const void* x, const void* w_r, float* logits,
+                               cudaStream_t s);
+cudaError_t launch_topk_bucket(const Geom& g, const RouteView& r, const Bufs& b, cudaStream_t s);
+
+// SIMT path (simt_ffn.cu), any dtype
+cudaError_t simt_forward(const Geom& g, const void* x, const void* w1, const void* w2,
+                         const RouteView& r, void* y, const Bufs& b, cudaStream_t s);
+cudaError_t simt_backward(const Geom& g, const void* x, const void* w1, const void* w2,
+                          const void* w_r, const RouteView& r, const void* dy, void* dx,
+                          float* dw1, float* dw2, float* dw_r, float* dgate_out, bool accumulate,
+                          const Bufs& b, cudaStream_t s);
+
+// shared HBM-bound kernels (combine.cu)
+cudaError_t launch_combine_fwd(const Geom& g, const RouteView& r, const void* part, void* y,
+                               cudaStream_t s);
+cudaError_t launch_combine_bwd(const Geom& g, const RouteView& r, const void* part,
+                               const float* dlogit, const void* w_r, void* dx, cudaStream_t s);
+cudaError_t launch_gather_dgate(const Geom& g, const RouteView& r, const float* dgate_rows,
+                                float* dgate_out, cudaStream_t s);
+
+// tcgen05 path (tc_ffn.cu), bf16 only
+bool tc_supported(const Geom& g);
+cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logits,
+                      cudaStream_t s);
+cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void* w2,
+                       const RouteView& r, void* y, const Bufs& b, cudaStream_t s);
+cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void* w2,
+                        const void* w_r, const RouteView& r, const void* dy, void* dx, float* dw1,
+                        float* dw2, float* dw_r, float* dgate_out, bool accumulate, const Bufs& b,
+                        cudaStream_t s);
+
+// device helpers shared by kernels
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace spt

@@ -1,0 +1,240 @@
+// route.cu -- a2 per-token top-k selection and a3 token bucketing,
+// plus the SIMT route network for the fp32 path.
+//
+// Route network x_R = x W_R, top-G' blocks by largest magnitude.
+// Bucketing replaces Alg. 4's per-block masks Mask_T = eq(Indices, i) and the
+// gathers X[Mask_T] by one device-side layout:
+//   K-topk    : one warp per token; k rounds of warp-argmax over 64-bit keys
+//               (|logit| bit pattern << 9 | (256 - id)), emits ids ascending,
+//               gates, and a per-chunk (256-token) block histogram in smem.
+//   K-scan    : one CTA per block: exclusive scan of the chunk histograms.
+//   K-scatter : one CTA per chunk: per-warp lane masks give each (token,block)
+//               pair its stable rank -> bucket_token / bucket_gate / pair_slot.
+// No atomics on global memory, no host synchronisation, deterministic.
+#include "internal.h"
+
+namespace spt {
+
+template <typename TIn>
+__device__ __forceinline__ float ldf(const TIn* p) {
+  return static_cast<float>(*p);
+}
+template <>
+__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+
+// ---------------------------------------------------------------- SIMT router
+template <typename TIn>
+__global__ void router_simt_kernel(int64_t T, int d, int G, const TIn* __restrict__ x,
+                                   const TIn* __restrict__ w_r, float* __restrict__ logits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (t >= T) return;
+  const TIn* xr = x + t * d;
+  for (int b = 0; b < G; ++b) {
+    const TIn* wr = w_r + (int64_t)b * d;
+    float s = 0.f;
+    for (int c = lane; c < d; c += 32) s = fmaf(ldf(xr + c), ldf(wr + c), s);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) logits[t * G + b] = s;
+  }
+}
+
+cudaError_t launch_router_simt(const Geom& g, const void* x, const void* w_r, float* logits,
+                               cudaStream_t s) {
+  const int warps = 8;
+  dim3 grid((unsigned)ceil_div(g.T, warps));
+  if (g.dtype == SPT_F32)
+    router_simt_kernel<float><<<grid, warps * 32, 0, s>>>(g.T, g.d, g.G, (const float*)x,
+                                                           (const float*)w_r, logits);
+  else
+    router_simt_kernel<__nv_bfloat16><<<grid, warps * 32, 0, s>>>(
+        g.T, g.d, g.G, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w_r, logits);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------- top-k
+// Selection key: larger |logit| bit pattern first (sign cleared, so NaN >
+// +Inf > finite), then lower block id.  key = absbits << 9 | (256 - b) >= 1.
+__global__ void __launch_bounds__(256) topk_hist_kernel(int64_t T, int G, int k, int gate_mode,
+                                                        const float* __restrict__ logits,
+                                                        int32_t* __restrict__ topk_idx,
+                                                        float* __restrict__ topk_gate,
+                                                        int32_t* __restrict__ chunk_counts) {
+  __shared__ int hist[kMaxBlocks];
+  for (int b = threadIdx.x; b < G; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t chunk = blockIdx.x;
+  const int nslot = (G + 31) / 32;
+  for (int i = 0; i < 32; ++i) {
+    const int64_t t = chunk * kRouteChunk + warp * 32 + i;
+    if (t >= T) break;
+    unsigned long long key[8];
+    float lg[8];
+    bool sel[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int b = s * 32 + lane;
+      sel[s] = false;
+      key[s] = 0ull;
+      lg[s] = 0.f;
+      if (s < nslot && b < G) {
+        lg[s] = logits[t * G + b];
+        const uint32_t ab = __float_as_uint(lg[s]) & 0x7fffffffu;
+        key[s] = ((unsigned long long)ab << 9) | (unsigned long long)(256 - b);
+      }
+    }
+    for (int r = 0; r < k; ++r) {
+      unsigned long long best = 0ull;
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (!sel[s] && key[s] > best) best = key[s];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+        best = other > best ? other : best;
+      }
+      const int bsel = 256 - (int)(best & 511ull);
+      if ((bsel & 31) == lane) {
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s == (bsel >> 5)) sel[s] = true;
+      }
+    }
+    // emit ascending block ids: slot-major ballots
+    int base = 0;
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const unsigned m = __ballot_sync(0xffffffffu, sel[s]);
+      if (sel[s]) {
+        const int pos = base + __popc(m & lt);
+        const int b = s * 32 + lane;
+        topk_idx[t * k + pos] = b;
+        topk_gate[t * k + pos] = gate_mode == SPT_GATE_SIGMOID ? 1.f / (1.f + expf(-lg[s])) : 1.f;
+        atomicAdd(&hist[b], 1);
+      }
+      base += __popc(m);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < G; b += blockDim.x) chunk_counts[chunk * G + b] = hist[b];
+}
+
+// --------------------------------------------------------------- bucket scan
+// CTA b: chunk_base[c][b] = sum_{c' < c} chunk_counts[c'][b]; n_b[b] = total.
+__global__ void __launch_bounds__(256) bucket_scan_kernel(int64_t n_chunks, int G,
+                                                          const int32_t* __restrict__ counts,
+                                                          int32_t* __restrict__ chunk_base,
+                                                          int32_t* __restrict__ n_b) {
+  __shared__ int wsum[8];
+  const int b = blockIdx.x;
+  const int per = (int)ceil_div(n_chunks, blockDim.x);
+  const int64_t c0 = (int64_t)threadIdx.x * per;
+  int local = 0;
+  for (int i = 0; i < per; ++i)
+    if (c0 + i < n_chunks) local += counts[(c0 + i) * G + b];
+  // block exclusive scan of `local`
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int wpre = 0;
+  for (int w = 0; w < warp; ++w) wpre += wsum[w];
+  int run = wpre + incl - local;
+  for (int i = 0; i < per; ++i)
+    if (c0 + i < n_chunks) {
+      chunk_base[(c0 + i) * G + b] = run;
+      run += counts[(c0 + i) * G + b];
+    }
+  if (threadIdx.x == blockDim.x - 1) n_b[b] = run;
+}
+
+// ------------------------------------------------------------ bucket scatter
+__global__ void __launch_bounds__(256) bucket_scatter_kernel(
+    int64_t T, int G, int k, const int32_t* __restrict__ n_b, const int32_t* __restrict__ chunk_base,
+    const int32_t* __restrict__ topk_idx, const float* __restrict__ topk_gate,
+    int32_t* __restrict__ block_offsets, int32_t* __restrict__ tile_offsets,
+    int32_t* __restrict__ bucket_token, float* __restrict__ bucket_gate,
+    int32_t* __restrict__ pair_slot) {
+  __shared__ int boff[kMaxBlocks + 1];
+  __shared__ int toff[kMaxBlocks + 1];
+  __shared__ unsigned mask[8][kMaxBlocks];
+  __shared__ int wbase[8][kMaxBlocks];
+  __shared__ int wsum[8], wsum2[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t chunk = blockIdx.x;
+  // exclusive scans over blocks of n_b and ceil(n_b / kTileM)
+  {
+    const int b = threadIdx.x;
+    const int v = b < G ? n_b[b] : 0;
+    const int vt = (int)ceil_div(v, kTileM);
+    int inc = v, inct = vt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc, o);
+      const int at = __shfl_up_sync(0xffffffffu, inct, o);
+      if (lane >= o) { inc += a; inct += at; }
+    }
+    if (lane == 31) { wsum[warp] = inc; wsum2[warp] = inct; }
+    __syncthreads();
+    int p = 0, pt = 0;
+    for (int w = 0; w < warp; ++w) { p += wsum[w]; pt += wsum2[w]; }
+    if (b < G) { boff[b] = p + inc - v; toff[b] = pt + inct - vt; }
+    if (b == G - 1) { boff[G] = p + inc; toff[G] = pt + inct; }
+  }
+  for (int i = threadIdx.x; i < 8 * kMaxBlocks; i += blockDim.x) (&mask[0][0])[i] = 0u;
+  __syncthreads();
+  if (chunk == 0)
+    for (int b = threadIdx.x; b <= G; b += blockDim.x) {
+      block_offsets[b] = boff[b];
+      tile_offsets[b] = toff[b];
+    }
+  const int64_t t = chunk * kRouteChunk + warp * 32 + lane;
+  const bool valid = t < T;
+  if (valid)
+    for (int j = 0; j < k; ++j) atomicOr(&mask[warp][topk_idx[t * k + j]], 1u << lane);
+  __syncthreads();
+  for (int b = threadIdx.x; b < G; b += blockDim.x) {
+    int run = 0;
+    for (int w = 0; w < 8; ++w) {
+      wbase[w][b] = run;
+      run += __popc(mask[w][b]);
+    }
+  }
+  __syncthreads();
+  if (valid) {
+    const unsigned lt = (1u << lane) - 1u;
+    for (int j = 0; j < k; ++j) {
+      const int b = topk_idx[t * k + j];
+      const int pos =
+          boff[b] + chunk_base[chunk * G + b] + wbase[warp][b] + __popc(mask[warp][b] & lt);
+      bucket_token[pos] = (int32_t)t;
+      bucket_gate[pos] = topk_gate[t * k + j];
+      pair_slot[t * k + j] = pos;
+    }
+  }
+}
+
+cudaError_t launch_topk_bucket(const Geom& g, const RouteView& r, const Bufs& b, cudaStream_t s) {
+  const unsigned nch = (unsigned)g.n_chunks;
+  topk_hist_kernel<<<nch, 256, 0, s>>>(g.T, g.G, g.k, g.gate, r.logits, r.topk_idx, r.topk_gate,
+                                       b.chunk_counts);
+  bucket_scan_kernel<<<g.G, 256, 0, s>>>(g.n_chunks, g.G, b.chunk_counts, b.chunk_base, b.n_b);
+  bucket_scatter_kernel<<<nch, 256, 0, s>>>(g.T, g.G, g.k, b.n_b, b.chunk_base, r.topk_idx,
+                                            r.topk_gate, r.block_offsets, r.tile_offsets,
+                                            r.bucket_token, r.bucket_gate, r.pair_slot);
+  count_launch(3);
+  return cudaGetLastError();
+}
+
+}  // namespace spt

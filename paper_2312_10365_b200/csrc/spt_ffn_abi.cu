@@ -1,0 +1,239 @@
+// spt_ffn_abi.cu -- the C ABI of include/spt_ffn.h: validation, workspace
+// carving and dispatch to the sm_100a kernels.  Host code only.
+#include <atomic>
+#include <cstring>
+
+#include "internal.h"
+
+namespace spt {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+static inline size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static spt_status make_geom(const spt_ffn_desc* d, Geom* g) {
+  if (!d) return SPT_ERR_INVALID_ARGUMENT;
+  if (d->n_tokens < 0 || d->d_model <= 0 || d->d_ff <= 0 || d->n_blocks <= 0)
+    return SPT_ERR_INVALID_ARGUMENT;
+  if (d->top_k < 1 || d->top_k > d->n_blocks) return SPT_ERR_INVALID_ARGUMENT;
+  if (d->d_ff % d->n_blocks) return SPT_ERR_INVALID_ARGUMENT;
+  if (d->dtype != SPT_F32 && d->dtype != SPT_BF16) return SPT_ERR_INVALID_ARGUMENT;
+  if (d->act < SPT_ACT_RELU || d->act > SPT_ACT_SWIGLU) return SPT_ERR_INVALID_ARGUMENT;
+  if (d->gate != SPT_GATE_SIGMOID && d->gate != SPT_GATE_NONE) return SPT_ERR_INVALID_ARGUMENT;
+  g->T = d->n_tokens;
+  g->d = d->d_model;
+  g->D = d->d_ff;
+  g->G = d->n_blocks;
+  g->k = d->top_k;
+  g->bw = g->D / g->G;
+  g->mp = d->act == SPT_ACT_SWIGLU ? 2 : 1;
+  g->dtype = d->dtype;
+  g->act = d->act;
+  g->gate = d->gate;
+  g->pairs = g->T * g->k;
+  g->rows_cap = g->pairs + (int64_t)g->G * kTileM;
+  g->n_chunks = ceil_div(g->T, kRouteChunk);
+  g->gpad = (int)ceil_div(g->G, 16) * 16;
+  g->esize = d->dtype == SPT_BF16 ? 2 : 4;
+  if (g->G > kMaxBlocks) return SPT_ERR_UNSUPPORTED;
+  if (g->d % 64) return SPT_ERR_UNSUPPORTED;
+  if (g->bw % 16) return SPT_ERR_UNSUPPORTED;
+  if (g->pairs + (int64_t)g->G * kTileM > INT32_MAX) return SPT_ERR_UNSUPPORTED;
+  if (g->dtype == SPT_BF16 && !tc_supported(*g)) return SPT_ERR_UNSUPPORTED;
+  return SPT_OK;
+}
+
+static int dwr_splits(const Geom& g) {
+  const int tiles = (int)(ceil_div(g.G, 128) * ceil_div(g.d, 256));
+  int s = (int)ceil_div(148, tiles);
+  const int max_s = (int)ceil_div(g.T, 64);
+  if (s > max_s) s = max_s;
+  return s < 1 ? 1 : s;
+}
+
+struct Sizes {
+  size_t z, h, stash;
+  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, ws;
+};
+
+static Sizes compute_sizes(const Geom& g) {
+  Sizes s{};
+  const size_t e = (size_t)g.esize;
+  s.z = align256((size_t)g.rows_cap * g.mp * g.bw * e);
+  s.h = align256((size_t)g.rows_cap * g.bw * e);
+  s.stash = s.z + s.h;
+  s.part = align256((size_t)g.rows_cap * g.d * e);
+  s.dz = align256((size_t)g.rows_cap * g.mp * g.bw * e);
+  s.da = g.dtype == SPT_F32 ? align256((size_t)g.rows_cap * g.bw * 4) : 0;
+  s.dlogit = align256((size_t)g.rows_cap * 4);
+  s.dgate = align256((size_t)g.rows_cap * 4);
+  s.dlg = g.dtype == SPT_BF16 ? align256((size_t)2 * g.T * g.gpad * 2) : 0;
+  s.dwr = g.dtype == SPT_BF16 ? align256((size_t)dwr_splits(g) * g.G * g.d * 4) : 0;
+  s.counts = align256((size_t)g.n_chunks * g.G * 4);
+  s.base = s.counts;
+  s.nb = align256((size_t)g.G * 4);
+  s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb;
+  return s;
+}
+
+static Bufs carve(const Geom& g, void* stash, void* ws) {
+  Sizes s = compute_sizes(g);
+  Bufs b{};
+  uint8_t* p = (uint8_t*)stash;
+  if (p) {
+    b.z = p;
+    b.h = p + s.z;
+  }
+  uint8_t* w = (uint8_t*)ws;
+  b.part = w; w += s.part;
+  b.dz = w; w += s.dz;
+  b.da = s.da ? (float*)w : nullptr; w += s.da;
+  b.dlogit = (float*)w; w += s.dlogit;
+  b.dgate = (float*)w; w += s.dgate;
+  b.dlg = s.dlg ? (void*)w : nullptr; w += s.dlg;
+  b.dwr_part = s.dwr ? (float*)w : nullptr; w += s.dwr;
+  b.n_split = g.dtype == SPT_BF16 ? dwr_splits(g) : 0;
+  b.chunk_counts = (int32_t*)w; w += s.counts;
+  b.chunk_base = (int32_t*)w; w += s.base;
+  b.n_b = (int32_t*)w; w += s.nb;
+  return b;
+}
+
+static RouteView view(const spt_route_buf* r) {
+  return RouteView{r->logits,       r->topk_idx,   r->topk_gate, r->block_offsets,
+                   r->bucket_token, r->bucket_gate, r->pair_slot, r->tile_offsets};
+}
+
+static bool route_complete(const spt_route_buf* r) {
+  return r && r->logits && r->topk_idx && r->topk_gate && r->block_offsets && r->bucket_token &&
+         r->bucket_gate && r->pair_slot && r->tile_offsets;
+}
+
+static spt_status device_ok() {
+  static int cached = -1;  // per-process; the library targets one architecture
+  if (cached < 0) {
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return SPT_ERR_CUDA;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cached = (major == 10 && minor == 0) ? 1 : 0;
+  }
+  return cached ? SPT_OK : SPT_ERR_UNSUPPORTED;
+}
+
+static spt_status to_status(cudaError_t e) { return e == cudaSuccess ? SPT_OK : SPT_ERR_CUDA; }
+
+}  // namespace spt
+
+using namespace spt;
+
+extern "C" {
+#pragma GCC visibility push(default)
+
+int spt_ffn_abi_version(void) { return SPT_FFN_ABI_VERSION; }
+
+uint64_t spt_ffn_launch_count(void) { return g_launches.load(); }
+
+const char* spt_status_string(spt_status s) {
+  switch (s) {
+    case SPT_OK: return "SPT_OK";
+    case SPT_ERR_INVALID_ARGUMENT: return "SPT_ERR_INVALID_ARGUMENT";
+    case SPT_ERR_UNSUPPORTED: return "SPT_ERR_UNSUPPORTED";
+    case SPT_ERR_WORKSPACE_TOO_SMALL: return "SPT_ERR_WORKSPACE_TOO_SMALL";
+    case SPT_ERR_CUDA: return "SPT_ERR_CUDA";
+  }
+  return "SPT_ERR_UNKNOWN";
+}
+
+spt_status spt_ffn_sizes(const spt_ffn_desc* desc, size_t* stash_bytes, size_t* workspace_bytes) {
+  if (!stash_bytes || !workspace_bytes) return SPT_ERR_INVALID_ARGUMENT;
+  Geom g;
+  spt_status st = make_geom(desc, &g);
+  if (st != SPT_OK) return st;
+  Sizes s = compute_sizes(g);
+  *stash_bytes = s.stash;
+  *workspace_bytes = s.ws;
+  return SPT_OK;
+}
+
+spt_status spt_ffn_route(const spt_ffn_desc* desc, const void* x, const void* w_r, unsigned flags,
+                         const spt_route_buf* r, void* ws, size_t ws_bytes, void* stream) {
+  Geom g;
+  spt_status st = make_geom(desc, &g);
+  if (st != SPT_OK) return st;
+  const bool logits_in = flags & SPT_ROUTE_LOGITS_IN;
+  if (!route_complete(r) || !ws || (!logits_in && (!x || !w_r))) return SPT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < compute_sizes(g).ws) return SPT_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = device_ok()) != SPT_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  Bufs b = carve(g, nullptr, ws);
+  RouteView rv = view(r);
+  if (g.T == 0) {
+    if (cudaMemsetAsync(r->block_offsets, 0, (g.G + 1) * 4, s) != cudaSuccess ||
+        cudaMemsetAsync(r->tile_offsets, 0, (g.G + 1) * 4, s) != cudaSuccess)
+      return SPT_ERR_CUDA;
+    return SPT_OK;
+  }
+  cudaError_t e = cudaSuccess;
+  if (!logits_in) {
+    e = g.dtype == SPT_BF16 ? tc_router(g, x, w_r, r->logits, s)
+                            : launch_router_simt(g, x, w_r, r->logits, s);
+    if (e != cudaSuccess) return SPT_ERR_CUDA;
+  }
+  return to_status(launch_topk_bucket(g, rv, b, s));
+}
+
+spt_status spt_ffn_forward(const spt_ffn_desc* desc, const void* x, const void* w1, const void* w2,
+                           const spt_route_buf* r, void* y, void* stash, void* ws, size_t ws_bytes,
+                           void* stream) {
+  Geom g;
+  spt_status st = make_geom(desc, &g);
+  if (st != SPT_OK) return st;
+  if (!x || !w1 || !w2 || !route_complete(r) || !y || !stash || !ws) return SPT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < compute_sizes(g).ws) return SPT_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = device_ok()) != SPT_OK) return st;
+  if (g.T == 0) return SPT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  Bufs b = carve(g, stash, ws);
+  RouteView rv = view(r);
+  cudaError_t e = g.dtype == SPT_BF16 ? tc_forward(g, x, w1, w2, rv, y, b, s)
+                                      : simt_forward(g, x, w1, w2, rv, y, b, s);
+  return to_status(e);
+}
+
+spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void* w1, const void* w2,
+                            const void* w_r, const spt_route_buf* r, const void* stash,
+                            const void* dy, void* dx, float* dw1, float* dw2, float* dw_r,
+                            float* dgate, unsigned flags, void* ws, size_t ws_bytes,
+                            void* stream) {
+  Geom g;
+  spt_status st = make_geom(desc, &g);
+  if (st != SPT_OK) return st;
+  if (!x || !w1 || !w2 || !w_r || !route_complete(r) || !stash || !dy || !dx || !dw1 || !dw2 ||
+      !dw_r || !ws)
+    return SPT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < compute_sizes(g).ws) return SPT_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = device_ok()) != SPT_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool acc = flags & SPT_BWD_ACCUMULATE_DW;
+  if (g.T == 0) {
+    if (acc) return SPT_OK;
+    const size_t w1b = (size_t)g.mp * g.D * g.d * 4, w2b = (size_t)g.D * g.d * 4,
+                 wrb = (size_t)g.G * g.d * 4;
+    if (cudaMemsetAsync(dw1, 0, w1b, s) != cudaSuccess || cudaMemsetAsync(dw2, 0, w2b, s) ||
+        cudaMemsetAsync(dw_r, 0, wrb, s))
+      return SPT_ERR_CUDA;
+    return SPT_OK;
+  }
+  Bufs b = carve(g, const_cast<void*>(stash), ws);
+  RouteView rv = view(r);
+  cudaError_t e = g.dtype == SPT_BF16
+                      ? tc_backward(g, x, w1, w2, w_r, rv, dy, dx, dw1, dw2, dw_r, dgate, acc, b, s)
+                      : simt_backward(g, x, w1, w2, w_r, rv, dy, dx, dw1, dw2, dw_r, dgate, acc, b,
+                                      s);
+  return to_status(e);
+}
+
+#pragma GCC visibility pop
+}  // extern "C"

@@ -1,0 +1,739 @@
+// tc_ffn.cu -- bf16 path of the routed FFN on the 5th-generation tensor cores.
+//
+// One persistent, warp-specialised tcgen05 kernel template serves every GEMM
+// on the hot path:
+//   warp 0     TMA producer (all 32 lanes issue; gathers use tile::gather4)
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5  epilogue: tcgen05.ld (TMEM -> registers), fused math, stores
+// M tile = 128 bucket rows (one TMEM lane per row), K stage = 64 bf16 (one
+// 128-byte swizzle row), N <= 256 per MMA, 2 TMEM accumulators (512 columns)
+// so the epilogue of tile i overlaps the MMAs of tile i+1, 3-6 smem stages.
+//
+// Kinds (Alg. 4 of PAPER.md:564-579 as grouped GEMMs over the bucket layout):
+//   ROUTER : logits = X W_R                    A = X tile,       B = w_r (K-major)
+//   FWD1   : Z_b = X[bucket_b] W1_b^T          A = gather4(X),   B = w1 rows (K-major)
+//            epilogue: Z stash, H~ = g * act(Z)     (Alg. 4 line 4, gate)
+//   FWD2   : P_b = H~_b W2_b                   A = H~ rows,      B = w2 rows (MN-major)
+//   DA     : dA_b = dY[bucket_b] W2_b^T        A = gather4(dY),  B = w2 rows (K-major)
+//            epilogue: dgate = rowdot(dA, act(Z)), dZ = g dA act'(Z), dlogit
+//   DX     : dXp_b = dZ_b W1_b                 A = dZ rows,      B = w1 rows (MN-major)
+//   DW1    : dW1_b = dZ_b^T X[bucket_b]        A = dZ (MN-major), B = gather4(X) along K
+//   DW2    : dW2_b = H~_b^T dY[bucket_b]       A = H~ (MN-major), B = gather4(dY) along K
+//   DWR    : dW_R = dLogits^T X  (split-K)     A = dense dlogits hi|lo (MN-major), B = X (MN-major)
+// Padded bucket rows: tile t128 of the schedule covers rows [t128*128, +128);
+// rows past a block's n_b are zero in every stash written here, which makes
+// the K tails of the weight-gradient GEMMs exact.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "act.cuh"
+#include "tc_common.cuh"
+#include "tmap.h"
+
+namespace spt {
+
+using namespace tc;
+
+enum Kind : int { K_ROUTER = 0, K_FWD1, K_FWD2, K_DA, K_DX, K_DW1, K_DW2, K_DWR };
+
+struct TcArgs {
+  CUtensorMap ta;  // A operand
+  CUtensorMap tb;  // B operand
+  RouteView r;
+  int64_t T;
+  int G, d, D, bw, mp, act, gate, gpad;
+  int NT;          // N tiles of 256 (FWD2/DX/DW*/DWR)
+  int MT;          // M tiles per block (DW*), per router (DWR)
+  int n_split;     // DWR split-K factor
+  int ksplit;      // DWR tokens per split (multiple of 64)
+  int acc_mode;    // DW*: accumulate into output
+  int BN;          // MMA N
+  void* out;       // kind-specific primary output
+  void* out2;      // secondary output (FWD1: h; DA: dz)
+  const void* aux; // DA: z stash
+  float* rows_f;   // DA: dgate rows
+  float* rows_g;   // DA: dlogit rows
+  void* dlg;       // DA: dense dlogits [2][T][gpad] bf16
+};
+
+constexpr int kThreads = 192;
+constexpr int kABytes = 16384;
+
+__host__ __device__ constexpr int b_bytes(int kind, int BN) {
+  return (kind == K_ROUTER || kind == K_FWD1 || kind == K_DA) ? BN * 128 : 32768;
+}
+
+__device__ __forceinline__ int find_block(const int32_t* tile_offsets, int G, int t128) {
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tile_offsets[mid] <= t128) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+struct TileInfo {
+  int b, nt, mt;
+  int n_valid;      // valid rows of the M tile (bucket-row kinds)
+  int64_t prow0;    // first padded bucket row of the M tile (bucket-row kinds)
+  int64_t pos0;     // bucket position of row 0 (bucket-row kinds) / of block start (DW*)
+  int nkb;          // K stages
+  int64_t kbase;    // DW*: first padded row of the block; DWR: first token of the split
+};
+
+template <int KIND>
+__device__ __forceinline__ int num_tiles(const TcArgs& a) {
+  if (KIND == K_ROUTER) return (int)ceil_div(a.T, 128);
+  if (KIND == K_FWD1 || KIND == K_DA) return a.r.tile_offsets[a.G];
+  if (KIND == K_FWD2 || KIND == K_DX) return a.r.tile_offsets[a.G] * a.NT;
+  if (KIND == K_DW1 || KIND == K_DW2) return a.G * a.MT * a.NT;
+  return a.MT * a.NT * a.n_split;  // DWR
+}
+
+template <int KIND>
+__device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
+  TileInfo ti{};
+  if (KIND == K_ROUTER) {
+    ti.prow0 = (int64_t)tile * 128;
+    ti.n_valid = (int)(a.T - ti.prow0 < 128 ? a.T - ti.prow0 : 128);
+    ti.nkb = a.d / 64;
+  } else if (KIND == K_FWD1 || KIND == K_DA || KIND == K_FWD2 || KIND == K_DX) {
+    int t128 = tile;
+    if (KIND == K_FWD2 || KIND == K_DX) {
+      t128 = tile / a.NT;
+      ti.nt = tile % a.NT;
+    }
+    ti.b = find_block(a.r.tile_offsets, a.G, t128);
+    const int mt = t128 - a.r.tile_offsets[ti.b];
+    const int nb = a.r.block_offsets[ti.b + 1] - a.r.block_offsets[ti.b];
+    ti.n_valid = nb - mt * 128;
+    ti.prow0 = (int64_t)t128 * 128;
+    ti.pos0 = a.r.block_offsets[ti.b] + mt * 128;
+    if (KIND == K_FWD1 || KIND == K_DA) ti.nkb = a.d / 64;
+    else if (KIND == K_FWD2) ti.nkb = (a.bw + 63) / 64;
+    else ti.nkb = (a.mp * a.bw + 63) / 64;
+  } else if (KIND == K_DW1 || KIND == K_DW2) {
+    ti.nt = tile % a.NT;
+    ti.mt = (tile / a.NT) % a.MT;
+    ti.b = tile / (a.NT * a.MT);
+    ti.pos0 = a.r.block_offsets[ti.b];
+    ti.n_valid = a.r.block_offsets[ti.b + 1] - a.r.block_offsets[ti.b];  // bucket size n_b
+    ti.kbase = (int64_t)a.r.tile_offsets[ti.b] * 128;
+    ti.nkb = 2 * (a.r.tile_offsets[ti.b + 1] - a.r.tile_offsets[ti.b]);
+  } else {  // DWR: tile = (split, mt, nt)
+    ti.nt = tile % a.NT;
+    ti.mt = (tile / a.NT) % a.MT;
+    const int s = tile / (a.NT * a.MT);
+    ti.b = s;
+    ti.kbase = (int64_t)s * a.ksplit;
+    const int64_t t1 = a.T < ti.kbase + a.ksplit ? a.T : ti.kbase + a.ksplit;
+    const int nk = t1 > ti.kbase ? (int)ceil_div(t1 - ti.kbase, 64) : 0;
+    ti.nkb = 2 * nk;  // hi part then lo part
+  }
+  return ti;
+}
+
+template <int KIND>
+__device__ __forceinline__ uint32_t stage_tx_bytes(const TcArgs& a) {
+  if (KIND == K_FWD1) return kABytes + a.mp * a.bw * 128;
+  if (KIND == K_DA) return kABytes + a.bw * 128;
+  if (KIND == K_ROUTER) return kABytes + a.gpad * 128;
+  return kABytes + 32768;
+}
+
+// ---------------------------------------------------------------- producer
+template <int KIND>
+__device__ __forceinline__ void produce_stage(const TcArgs& a, const TileInfo& ti, int kb,
+                                              uint8_t* sA, uint8_t* sB, uint64_t* bar, int lane,
+                                              const int (&rows4)[4]) {
+  if (KIND == K_ROUTER) {
+    if (lane == 0) {
+      tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
+      tma_load_2d(sB, &a.tb, bar, kb * 64, 0);
+    }
+  } else if (KIND == K_FWD1 || KIND == K_DA) {
+    // A: 128 gathered token rows, lane l -> rows 4l..4l+3
+    tma_gather4(sA + lane * 512, &a.ta, bar, kb * 64, rows4[0], rows4[1], rows4[2], rows4[3]);
+    if (lane == 0) {
+      tma_load_2d(sB, &a.tb, bar, kb * 64, ti.b * a.bw);
+      if (KIND == K_FWD1 && a.mp == 2)
+        tma_load_2d(sB + a.bw * 128, &a.tb, bar, kb * 64, a.D + ti.b * a.bw);
+    }
+  } else if (KIND == K_FWD2 || KIND == K_DX) {
+    if (lane == 0) {
+      tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
+      int krow;
+      if (KIND == K_FWD2) krow = ti.b * a.bw + kb * 64;
+      else krow = kb * 64 < a.bw ? ti.b * a.bw + kb * 64 : a.D + ti.b * a.bw + (kb * 64 - a.bw);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, krow);
+    }
+  } else if (KIND == K_DW1 || KIND == K_DW2) {
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        tma_load_2d(sA + j * 8192, &a.ta, bar, ti.mt * 128 + j * 64, (int)(ti.kbase + kb * 64));
+    }
+    // B: 64 gathered token rows (K) x 256 columns (N): 64 gather4 calls over 32 lanes
+#pragma unroll
+    for (int c2 = 0; c2 < 2; ++c2) {
+      const int c = lane + 32 * c2;
+      const int j = c >> 4, rg = c & 15;
+      int rr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = kb * 64 + rg * 4 + i;  // entry within block bucket
+        rr[i] = e < ti.n_valid ? a.r.bucket_token[ti.pos0 + e] : (int)a.T;
+      }
+      tma_gather4(sB + j * 8192 + rg * 512, &a.tb, bar, ti.nt * 256 + j * 64, rr[0], rr[1], rr[2],
+                  rr[3]);
+    }
+  } else {  // DWR
+    if (lane == 0) {
+      const int nk = ti.nkb / 2;
+      const int part = kb >= nk;
+      const int kk = part ? kb - nk : kb;
+      const int trow = (int)(ti.kbase + kk * 64);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        tma_load_2d(sA + j * 8192, &a.ta, bar, ti.mt * 128 + j * 64, (int)(part * a.T) + trow);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, trow);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- epilogues
+// Row `row` of the tile is TMEM lane `row`; this thread owns it entirely.
+template <int KIND>
+__device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, uint32_t tacc,
+                                         int row) {
+  const bool valid = row < ti.n_valid;
+  if (KIND == K_ROUTER) {
+    const int64_t t = ti.prow0 + row;
+    for (int c0 = 0; c0 < a.gpad; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(tacc + c0, v);
+      tmem_ld_wait();
+      if (valid) {
+        float* dst = (float*)a.out + t * a.G;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (c0 + i < a.G) dst[c0 + i] = __uint_as_float(v[i]);
+      }
+    }
+  } else if (KIND == K_FWD1) {
+    const float g = valid ? a.r.bucket_gate[ti.pos0 + row] : 0.f;
+    const int64_t prow = ti.prow0 + row;
+    __nv_bfloat16* zr = (__nv_bfloat16*)a.out + prow * (int64_t)(a.mp * a.bw);
+    __nv_bfloat16* hr = (__nv_bfloat16*)a.out2 + prow * (int64_t)a.bw;
+    for (int u0 = 0; u0 < a.bw; u0 += 32) {
+      uint32_t vg[32], vu[32];
+      tmem_ld32(tacc + u0, vg);
+      if (a.mp == 2) tmem_ld32(tacc + a.bw + u0, vu);
+      tmem_ld_wait();
+      uint32_t pz[16], pu[16], ph[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float z0 = valid ? __uint_as_float(vg[i]) : 0.f;
+        float z1 = valid ? __uint_as_float(vg[i + 1]) : 0.f;
+        float u0f = 0.f, u1f = 0.f;
+        if (a.mp == 2) {
+          u0f = valid ? __uint_as_float(vu[i]) : 0.f;
+          u1f = valid ? __uint_as_float(vu[i + 1]) : 0.f;
+          pu[i / 2] = pack_bf16(u0f, u1f);
+        }
+        pz[i / 2] = pack_bf16(z0, z1);
+        ph[i / 2] = pack_bf16(g * act_fwd(a.act, z0, u0f), g * act_fwd(a.act, z1, u1f));
+      }
+      uint4* zd = reinterpret_cast<uint4*>(zr + u0);
+      uint4* hd = reinterpret_cast<uint4*>(hr + u0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        zd[q] = make_uint4(pz[4 * q], pz[4 * q + 1], pz[4 * q + 2], pz[4 * q + 3]);
+        hd[q] = make_uint4(ph[4 * q], ph[4 * q + 1], ph[4 * q + 2], ph[4 * q + 3]);
+      }
+      if (a.mp == 2) {
+        uint4* ud = reinterpret_cast<uint4*>(zr + a.bw + u0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ud[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
+      }
+    }
+  } else if (KIND == K_FWD2 || KIND == K_DX) {
+    const int64_t prow = ti.prow0 + row;
+    __nv_bfloat16* dst = (__nv_bfloat16*)a.out + prow * (int64_t)a.d + ti.nt * 256;
+    const int ncols = min(256, a.d - ti.nt * 256);
+    for (int c0 = 0; c0 < ncols; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(tacc + c0, v);
+      tmem_ld_wait();
+      if (valid) {
+        uint32_t p[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          p[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) d4[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+      }
+    }
+  } else if (KIND == K_DA) {
+    const int64_t prow = ti.prow0 + row;
+    const float g = valid ? a.r.bucket_gate[ti.pos0 + row] : 0.f;
+    const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + prow * (int64_t)(a.mp * a.bw);
+    __nv_bfloat16* dzr = (__nv_bfloat16*)a.out2 + prow * (int64_t)(a.mp * a.bw);
+    float dgate = 0.f;
+    for (int u0 = 0; u0 < a.bw; u0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(tacc + u0, v);
+      tmem_ld_wait();
+      uint32_t zg4[16], zu4[16];
+      if (valid) {
+        const uint4* zs = reinterpret_cast<const uint4*>(zr + u0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 w = zs[q];
+          zg4[4 * q] = w.x; zg4[4 * q + 1] = w.y; zg4[4 * q + 2] = w.z; zg4[4 * q + 3] = w.w;
+        }
+        if (a.mp == 2) {
+          const uint4* us = reinterpret_cast<const uint4*>(zr + a.bw + u0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 w = us[q];
+            zu4[4 * q] = w.x; zu4[4 * q + 1] = w.y; zu4[4 * q + 2] = w.z; zu4[4 * q + 3] = w.w;
+          }
+        }
+      }
+      uint32_t pg[16], pu[16];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float dA = 0.f, zg = 0.f, zu = 0.f;
+        if (valid) {
+          dA = __uint_as_float(v[i]);
+          const uint32_t wg = zg4[i / 2];
+          zg = __uint_as_float((i & 1) ? (wg & 0xffff0000u) : (wg << 16));
+          if (a.mp == 2) {
+            const uint32_t wu = zu4[i / 2];
+            zu = __uint_as_float((i & 1) ? (wu & 0xffff0000u) : (wu << 16));
+          }
+        }
+        float av, dg, du;
+        act_fwd_bwd(a.act, zg, zu, av, dg, du);
+        dgate = fmaf(dA, av, dgate);
+        const float dzg = g * dA * dg, dzu = g * dA * du;
+        if (i & 1) {
+          pg[i / 2] |= (uint32_t)__bfloat16_as_ushort(__float2bfloat16(dzg)) << 16;
+          pu[i / 2] |= (uint32_t)__bfloat16_as_ushort(__float2bfloat16(dzu)) << 16;
+        } else {
+          pg[i / 2] = __bfloat16_as_ushort(__float2bfloat16(dzg));
+          pu[i / 2] = __bfloat16_as_ushort(__float2bfloat16(dzu));
+        }
+      }
+      uint4* d4 = reinterpret_cast<uint4*>(dzr + u0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d4[q] = make_uint4(pg[4 * q], pg[4 * q + 1], pg[4 * q + 2], pg[4 * q + 3]);
+      if (a.mp == 2) {
+        uint4* u4 = reinterpret_cast<uint4*>(dzr + a.bw + u0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u4[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
+      }
+    }
+    // dlogit = dgate * g (1 - g) = dgate * sigma(z) sigma(-z): no cancellation in 1 - g
+    float dlogit = 0.f;
+    int64_t t = 0;
+    if (valid && a.gate == SPT_GATE_SIGMOID) {
+      t = a.r.bucket_token[ti.pos0 + row];
+      const float z = a.r.logits[t * a.G + ti.b];
+      dlogit = dgate * sigmoid_pair(z);
+    }
+    a.rows_f[prow] = valid ? dgate : 0.f;
+    a.rows_g[prow] = dlogit;
+    if (valid && a.gate == SPT_GATE_SIGMOID) {
+      __nv_bfloat16* dl = (__nv_bfloat16*)a.dlg;
+      const __nv_bfloat16 hi = __float2bfloat16(dlogit);
+      const __nv_bfloat16 lo = __float2bfloat16(dlogit - __bfloat162float(hi));
+      dl[t * a.gpad + ti.b] = hi;
+      dl[(a.T + t) * a.gpad + ti.b] = lo;
+    }
+  } else if (KIND == K_DW1 || KIND == K_DW2 || KIND == K_DWR) {
+    // NOTE: tcgen05.ld is warp-collective (.sync.aligned): every lane executes
+    // the loads; only the stores are predicated on the row being real.
+    int64_t orow = 0;
+    bool live;
+    if (KIND == K_DWR) {  // split-K partial [split][G][d]
+      const int gb = ti.mt * 128 + row;
+      live = gb < a.G;
+      orow = (int64_t)ti.b * a.G + gb;
+    } else {
+      const int f = ti.mt * 128 + row;  // feature row within the block's m'*bw (or bw)
+      const int M = KIND == K_DW1 ? a.mp * a.bw : a.bw;
+      live = f < M;
+      if (KIND == K_DW1 && a.mp == 2)
+        orow = f < a.bw ? (int64_t)ti.b * a.bw + f : (int64_t)a.D + (int64_t)ti.b * a.bw + (f - a.bw);
+      else
+        orow = (int64_t)ti.b * a.bw + f;
+    }
+    float* dst = (float*)a.out + orow * a.d + ti.nt * 256;
+    const int ncols = min(256, a.d - ti.nt * 256);
+    const bool acc = KIND != K_DWR && a.acc_mode;
+    for (int c0 = 0; c0 < ncols; c0 += 32) {
+      uint32_t v[32];
+      if (ti.nkb > 0) {
+        tmem_ld32(tacc + c0, v);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0u;
+      }
+      if (!live) continue;
+      float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 o = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                               __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        if (acc) {
+          const float4 p = d4[q];
+          o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+        }
+        d4[q] = o;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcArgs a,
+                                                               int n_stages) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  constexpr bool kAmn = KIND == K_DW1 || KIND == K_DW2 || KIND == K_DWR;
+  constexpr bool kBmn = !(KIND == K_ROUTER || KIND == K_FWD1 || KIND == K_DA);
+  const int bstride = (b_bytes(KIND, a.BN) + 1023) & ~1023;
+  const int sstride = kABytes + bstride;
+  uint64_t* full = (uint64_t*)(smem + n_stages * sstride);
+  uint64_t* empty = full + n_stages;
+  uint64_t* tfull = empty + n_stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&a.ta);
+    tma_prefetch_desc(&a.tb);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ntiles = num_tiles<KIND>(a);
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t tx = stage_tx_bytes<KIND>(a);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const TileInfo ti = decode<KIND>(a, tile);
+      int rows4[4] = {0, 0, 0, 0};
+      if (KIND == K_FWD1 || KIND == K_DA) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = lane * 4 + i;
+          rows4[i] = rr < ti.n_valid ? a.r.bucket_token[ti.pos0 + rr] : (int)a.T;
+        }
+      }
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        if (lane == 0) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], tx);
+        }
+        __syncwarp();
+        uint8_t* sA = smem + stage * sstride;
+        produce_stage<KIND>(a, ti, kb, sA, sA + kABytes, &full[stage], lane, rows4);
+        if (++stage == n_stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    const uint32_t idesc = idesc_bf16(128, a.BN, kAmn, kBmn);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const TileInfo ti = decode<KIND>(a, tile);
+      if (lane == 0) {
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t dtm = tmem + acc * 256;
+        for (int kb = 0; kb < ti.nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * sstride);
+          const uint32_t sb = sa + kABytes;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = kAmn ? sdesc_sw128(sa + k * 2048, 8192, 1024)
+                                     : sdesc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = kBmn ? sdesc_sw128(sb + k * 2048, 8192, 1024)
+                                     : sdesc_sw128(sb + k * 32, 16, 1024);
+            mma_bf16(dtm, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == n_stages) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  } else {
+    // --------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const TileInfo ti = decode<KIND>(a, tile);
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      epilogue<KIND>(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, row);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ====================================================================== host
+static bool debug_sync() {  // SPT_FFN_DEBUG_SYNC=1: synchronise + report after each GEMM launch
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int KIND>
+static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
+  const int bst = (b_bytes(KIND, a.BN) + 1023) & ~1023;
+  const int sst = kABytes + bst;
+  const int budget = 227 * 1024 - 1024 - 256;
+  int stages = std::min(6, budget / sst);
+  const int smem = 1024 + stages * sst + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<KIND>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int grid = std::max(1, std::min(tiles_upper, num_sms()));
+  tc_gemm_kernel<KIND><<<grid, kThreads, smem, s>>>(a, stages);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (debug_sync()) {
+    e = cudaStreamSynchronize(s);
+    fprintf(stderr, "[spt] tc kind %d grid %d stages %d smem %d BN %d: %s\n", KIND, grid, stages,
+            smem, a.BN, cudaGetErrorString(e));
+  }
+  return e;
+}
+
+static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
+  a.r = r;
+  a.T = g.T;
+  a.G = g.G;
+  a.d = g.d;
+  a.D = g.D;
+  a.bw = g.bw;
+  a.mp = g.mp;
+  a.act = g.act;
+  a.gate = g.gate;
+  a.gpad = g.gpad;
+  a.NT = (int)ceil_div(g.d, 256);
+}
+
+static int bucket_tiles_upper(const Geom& g) { return (int)(ceil_div(g.pairs, 128) + g.G); }
+
+bool tc_supported(const Geom& g) {
+  if (g.d % 64) return false;
+  if (g.mp * g.bw > 256) return false;          // FWD1 N = m' * bw in one MMA
+  if (g.mp == 2 && g.bw % 64) return false;     // DX K stages must not straddle gate/up
+  if (g.gpad > 256) return false;
+  return true;
+}
+
+// tensor-map encode status is checked BEFORE the launch: a kernel must never
+// run with a map the driver rejected (its TMA loads would never complete)
+#define TRY(x)                                                                    \
+  do {                                                                            \
+    if (!ok) {                                                                    \
+      if (debug_sync()) fprintf(stderr, "[spt] tensor map encode failed (%s)\n", #x); \
+      return cudaErrorInvalidValue;                                               \
+    }                                                                             \
+    cudaError_t e_ = (x);                                                         \
+    if (e_ != cudaSuccess) return e_;                                             \
+  } while (0)
+
+cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logits,
+                      cudaStream_t s) {
+  TcArgs a{};
+  base_args(a, g, RouteView{});
+  bool ok = make_tmap_bf16_2d(&a.ta, x, g.T, g.d, g.d, 64, 128) &&
+            make_tmap_bf16_2d(&a.tb, w_r, g.G, g.d, g.d, 64, g.gpad);
+  a.BN = g.gpad;
+  a.out = logits;
+  TRY(launch<K_ROUTER>(a, (int)ceil_div(g.T, 128), s));
+  return cudaSuccess;
+}
+
+cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void* w2,
+                       const RouteView& r, void* y, const Bufs& b, cudaStream_t s) {
+  const int up = bucket_tiles_upper(g);
+  {
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, x, g.T, g.d, g.d, 64, 1) &&
+              make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, g.bw);
+    a.BN = g.mp * g.bw;
+    a.out = b.z;
+    a.out2 = b.h;
+    TRY(launch<K_FWD1>(a, up, s));
+  }
+  {
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, 128) &&
+              make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, 64);
+    a.BN = 256;
+    a.out = b.part;
+    TRY(launch<K_FWD2>(a, up * a.NT, s));
+  }
+  return launch_combine_fwd(g, r, b.part, y, s);
+}
+
+__global__ void dwr_reduce_kernel(int n_split, int64_t n, const float* __restrict__ part,
+                                  float* __restrict__ out, int acc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s = acc ? out[i] : 0.f;
+  for (int k = 0; k < n_split; ++k) s += part[k * n + i];
+  out[i] = s;
+}
+
+cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void* w2,
+                        const void* w_r, const RouteView& r, const void* dy, void* dx, float* dw1,
+                        float* dw2, float* dw_r, float* dgate_out, bool accumulate, const Bufs& b,
+                        cudaStream_t s) {
+  const int up = bucket_tiles_upper(g);
+  const bool sig = g.gate == SPT_GATE_SIGMOID;
+  if (sig && cudaMemsetAsync(b.dlg, 0, (size_t)2 * g.T * g.gpad * 2, s) != cudaSuccess)
+    return cudaErrorUnknown;
+  {  // a7: dA = dY[bucket] W2_b^T with the dgate / dZ / dlogit epilogue
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, dy, g.T, g.d, g.d, 64, 1) &&
+              make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, g.bw);
+    a.BN = g.bw;
+    a.aux = b.z;
+    a.out2 = b.dz;
+    a.rows_f = b.dgate;
+    a.rows_g = b.dlogit;
+    a.dlg = b.dlg;
+    TRY(launch<K_DA>(a, up, s));
+  }
+  {  // a8: dXp = dZ W1_b, then combine with the router term
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
+                                (uint64_t)g.mp * g.bw, 64, 128) &&
+              make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, 64);
+    a.BN = 256;
+    a.out = b.part;
+    TRY(launch<K_DX>(a, up * a.NT, s));
+  }
+  cudaError_t e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
+  if (e != cudaSuccess) return e;
+  {  // a9: dW1_b = dZ_b^T X[bucket_b]
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
+                                (uint64_t)g.mp * g.bw, 64, 64) &&
+              make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 1);
+    a.BN = 256;
+    a.MT = (int)ceil_div(g.mp * g.bw, 128);
+    a.out = dw1;
+    a.acc_mode = accumulate;
+    TRY(launch<K_DW1>(a, g.G * a.MT * a.NT, s));
+  }
+  {  // a9: dW2_b = H~_b^T dY[bucket_b]
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, 64) &&
+              make_tmap_bf16_2d(&a.tb, dy, g.T, g.d, g.d, 64, 1);
+    a.BN = 256;
+    a.MT = (int)ceil_div(g.bw, 128);
+    a.out = dw2;
+    a.acc_mode = accumulate;
+    TRY(launch<K_DW2>(a, g.G * a.MT * a.NT, s));
+  }
+  // a10: dW_R = dLogits^T X  (split-K, hi + lo bf16 halves of dlogit)
+  if (sig) {
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, b.dlg, (uint64_t)2 * g.T, g.gpad, g.gpad, 64, 64) &&
+              make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 64);
+    a.BN = 256;
+    a.MT = (int)ceil_div(g.G, 128);
+    a.n_split = b.n_split;
+    a.ksplit = (int)(ceil_div(ceil_div(g.T, b.n_split), 64) * 64);
+    a.out = b.dwr_part;
+    TRY(launch<K_DWR>(a, a.MT * a.NT * a.n_split, s));
+    const int64_t n = (int64_t)g.G * g.d;
+    dwr_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(b.n_split, n, b.dwr_part, dw_r,
+                                                                 accumulate ? 1 : 0);
+    count_launch();
+  } else if (!accumulate) {
+    if (cudaMemsetAsync(dw_r, 0, (size_t)g.G * g.d * 4, s) != cudaSuccess) return cudaErrorUnknown;
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (dgate_out) return launch_gather_dgate(g, r, b.dgate, dgate_out, s);
+  return cudaSuccess;
+}
+
+}  // namespace spt

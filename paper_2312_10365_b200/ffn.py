@@ -1,0 +1,135 @@
+"""Thin Python binding of the routed-FFN C ABI (include/spt_ffn.h).
+
+Same names as the C entry points; argument marshalling only (torch tensors ->
+device pointers, current CUDA stream).  Every step of the path runs in
+libspt_ffn.so's sm_100a kernels.  PyTorch supplies device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+
+_DT = {torch.float32: L.SPT_F32, torch.bfloat16: L.SPT_BF16}
+
+
+def make_desc(T: int, d: int, D: int, G: int, k: int, dtype: torch.dtype, act: int,
+              gate: int = L.SPT_GATE_SIGMOID) -> L.spt_ffn_desc:
+    if dtype not in _DT:
+        raise ValueError(f"unsupported dtype {dtype}")
+    return L.spt_ffn_desc(int(T), int(d), int(D), int(G), int(k), _DT[dtype], int(act), int(gate))
+
+
+def spt_ffn_sizes(desc: L.spt_ffn_desc) -> tuple[int, int]:
+    """(stash_bytes, workspace_bytes) for ``desc``."""
+    s, w = ctypes.c_size_t(), ctypes.c_size_t()
+    L.check("spt_ffn_sizes", L.lib().spt_ffn_sizes(ctypes.byref(desc), ctypes.byref(s), ctypes.byref(w)))
+    return s.value, w.value
+
+
+def _p(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libspt_ffn takes device tensors only")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+@dataclass
+class RouteBuffers:
+    """Device buffers of spt_route_buf (caller-owned)."""
+    logits: torch.Tensor        # [T, G] f32
+    topk_idx: torch.Tensor      # [T, k] i32
+    topk_gate: torch.Tensor     # [T, k] f32
+    block_offsets: torch.Tensor # [G+1] i32
+    bucket_token: torch.Tensor  # [T*k] i32
+    bucket_gate: torch.Tensor   # [T*k] f32
+    pair_slot: torch.Tensor     # [T*k] i32
+    tile_offsets: torch.Tensor  # [G+1] i32
+
+    @staticmethod
+    def empty(T: int, G: int, k: int, device="cuda") -> "RouteBuffers":
+        f, i = dict(dtype=torch.float32, device=device), dict(dtype=torch.int32, device=device)
+        return RouteBuffers(torch.empty(T, G, **f), torch.empty(T, k, **i), torch.empty(T, k, **f),
+                            torch.empty(G + 1, **i), torch.empty(T * k, **i), torch.empty(T * k, **f),
+                            torch.empty(T * k, **i), torch.empty(G + 1, **i))
+
+    def as_c(self) -> L.spt_route_buf:
+        return L.spt_route_buf(*[self.__dict__[n].data_ptr() for n, _ in L.spt_route_buf._fields_])
+
+
+def spt_ffn_route(desc, x, w_r, route: RouteBuffers, ws: torch.Tensor, flags: int = 0, stream=None):
+    rb = route.as_c()
+    L.check("spt_ffn_route", L.lib().spt_ffn_route(
+        ctypes.byref(desc), _p(x), _p(w_r), flags, ctypes.byref(rb), _p(ws), ws.numel() * ws.element_size(),
+        _stream(stream)))
+
+
+def spt_ffn_forward(desc, x, w1, w2, route: RouteBuffers, y, stash, ws, stream=None):
+    rb = route.as_c()
+    L.check("spt_ffn_forward", L.lib().spt_ffn_forward(
+        ctypes.byref(desc), _p(x), _p(w1), _p(w2), ctypes.byref(rb), _p(y), _p(stash), _p(ws),
+        ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def spt_ffn_backward(desc, x, w1, w2, w_r, route: RouteBuffers, stash, dy, dx, dw1, dw2, dw_r,
+                     ws, dgate=None, flags: int = 0, stream=None):
+    rb = route.as_c()
+    L.check("spt_ffn_backward", L.lib().spt_ffn_backward(
+        ctypes.byref(desc), _p(x), _p(w1), _p(w2), _p(w_r), ctypes.byref(rb), _p(stash), _p(dy), _p(dx),
+        _p(dw1), _p(dw2), _p(dw_r), _p(dgate), flags, _p(ws), ws.numel() * ws.element_size(),
+        _stream(stream)))
+
+
+def spt_status_string(code: int) -> str:
+    return L.status_string(code)
+
+
+def launch_count() -> int:
+    return int(L.lib().spt_ffn_launch_count())
+
+
+class RoutedFFN:
+    """Buffers for one routed-FFN layer shape (a convenience owner of memory;
+    the three methods are the ABI calls)."""
+
+    def __init__(self, T, d, D, G, k, dtype, act, gate=L.SPT_GATE_SIGMOID, device="cuda"):
+        self.desc = make_desc(T, d, D, G, k, dtype, act, gate)
+        self.T, self.d, self.D, self.G, self.k = T, d, D, G, k
+        self.dtype, self.act, self.gate = dtype, act, gate
+        self.mp = 2 if act == L.SPT_ACT_SWIGLU else 1
+        stash_b, ws_b = spt_ffn_sizes(self.desc)
+        self.stash = torch.empty(max(stash_b, 16), dtype=torch.uint8, device=device)
+        self.ws = torch.empty(max(ws_b, 16), dtype=torch.uint8, device=device)
+        self.route_buf = RouteBuffers.empty(T, G, k, device)
+        self.y = torch.empty(T, d, dtype=dtype, device=device)
+        self.dx = torch.empty(T, d, dtype=dtype, device=device)
+        w1_shape = (2, D, d) if self.mp == 2 else (D, d)
+        self.dw1 = torch.empty(w1_shape, dtype=torch.float32, device=device)
+        self.dw2 = torch.empty(D, d, dtype=torch.float32, device=device)
+        self.dw_r = torch.empty(G, d, dtype=torch.float32, device=device)
+        self.dgate = torch.empty(T, k, dtype=torch.float32, device=device)
+
+    def route(self, x, w_r, flags=0, stream=None):
+        spt_ffn_route(self.desc, x, w_r, self.route_buf, self.ws, flags, stream)
+        return self.route_buf
+
+    def forward(self, x, w1, w2, stream=None):
+        spt_ffn_forward(self.desc, x, w1, w2, self.route_buf, self.y, self.stash, self.ws, stream)
+        return self.y
+
+    def backward(self, x, w1, w2, w_r, dy, flags=0, want_dgate=False, stream=None):
+        spt_ffn_backward(self.desc, x, w1, w2, w_r, self.route_buf, self.stash, dy, self.dx, self.dw1,
+                         self.dw2, self.dw_r, self.ws, self.dgate if want_dgate else None, flags, stream)
+        return self.dx, self.dw1, self.dw2, self.dw_r

@@ -1,0 +1,92 @@
+"""The C ABI library loads, exports every symbol include/spt_ffn.h declares, and
+validates arguments on the host (CPU-only: no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "spt_ffn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(spt_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2312_10365_b200 import _lib
+    L = _lib.lib()
+    decl = _declared_symbols()
+    assert set(decl) == set(_lib.EXPORTED), decl
+    for name in decl:
+        assert hasattr(L, name), name
+    assert L.spt_ffn_abi_version() == 1
+
+
+def test_status_strings():
+    from paper_2312_10365_b200 import _lib
+    assert _lib.status_string(0) == "SPT_OK"
+    assert _lib.status_string(3) == "SPT_ERR_WORKSPACE_TOO_SMALL"
+    assert _lib.status_string(99) == "SPT_ERR_UNKNOWN"
+
+
+def _desc(**kw):
+    import torch
+    from paper_2312_10365_b200 import make_desc
+    a = dict(T=256, d=128, D=512, G=8, k=2, dtype=torch.float32, act=0, gate=0)
+    a.update(kw)
+    return make_desc(**a)
+
+
+def test_sizes_valid_and_monotone():
+    from paper_2312_10365_b200 import spt_ffn_sizes
+    s1, w1 = spt_ffn_sizes(_desc())
+    s2, w2 = spt_ffn_sizes(_desc(T=512))
+    assert s1 > 0 and w1 > 0 and s2 > s1 and w2 > w1
+    s0, w0 = spt_ffn_sizes(_desc(T=0))
+    assert s0 >= 0 and w0 >= 0
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(k=9), 1),            # k > G
+    (dict(k=0), 1),
+    (dict(D=500), 1),          # D % G != 0
+    (dict(T=-1), 1),
+    (dict(d=0), 1),
+    (dict(act=7), 1),
+    (dict(gate=5), 1),
+    (dict(G=512, D=512 * 16, k=2), 2),   # G > 256
+    (dict(d=96), 2),                     # d % 64
+    (dict(D=8 * 24), 2),                 # bw = 24, not a multiple of 16
+])
+def test_invalid_descriptors(kw, code):
+    from paper_2312_10365_b200 import _lib, spt_ffn_sizes
+    with pytest.raises(_lib.SptError) as e:
+        spt_ffn_sizes(_desc(**kw))
+    assert e.value.code == code
+
+
+def test_null_pointers_rejected_before_any_launch():
+    from paper_2312_10365_b200 import _lib
+    L = _lib.lib()
+    d = _desc()
+    rb = _lib.spt_route_buf()
+    assert L.spt_ffn_route(ctypes.byref(d), None, None, 0, ctypes.byref(rb), None, 0, None) == 1
+    assert L.spt_ffn_forward(ctypes.byref(d), None, None, None, ctypes.byref(rb), None, None,
+                             None, 0, None) == 1
+    assert L.spt_ffn_backward(ctypes.byref(d), *([None] * 4), ctypes.byref(rb), *([None] * 7),
+                              0, None, 0, None) == 1
+    s = ctypes.c_size_t()
+    assert L.spt_ffn_sizes(None, ctypes.byref(s), ctypes.byref(s)) == 1
+    assert L.spt_ffn_sizes(ctypes.byref(d), None, ctypes.byref(s)) == 1
+
+
+def test_workspace_too_small_rejected():
+    from paper_2312_10365_b200 import _lib
+    L = _lib.lib()
+    d = _desc()
+    fake = ctypes.c_void_p(16)  # never dereferenced: size check precedes any launch
+    rb = _lib.spt_route_buf(*([16] * 8))
+    assert L.spt_ffn_route(ctypes.byref(d), fake, fake, 0, ctypes.byref(rb), fake, 1, None) == 3

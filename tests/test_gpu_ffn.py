@@ -1,0 +1,127 @@
+"""GPU parity of the routed-FFN forward and backward against the fp64 oracle.
+
+Inputs: synthetic seeded tensors (synthetic/).  Routing: either the GPU's own
+router (then the oracle is given the same top-k, which test_gpu_route checks
+bit-exactly) or fixed generator logits via SPT_ROUTE_LOGITS_IN.  Error metric:
+infinity-norm relative error (reading c14), bound 1e-4 fp32 / 2e-2 bf16
+(BASELINE.json north_star).  Sizes span several 128-row tiles and ragged
+tails; full BASELINE sizes are covered by sampled rows/blocks in
+test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+
+import synthetic as S
+from helpers import TOL, gpu_run, oracle_run, relerr
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ("y", "dx", "dw1", "dw2", "dw_r", "dgate")
+
+
+def _check(cfg, got, ref, names=NAMES, tol=None):
+    tol = TOL[cfg.dtype] if tol is None else tol
+    errs = {}
+    for n in names:
+        if n == "dw_r" and cfg.gate == S.GATE_NONE:
+            assert np.all(got[n] == 0), "GATE_NONE: router gets no gradient"
+            continue
+        errs[n] = relerr(got[n], ref[n])
+    bad = {n: e for n, e in errs.items() if not e <= tol}
+    assert not bad, f"{cfg.name}: {errs}"
+    return errs
+
+
+def _parity(orc, cfg, T, kind=None, names=NAMES):
+    inp = S.make_inputs(cfg, T)
+    logits = None if kind is None else S.make_logits(T, cfg.G, cfg.k, kind, seed=cfg.seed)
+    got = gpu_run(cfg, T, inp, logits_in=logits)
+    lg = logits.astype(np.float64) if logits is not None else orc.router(inp["x"], inp["w_r"])
+    # the GPU's selection (checked bit-exact against the oracle's top-k in test_gpu_route)
+    assert np.array_equal(got["topk_idx"], orc.topk(got["logits"], cfg.k))
+    ref = oracle_run(orc, cfg, inp, lg, got["topk_idx"])
+    return _check(cfg, got, ref, names)
+
+
+@pytest.mark.parametrize("gate", [S.GATE_SIGMOID, S.GATE_NONE])
+@pytest.mark.parametrize("T", [256, 1, 131, 1000])
+def test_tiny_fp32(orc, T, gate):
+    _parity(orc, S.CONFIGS["tiny"].with_(gate=gate), T)
+
+
+@pytest.mark.parametrize("kind", ["normal", "zipf", "same", "ties"])
+def test_tiny_fixed_logits(orc, kind):
+    _parity(orc, S.CONFIGS["tiny"], 700, kind=kind)
+
+
+@pytest.mark.parametrize("act", [S.ACT_RELU, S.ACT_GELU, S.ACT_SWIGLU])
+def test_fp32_all_activations(orc, act):
+    cfg = S.CONFIGS["tiny"].with_(act=act, name=f"tiny-act{act}")
+    _parity(orc, cfg, 333)
+
+
+@pytest.mark.parametrize("name,T", [("bert", 1000), ("opt", 600), ("llama", 300)])
+def test_bf16_configs(orc, name, T):
+    _parity(orc, S.CONFIGS[name], T)
+
+
+@pytest.mark.parametrize("name", ["bert", "opt", "llama"])
+def test_bf16_gate_none(orc, name):
+    _parity(orc, S.CONFIGS[name].with_(gate=S.GATE_NONE), 257)
+
+
+@pytest.mark.parametrize("kind", ["zipf", "same"])
+def test_bf16_skewed_buckets(orc, kind):
+    """Skewed / degenerate bucket sizes: empty buckets and k buckets of size T."""
+    _parity(orc, S.CONFIGS["opt"], 700, kind=kind)
+
+
+def test_k_equals_G_is_dense(orc):
+    cfg = S.FfnConfig("kG", 128, 512, 4, 4, 300, "bf16", S.ACT_SWIGLU)
+    _parity(orc, cfg, 300)
+
+
+def test_k1_bf16(orc):
+    cfg = S.FfnConfig("k1", 256, 2048, 16, 1, 400, "bf16", S.ACT_GELU)
+    _parity(orc, cfg, 400)
+
+
+def test_empty_batch():
+    import torch
+    import paper_2312_10365_b200 as P
+    f = P.RoutedFFN(0, 128, 512, 8, 2, torch.float32, P.SPT_ACT_RELU)
+    x = torch.empty(0, 128, device="cuda")
+    w1 = torch.randn(512, 128, device="cuda")
+    w2 = torch.randn(512, 128, device="cuda")
+    w_r = torch.randn(8, 128, device="cuda")
+    f.route(x, w_r)
+    f.forward(x, w1, w2)
+    f.dw1.fill_(7)
+    f.backward(x, w1, w2, w_r, x)
+    torch.cuda.synchronize()
+    assert f.route_buf.block_offsets.cpu().tolist() == [0] * 9
+    assert float(f.dw1.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("name", ["tiny", "bert"])
+def test_accumulate_dw(orc, name):
+    cfg = S.CONFIGS[name]
+    T = 300
+    inp = S.make_inputs(cfg, T)
+    base = gpu_run(cfg, T, inp)
+    rng = np.random.default_rng(0)
+    prior = {n: rng.standard_normal(base[n].shape).astype(np.float32) for n in ("dw1", "dw2", "dw_r")}
+    acc = gpu_run(cfg, T, inp, accumulate_from=prior)
+    for n in ("dw1", "dw2", "dw_r"):
+        assert relerr(acc[n] - prior[n], base[n]) < 1e-5
+
+
+@pytest.mark.parametrize("name", ["tiny", "llama"])
+def test_deterministic(orc, name):
+    cfg = S.CONFIGS[name]
+    T = 513
+    inp = S.make_inputs(cfg, T)
+    a = gpu_run(cfg, T, inp)
+    b = gpu_run(cfg, T, inp)
+    for n in NAMES + ("logits", "bucket_token"):
+        assert np.array_equal(a[n], b[n]), n
