@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark of the SPT routed FFN (arXiv 2312.10365) on B200.
+
+One "step" = the whole hot path of SURVEY §8(a) over one batch of synthetic
+tokens resident in HBM: route (router GEMM, top-k, bucketing) -> forward
+(gather-fused grouped GEMMs + combine) -> backward (dA/dZ, dX, dW1, dW2, dW_R)
+-> (N > 1) one NCCL SUM all-reduce of the flat fp32 weight gradients.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama_scale]
+  python bench.py --impl reference ...     (the CPU oracle as the reference arm)
+
+Default workload: BASELINE.json configs[4] "LLaMA-7B FFN token-sharded scaling
+run ... seq 4096" -- d=4096, D=11008 (SwiGLU), G=86, k=22, 8 x 4096 tokens per
+GPU (weak scaling), bf16 storage / fp32 accumulate, random-init weights and
+random tokens ("Random" workload).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synthetic as S  # noqa: E402
+
+METRIC = "routed-FFN fwd+bwd tokens/s at 1/2/4/8 B200; tensor-pipe % of bf16 peak"
+UNIT = "tokens/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16": d["bf16_tflops"],
+                "bf16_sustained": d["bf16_tflops_sustained"], "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0,
+            "src": "fallback (B200_PROFILING.md)"}
+
+
+# --------------------------------------------------------------- work model
+def kernel_work(cfg, T):
+    """Algorithmic FLOPs (tensor kernels) or bytes (HBM kernels) per launch,
+    per SURVEY §8(d): GEMM work counts only activated blocks."""
+    P = T * cfg.k
+    mp, bw, d, G = cfg.mprime, cfg.bw, cfg.d, cfg.G
+    e = 2 if cfg.dtype == "bf16" else 4
+    return {
+        "tc_router": ("tensor", 2.0 * T * d * G),
+        "tc_fwd1_gate_up": ("tensor", 2.0 * P * mp * bw * d),
+        "tc_fwd2_down": ("tensor", 2.0 * P * bw * d),
+        "tc_bwd_dA": ("tensor", 2.0 * P * bw * d),
+        "tc_bwd_dX": ("tensor", 2.0 * P * mp * bw * d),
+        "tc_bwd_dW1": ("tensor", 2.0 * P * mp * bw * d),
+        "tc_bwd_dW2": ("tensor", 2.0 * P * bw * d),
+        "tc_bwd_dWR": ("tensor", 2.0 * P * d),
+        "combine_fwd": ("hbm", P * d * e + 8.0 * P + T * d * e),
+        "combine_bwd": ("hbm", P * d * e + 12.0 * P + T * d * e),
+        "topk_hist": ("hbm", 4.0 * T * G + 8.0 * T * cfg.k),
+        "bucket_scatter": ("hbm", 20.0 * P),
+    }
+
+
+def step_gemm_flops(cfg, T):
+    """fwd 2(m'+1) d bw k + bwd 2x that, per token, + router 6 d G."""
+    per_tok = 2.0 * (cfg.mprime + 1) * cfg.d * cfg.bw * cfg.k * 3 + 6.0 * cfg.d * cfg.G
+    return per_tok * T
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception as ex:  # nvidia-smi missing: report no clocks
+            log("clock sampler unavailable:", ex)
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append((float(p[1]), float(p[2]), p[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i in range(4) if r[i].lower() == "active"})
+        sm = [r[0] for r in rows]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in rows),
+                "sm_mhz_min": min(sm), "samples": len(rows), "reasons": reasons}
+
+
+# ----------------------------------------------------------------- oracle
+def oracle_sample(cfg, n_tok):
+    """The CPU oracle (as it stands) over route + fwd + bwd of `n_tok` tokens of
+    the workload; returns (seconds, threads)."""
+    import oracle
+    inp = S.make_inputs(cfg, n_tok)
+    t = time.perf_counter()
+    lg = oracle.router(inp["x"], inp["w_r"])
+    ti = oracle.topk(lg.astype(np.float32), cfg.k)
+    oracle.bucket(ti, cfg.G)
+    oracle.forward(inp["x"], inp["w1"], inp["w2"], lg, ti, cfg.act, cfg.gate)
+    oracle.backward(inp["x"], inp["w1"], inp["w2"], inp["w_r"], lg, ti, inp["dy"], cfg.act, cfg.gate)
+    return time.perf_counter() - t, oracle.max_threads()
+
+
+def cpu_baseline(cfg, target_s=15.0):
+    t0, _ = oracle_sample(cfg, 16)
+    n = int(max(16, min(4096, 16 * target_s / max(t0, 1e-3))))
+    secs, cores = oracle_sample(cfg, n)
+    return {"value": n / secs, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} tokens of {cfg.name} (route+fwd+bwd, all {cfg.G} blocks' dW), "
+                      f"{secs:.1f} s, fp64 C oracle, OpenMP"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    t0, _ = oracle_sample(cfg, 8)
+    budget = 150.0 / max(1, args.steps + args.warmup)          # seconds per step
+    n = int(max(8, min(2048, 8 * budget / max(t0, 1e-3))))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, n)
+    tot, cores = 0.0, 1
+    for _ in range(args.steps):
+        s, cores = oracle_sample(cfg, n)
+        tot += s
+    value = n * args.steps / tot
+    sample = f"{n} tokens of {cfg.name} per step (route+fwd+bwd, fp64 C oracle, OpenMP)"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(cfg, args.gpus, cfg.T),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def workload_config(cfg, world, T):
+    return {"workload": f"{cfg.name}: routed FFN d={cfg.d} D={cfg.D} G={cfg.G} k={cfg.k} bw={cfg.bw} "
+                        f"act={['relu', 'gelu', 'swiglu'][cfg.act]} "
+                        f"gate={['sigmoid', 'none'][cfg.gate]}, {T} tokens per GPU",
+            "tokens_per_gpu": T, "global_tokens": T * world, "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (x, dy %.0f MB each; weights %.0f MB)" % (
+                T * cfg.d * (2 if cfg.dtype == 'bf16' else 4) / 1e6,
+                (cfg.mprime + 1) * cfg.D * cfg.d * (2 if cfg.dtype == 'bf16' else 4) / 1e6)}
+
+
+# ------------------------------------------------------------------- ours
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama_scale", choices=sorted(S.CONFIGS))
+    ap.add_argument("--tokens", type=int, default=0, help="override tokens per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    args = ap.parse_args()
+    cfg = S.CONFIGS[args.config]
+    if args.tokens:
+        cfg = cfg.with_(T=args.tokens)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_10365_b200 as P
+    from paper_2312_10365_b200 import dp
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    T = cfg.T
+    dt = torch.float32 if cfg.dtype == "f32" else torch.bfloat16
+    t_gen = time.time()
+    inp = S.make_inputs(cfg, T, token_offset=rank * ((T + 1023) // 1024) * 1024)
+    log(f"[rank {rank}] inputs generated in {time.time() - t_gen:.1f}s")
+    dev = {n: torch.from_numpy(inp[n]).to(dt).cuda() for n in ("x", "w1", "w2", "w_r", "dy")}
+    del inp
+    x, w1, w2, w_r, dy = (dev[n] for n in ("x", "w1", "w2", "w_r", "dy"))
+    f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, dt, cfg.act, cfg.gate)
+    fg = dp.attach_flat_grads(f)
+
+    def step():
+        f.route(x, w_r)
+        f.forward(x, w1, w2)
+        f.backward(x, w1, w2, w_r, dy)
+        dp.allreduce_grads(fg)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    n0 = P.launch_count()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = P.launch_count() - n0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_max = dp.max_over_ranks(ms, device="cuda")
+    value = T * world / (ms_max / 1e3)
+
+    # ---- per-kernel device times (CUDA events around each library launch)
+    prof = {}
+    if not args.no_profile:
+        P.profile_enable(True)
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        prof = P.profile_read()
+        P.profile_enable(False)
+    clocks = sampler.stop()
+
+    # ---- end to end through the public API, host buffers
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty_like(x, device="cpu").pin_memory()
+        dyh = torch.empty_like(dy, device="cpu").pin_memory()
+        xh.copy_(x)
+        dyh.copy_(dy)
+        yh = torch.empty_like(x, device="cpu").pin_memory()
+        dxh = torch.empty_like(x, device="cpu").pin_memory()
+
+        def e2e_step():
+            x.copy_(xh, non_blocking=True)
+            dy.copy_(dyh, non_blocking=True)
+            step()
+            yh.copy_(f.y, non_blocking=True)
+            dxh.copy_(f.dx, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        k2 = max(3, args.steps // 3)
+        ev0.record(stream)
+        for _ in range(k2):
+            e2e_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms_e = dp.max_over_ranks(ev0.elapsed_time(ev1) / k2, device="cuda")
+        nb = x.numel() * x.element_size()
+        e2e = {"value": T * world / (ms_e / 1e3), "unit": UNIT, "ms_per_step": ms_e,
+               "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
+               "what": "H2D x, dy from pinned host + route/fwd/bwd(+allreduce) + D2H y, dx to pinned host"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    pk = peaks()
+    work = kernel_work(cfg, T)
+    kernels = {}
+    for name, (cnt, tot) in prof.items():
+        per = tot / max(cnt, 1)
+        kernels[name] = {"launches_per_step": cnt / args.steps, "ms_per_launch": per}
+        if name in work:
+            kind, amt = work[name]
+            if kind == "tensor":
+                kernels[name]["tflops"] = amt / (per / 1e3) / 1e12
+            else:
+                kernels[name]["gbs"] = amt / (per / 1e3) / 1e9
+    roofline = None
+    if prof:
+        step_ms_prof = sum(t for _, t in prof.values()) / args.steps
+        dom = max(prof, key=lambda n: prof[n][1])
+        cnt, tot = prof[dom]
+        per = tot / cnt
+        kind, amt = work.get(dom, ("tensor", 0.0))
+        if kind == "tensor":
+            ach = amt / (per / 1e3) / 1e12
+            roofline = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk["bf16_sustained"],
+                        "unit": "TFLOP/s", "frac": ach / pk["bf16_sustained"], "traffic": None,
+                        "peak_src": pk["src"] + " bf16 sustained",
+                        "algorithmic_per_launch": amt, "ms_per_launch": per,
+                        "share_of_step": tot / args.steps / step_ms_prof}
+        else:
+            ach = amt / (per / 1e3) / 1e9
+            roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": ach / pk["hbm_gbs"], "traffic": None, "peak_src": pk["src"],
+                        "algorithmic_per_launch": amt, "ms_per_launch": per,
+                        "share_of_step": tot / args.steps / step_ms_prof}
+    step_tf = step_gemm_flops(cfg, T) / (ms_max / 1e3) / 1e12
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded random tokens and weights)",
+        "config": workload_config(cfg, world, T),
+        "tensor_pipe_frac_of_bf16_peak": {"step_gemm_tflops": step_tf, "peak": pk["bf16_sustained"],
+                                          "frac": step_tf / pk["bf16_sustained"],
+                                          "peak_src": pk["src"] + " bf16 sustained"},
+        "roofline": roofline, "kernels": kernels, "gpu_launches": launches, "clocks": clocks, "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(cfg)
+        except Exception as ex:  # oracle build failure must not hide the GPU number
+            out["cpu_baseline"] = {"error": str(ex)}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -145,6 +145,15 @@ int spt_ffn_abi_version(void);
  * (host-side counter, for the benchmark's gpu_launches report). */
 uint64_t spt_ffn_launch_count(void);
 
+/* Optional instrumentation: when enabled, every kernel the library launches is
+ * bracketed by a pair of CUDA events on its launch stream (small overhead).
+ * spt_ffn_profile_enable(1) clears previous records; spt_ffn_profile_read
+ * waits for the recorded events, writes "name count total_ms\n" lines (one per
+ * kernel name, first-launch order, NUL-terminated, truncated to len) into buf,
+ * clears the records and returns the full text length (or -1 on a CUDA error). */
+spt_status spt_ffn_profile_enable(int on);
+int64_t spt_ffn_profile_read(char* buf, size_t len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,8 @@ SPT_TILE_M = 128
 
 # every symbol include/spt_ffn.h declares
 EXPORTED = ("spt_ffn_sizes", "spt_ffn_route", "spt_ffn_forward", "spt_ffn_backward",
-            "spt_status_string", "spt_ffn_abi_version", "spt_ffn_launch_count")
+            "spt_status_string", "spt_ffn_abi_version", "spt_ffn_launch_count",
+            "spt_ffn_profile_enable", "spt_ffn_profile_read")
 
 
 class spt_ffn_desc(ctypes.Structure):
@@ -65,6 +66,10 @@ def lib() -> ctypes.CDLL:
         L.spt_status_string.restype = ctypes.c_char_p
         L.spt_ffn_abi_version.restype = ctypes.c_int
         L.spt_ffn_launch_count.restype = ctypes.c_uint64
+        L.spt_ffn_profile_enable.argtypes = [ctypes.c_int]
+        L.spt_ffn_profile_enable.restype = ctypes.c_int
+        L.spt_ffn_profile_read.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
+        L.spt_ffn_profile_read.restype = ctypes.c_int64
         _lib = L
     return _lib
 

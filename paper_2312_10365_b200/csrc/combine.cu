@@ -107,12 +107,14 @@ __global__ void __launch_bounds__(128) combine_kernel(int64_t T, int d, int k, R
 
 cudaError_t launch_combine_fwd(const Geom& g, const RouteView& r, const void* part, void* y,
                                cudaStream_t s) {
+  prof_begin("combine_fwd", s);
   if (g.dtype == SPT_BF16)
     combine_kernel<__nv_bfloat16, false><<<(unsigned)g.T, 128, 0, s>>>(
         g.T, g.d, g.k, r, (const __nv_bfloat16*)part, nullptr, nullptr, (__nv_bfloat16*)y);
   else
     combine_kernel<float, false><<<(unsigned)g.T, 128, 0, s>>>(g.T, g.d, g.k, r, (const float*)part,
                                                                nullptr, nullptr, (float*)y);
+  prof_end(s);
   count_launch();
   return cudaGetLastError();
 }
@@ -121,6 +123,7 @@ cudaError_t launch_combine_bwd(const Geom& g, const RouteView& r, const void* pa
                                const float* dlogit, const void* w_r, void* dx, cudaStream_t s) {
   // GATE_NONE: dlogit == 0, the router term vanishes (no gradient path, reading c2)
   const void* wr = g.gate == SPT_GATE_SIGMOID ? w_r : nullptr;
+  prof_begin("combine_bwd", s);
   if (g.dtype == SPT_BF16)
     combine_kernel<__nv_bfloat16, true><<<(unsigned)g.T, 128, 0, s>>>(
         g.T, g.d, g.k, r, (const __nv_bfloat16*)part, dlogit, (const __nv_bfloat16*)wr,
@@ -128,6 +131,7 @@ cudaError_t launch_combine_bwd(const Geom& g, const RouteView& r, const void* pa
   else
     combine_kernel<float, true><<<(unsigned)g.T, 128, 0, s>>>(
         g.T, g.d, g.k, r, (const float*)part, dlogit, (const float*)wr, (float*)dx);
+  prof_end(s);
   count_launch();
   return cudaGetLastError();
 }
@@ -141,8 +145,10 @@ __global__ void gather_dgate_kernel(int64_t T, int k, RouteView r, const float* 
 
 cudaError_t launch_gather_dgate(const Geom& g, const RouteView& r, const float* dgate_rows,
                                 float* dgate_out, cudaStream_t s) {
+  prof_begin("gather_dgate", s);
   gather_dgate_kernel<<<(unsigned)ceil_div(g.pairs, 256), 256, 0, s>>>(g.T, g.k, r, dgate_rows,
                                                                        dgate_out);
+  prof_end(s);
   count_launch();
   return cudaGetLastError();
 }

@@ -56,6 +56,9 @@ struct Bufs {
 };
 
 void count_launch(int n = 1);
+// optional per-kernel CUDA-event profiling (spt_ffn_profile_enable / _read)
+void prof_begin(const char* name, cudaStream_t s);
+void prof_end(cudaStream_t s);
 
 // routing (route.cu)
 cudaError_t launch_router_simt(const Geom& g, const void* x, const void* w_r, float* logits,

@@ -46,12 +46,14 @@ cudaError_t launch_router_simt(const Geom& g, const void* x, const void* w_r, fl
                                cudaStream_t s) {
   const int warps = 8;
   dim3 grid((unsigned)ceil_div(g.T, warps));
+  prof_begin("router_simt", s);
   if (g.dtype == SPT_F32)
     router_simt_kernel<float><<<grid, warps * 32, 0, s>>>(g.T, g.d, g.G, (const float*)x,
                                                            (const float*)w_r, logits);
   else
     router_simt_kernel<__nv_bfloat16><<<grid, warps * 32, 0, s>>>(
         g.T, g.d, g.G, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w_r, logits);
+  prof_end(s);
   count_launch();
   return cudaGetLastError();
 }
@@ -227,12 +229,18 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
 
 cudaError_t launch_topk_bucket(const Geom& g, const RouteView& r, const Bufs& b, cudaStream_t s) {
   const unsigned nch = (unsigned)g.n_chunks;
+  prof_begin("topk_hist", s);
   topk_hist_kernel<<<nch, 256, 0, s>>>(g.T, g.G, g.k, g.gate, r.logits, r.topk_idx, r.topk_gate,
                                        b.chunk_counts);
+  prof_end(s);
+  prof_begin("bucket_scan", s);
   bucket_scan_kernel<<<g.G, 256, 0, s>>>(g.n_chunks, g.G, b.chunk_counts, b.chunk_base, b.n_b);
+  prof_end(s);
+  prof_begin("bucket_scatter", s);
   bucket_scatter_kernel<<<nch, 256, 0, s>>>(g.T, g.G, g.k, b.n_b, b.chunk_base, r.topk_idx,
                                             r.topk_gate, r.block_offsets, r.tile_offsets,
                                             r.bucket_token, r.bucket_gate, r.pair_slot);
+  prof_end(s);
   count_launch(3);
   return cudaGetLastError();
 }

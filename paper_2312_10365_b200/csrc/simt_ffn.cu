@@ -313,10 +313,16 @@ cudaError_t fwd_impl(const Geom& g, const T* x, const T* w1, const T* w2, const 
                      const Bufs& b, cudaStream_t s) {
   const unsigned tiles64 = (unsigned)((ceil_div(g.pairs, kTileM) + g.G) * (kTileM / 64));
   OpZ<T> oz{r, x, w1, (T*)b.z, g.d, g.D, g.bw, g.mp};
+  prof_begin("simt_f1", s);
   k_f1<T><<<dim3(tiles64, (unsigned)ceil_div(g.mp * g.bw, 64)), 256, 0, s>>>(oz, g.G);
+  prof_end(s);
+  prof_begin("simt_f1b", s);
   k_f1b<T><<<tiles64, 256, 0, s>>>(r, g.G, g.bw, g.mp, g.act, (const T*)b.z, (T*)b.h);
+  prof_end(s);
   OpP<T> op{(const T*)b.h, w2, (T*)b.part, g.d, g.bw};
+  prof_begin("simt_f2", s);
   k_f2<T><<<dim3(tiles64, (unsigned)ceil_div(g.d, 64)), 256, 0, s>>>(op, r, g.G);
+  prof_end(s);
   count_launch(3);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -329,22 +335,34 @@ cudaError_t bwd_impl(const Geom& g, const T* x, const T* w1, const T* w2, const 
                      float* dgate_out, bool acc, const Bufs& b, cudaStream_t s) {
   const unsigned tiles64 = (unsigned)((ceil_div(g.pairs, kTileM) + g.G) * (kTileM / 64));
   OpDA<T> oda{r, dy, w2, b.da, g.d, g.bw};
+  prof_begin("simt_b1", s);
   k_b1<T><<<dim3(tiles64, (unsigned)ceil_div(g.bw, 64)), 256, 0, s>>>(oda, g.G);
+  prof_end(s);
+  prof_begin("simt_b1b", s);
   k_b1b<T><<<tiles64, 256, 0, s>>>(r, g.G, g.bw, g.mp, g.act, g.gate, (const T*)b.z, b.da,
                                    (T*)b.dz, b.dgate, b.dlogit);
+  prof_end(s);
   OpDX<T> odx{(const T*)b.dz, w1, (T*)b.part, g.d, g.D, g.bw, g.mp};
+  prof_begin("simt_b2", s);
   k_b2<T><<<dim3(tiles64, (unsigned)ceil_div(g.d, 64)), 256, 0, s>>>(odx, r, g.G);
+  prof_end(s);
   count_launch(3);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if ((e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s)) != cudaSuccess) return e;
   const int M1 = g.mp * g.bw;
   OpDW<T> o1{r, (const T*)b.dz, x, dw1, g.d, g.D, g.bw, M1, acc ? 1 : 0, g.mp == 2 ? 1 : 0, 0};
+  prof_begin("simt_dw", s);
   k_dw<T><<<dim3((unsigned)ceil_div(M1, 64), (unsigned)ceil_div(g.d, 64), g.G), 256, 0, s>>>(o1);
+  prof_end(s);
   OpDW<T> o2{r, (const T*)b.h, dy, dw2, g.d, g.D, g.bw, g.bw, acc ? 1 : 0, 0, 0};
+  prof_begin("simt_dw", s);
   k_dw<T><<<dim3((unsigned)ceil_div(g.bw, 64), (unsigned)ceil_div(g.d, 64), g.G), 256, 0, s>>>(o2);
+  prof_end(s);
+  prof_begin("simt_dwr", s);
   k_dwr<T><<<dim3((unsigned)ceil_div(g.d, 128), g.G), 128, 0, s>>>(r, g.d, x, b.dlogit, dw_r,
                                                                   acc ? 1 : 0);
+  prof_end(s);
   count_launch(3);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (dgate_out) return launch_gather_dgate(g, r, b.dgate, dgate_out, s);

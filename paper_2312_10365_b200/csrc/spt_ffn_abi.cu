@@ -1,7 +1,12 @@
 // spt_ffn_abi.cu -- the C ABI of include/spt_ffn.h: validation, workspace
 // carving and dispatch to the sm_100a kernels.  Host code only.
 #include <atomic>
+#include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "internal.h"
 
@@ -9,6 +14,40 @@ namespace spt {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+// ---- per-kernel profiling: a pair of CUDA events around every launch, on the
+// launch stream; aggregated on read.  Off by default (zero overhead).
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_ev_pool;
+
+static cudaEvent_t ev_get() {
+  if (!g_ev_pool.empty()) {
+    cudaEvent_t e = g_ev_pool.back();
+    g_ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+void prof_begin(const char* name, cudaStream_t s) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> l(g_prof_mu);
+  ProfRec r{name, ev_get(), ev_get()};
+  cudaEventRecord(r.a, s);
+  g_prof.push_back(r);
+}
+void prof_end(cudaStream_t s) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> l(g_prof_mu);
+  if (!g_prof.empty()) cudaEventRecord(g_prof.back().b, s);
+}
 
 static inline size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
@@ -105,10 +144,15 @@ static RouteView view(const spt_route_buf* r) {
                    r->bucket_token, r->bucket_gate, r->pair_slot, r->tile_offsets};
 }
 
-static bool route_complete(const spt_route_buf* r) {
-  return r && r->logits && r->topk_idx && r->topk_gate && r->block_offsets && r->bucket_token &&
-         r->bucket_gate && r->pair_slot && r->tile_offsets;
+// Token-sized buffers may be NULL when T == 0 (empty allocations); the [G+1]
+// offset arrays are always required.
+static bool route_complete(const spt_route_buf* r, int64_t T) {
+  if (!r || !r->block_offsets || !r->tile_offsets) return false;
+  if (T == 0) return true;
+  return r->logits && r->topk_idx && r->topk_gate && r->bucket_token && r->bucket_gate &&
+         r->pair_slot;
 }
+static inline bool tok_ok(const void* p, int64_t T) { return p || T == 0; }
 
 static spt_status device_ok() {
   static int cached = -1;  // per-process; the library targets one architecture
@@ -134,6 +178,51 @@ extern "C" {
 int spt_ffn_abi_version(void) { return SPT_FFN_ABI_VERSION; }
 
 uint64_t spt_ffn_launch_count(void) { return g_launches.load(); }
+
+spt_status spt_ffn_profile_enable(int on) {
+  std::lock_guard<std::mutex> l(g_prof_mu);
+  g_prof_on = on != 0;
+  for (auto& r : g_prof) {
+    g_ev_pool.push_back(r.a);
+    g_ev_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  return SPT_OK;
+}
+
+int64_t spt_ffn_profile_read(char* buf, size_t len) {
+  std::lock_guard<std::mutex> l(g_prof_mu);
+  std::map<std::string, std::pair<long, double>> agg;
+  std::vector<std::string> order;
+  for (auto& r : g_prof) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) return -1;
+    auto it = agg.find(r.name);
+    if (it == agg.end()) {
+      order.push_back(r.name);
+      agg[r.name] = {1, ms};
+    } else {
+      it->second.first += 1;
+      it->second.second += ms;
+    }
+    g_ev_pool.push_back(r.a);
+    g_ev_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  std::string out;
+  char line[256];
+  for (auto& n : order) {
+    snprintf(line, sizeof line, "%s %ld %.6f\n", n.c_str(), agg[n].first, agg[n].second);
+    out += line;
+  }
+  if (buf && len) {
+    size_t n = out.size() < len - 1 ? out.size() : len - 1;
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)out.size();
+}
 
 const char* spt_status_string(spt_status s) {
   switch (s) {
@@ -163,7 +252,8 @@ spt_status spt_ffn_route(const spt_ffn_desc* desc, const void* x, const void* w_
   spt_status st = make_geom(desc, &g);
   if (st != SPT_OK) return st;
   const bool logits_in = flags & SPT_ROUTE_LOGITS_IN;
-  if (!route_complete(r) || !ws || (!logits_in && (!x || !w_r))) return SPT_ERR_INVALID_ARGUMENT;
+  if (!route_complete(r, g.T) || !ws || (!logits_in && (!tok_ok(x, g.T) || !w_r)))
+    return SPT_ERR_INVALID_ARGUMENT;
   if (ws_bytes < compute_sizes(g).ws) return SPT_ERR_WORKSPACE_TOO_SMALL;
   if ((st = device_ok()) != SPT_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
@@ -190,7 +280,8 @@ spt_status spt_ffn_forward(const spt_ffn_desc* desc, const void* x, const void* 
   Geom g;
   spt_status st = make_geom(desc, &g);
   if (st != SPT_OK) return st;
-  if (!x || !w1 || !w2 || !route_complete(r) || !y || !stash || !ws) return SPT_ERR_INVALID_ARGUMENT;
+  if (!tok_ok(x, g.T) || !w1 || !w2 || !route_complete(r, g.T) || !tok_ok(y, g.T) || !stash || !ws)
+    return SPT_ERR_INVALID_ARGUMENT;
   if (ws_bytes < compute_sizes(g).ws) return SPT_ERR_WORKSPACE_TOO_SMALL;
   if ((st = device_ok()) != SPT_OK) return st;
   if (g.T == 0) return SPT_OK;
@@ -210,8 +301,8 @@ spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void*
   Geom g;
   spt_status st = make_geom(desc, &g);
   if (st != SPT_OK) return st;
-  if (!x || !w1 || !w2 || !w_r || !route_complete(r) || !stash || !dy || !dx || !dw1 || !dw2 ||
-      !dw_r || !ws)
+  if (!tok_ok(x, g.T) || !w1 || !w2 || !w_r || !route_complete(r, g.T) || !stash ||
+      !tok_ok(dy, g.T) || !tok_ok(dx, g.T) || !dw1 || !dw2 || !dw_r || !ws)
     return SPT_ERR_INVALID_ARGUMENT;
   if (ws_bytes < compute_sizes(g).ws) return SPT_ERR_WORKSPACE_TOO_SMALL;
   if ((st = device_ok()) != SPT_OK) return st;

@@ -563,7 +563,11 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
     attr_set = true;
   }
   const int grid = std::max(1, std::min(tiles_upper, num_sms()));
+  static const char* kNames[] = {"tc_router", "tc_fwd1_gate_up", "tc_fwd2_down", "tc_bwd_dA",
+                                 "tc_bwd_dX", "tc_bwd_dW1", "tc_bwd_dW2", "tc_bwd_dWR"};
+  prof_begin(kNames[KIND], s);
   tc_gemm_kernel<KIND><<<grid, kThreads, smem, s>>>(a, stages);
+  prof_end(s);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (debug_sync()) {
@@ -725,8 +729,10 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.out = b.dwr_part;
     TRY(launch<K_DWR>(a, a.MT * a.NT * a.n_split, s));
     const int64_t n = (int64_t)g.G * g.d;
+    prof_begin("dwr_reduce", s);
     dwr_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(b.n_split, n, b.dwr_part, dw_r,
                                                                  accumulate ? 1 : 0);
+    prof_end(s);
     count_launch();
   } else if (!accumulate) {
     if (cudaMemsetAsync(dw_r, 0, (size_t)g.G * g.d * 4, s) != cudaSuccess) return cudaErrorUnknown;

@@ -100,6 +100,23 @@ def launch_count() -> int:
     return int(L.lib().spt_ffn_launch_count())
 
 
+def profile_enable(on: bool = True) -> None:
+    L.check("spt_ffn_profile_enable", L.lib().spt_ffn_profile_enable(1 if on else 0))
+
+
+def profile_read() -> dict:
+    """{kernel name: (launches, total_ms)} since profile_enable / the last read."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    n = L.lib().spt_ffn_profile_read(buf, len(buf))
+    if n < 0:
+        raise RuntimeError("spt_ffn_profile_read failed")
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split()
+        out[name] = (int(cnt), float(ms))
+    return out
+
+
 class RoutedFFN:
     """Buffers for one routed-FFN layer shape (a convenience owner of memory;
     the three methods are the ABI calls)."""

@@ -103,21 +103,24 @@ def bf16_bits(a32: np.ndarray) -> np.ndarray:
     return (u >> 16).astype(np.uint16)
 
 
-def make_inputs(cfg: FfnConfig, T: int | None = None, need=("x", "w1", "w2", "w_r", "dy")) -> dict:
+def make_inputs(cfg: FfnConfig, T: int | None = None, need=("x", "w1", "w2", "w_r", "dy"),
+                token_offset: int = 0) -> dict:
     """Seeded inputs for ``cfg`` (optionally overriding the token count T).
 
     x, dy: [T, d]; w1: [D, d] (or [2, D, d] for SwiGLU: gate, up) = W_I^T of
     Eq. 4 (PAPER.md:146); w2: [D, d] = W_O; w_r: [G, d] = W_R^T (PAPER.md:435).
     Token rows are drawn independently per token index, so the first T' rows of a
-    T-token draw equal a T'-token draw (used for sampled oracle checks).
+    T-token draw equal a T'-token draw (used for sampled oracle checks), and
+    ``token_offset`` (a multiple of 1024) selects rows [offset, offset+T) of the
+    global token stream (data-parallel shards: weights identical, tokens disjoint).
     """
     T = cfg.T if T is None else T
     s, d, D, G, k, bw, dt = cfg.seed, cfg.d, cfg.D, cfg.G, cfg.k, cfg.bw, cfg.dtype
     out = {}
     if "x" in need:
-        out["x"] = _token_rows(s, "x", T, d, 1.0, dt)
+        out["x"] = _token_rows(s, "x", T, d, 1.0, dt, token_offset)
     if "dy" in need:
-        out["dy"] = _token_rows(s, "dy", T, d, 1.0, dt)
+        out["dy"] = _token_rows(s, "dy", T, d, 1.0, dt, token_offset)
     if "w1" in need:
         shape = (2, D, d) if cfg.act == ACT_SWIGLU else (D, d)
         out["w1"] = round_to_dtype(_stream(s, "w1").standard_normal(shape) / np.sqrt(d), dt)
@@ -131,13 +134,15 @@ def make_inputs(cfg: FfnConfig, T: int | None = None, need=("x", "w1", "w2", "w_
 _ROW_CHUNK = 1024
 
 
-def _token_rows(seed, name, T, d, std, dtype):
+def _token_rows(seed, name, T, d, std, dtype, offset=0):
     """[T, d] rows drawn in chunks of 1024 tokens, each chunk its own stream, so
     that any prefix (and any chunk) can be regenerated without the whole tensor."""
+    if offset % _ROW_CHUNK:
+        raise ValueError("token_offset must be a multiple of 1024")
     out = np.empty((T, d), dtype=np.float32)
     for c0 in range(0, T, _ROW_CHUNK):
         c1 = min(T, c0 + _ROW_CHUNK)
-        g = _stream(seed, name, 1 + c0 // _ROW_CHUNK)
+        g = _stream(seed, name, 1 + (offset + c0) // _ROW_CHUNK)
         out[c0:c1] = round_to_dtype(g.standard_normal((_ROW_CHUNK, d))[: c1 - c0] * std, dtype)
     return out
 
