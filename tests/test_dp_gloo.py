@@ -1,0 +1,96 @@
+"""Data-parallel host logic on CPU with gloo, world_size 2.
+
+Token-sharded DP: each rank owns a contiguous token shard, computes its
+shard's weight gradients, and one SUM all-reduce of the flat fp32 gradient
+buffer (paper_2312_10365_b200.dp) must give the full-batch gradient (reading
+c16), while per-token outputs are independent of the world size.  The per-rank
+compute here is the CPU oracle (test infrastructure), so the test exercises
+exactly the sharding / flat-buffer / all-reduce / max-over-ranks code that
+bench.py runs over NCCL on the GPU box.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synthetic as S
+from paper_2312_10365_b200 import dp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, T, out_q):
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = S.CONFIGS["tiny"].with_(act=S.ACT_SWIGLU, d=64, D=256, G=8, k=3)
+    inp = S.make_inputs(cfg, T)
+    t0, t1 = dp.shard_range(T, rank, world)
+    sh = {n: inp[n][t0:t1] for n in ("x", "dy")}
+    lg = oracle.router(sh["x"], inp["w_r"])
+    ti = oracle.topk(lg.astype(np.float32), cfg.k)
+    g = oracle.backward(sh["x"], inp["w1"], inp["w2"], inp["w_r"], lg, ti, sh["dy"], cfg.act, cfg.gate)
+    fg = dp.FlatGrads({"dw1": g["dw1"].shape, "dw2": g["dw2"].shape, "dw_r": g["dw_r"].shape}, device="cpu")
+    for n in ("dw1", "dw2", "dw_r"):
+        fg[n].copy_(torch.from_numpy(g[n].astype(np.float32)))
+    dp.allreduce_grads(fg)
+    tmax = dp.max_over_ranks(float(rank + 1))
+    out_q.put((rank, {n: fg[n].numpy().copy() for n in ("dw1", "dw2", "dw_r")}, g["dx"], (t0, t1), tmax))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("T", [64, 67])
+def test_allreduce_equals_full_batch(orc, T):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort(key=lambda r: r[0])
+    cfg = S.CONFIGS["tiny"].with_(act=S.ACT_SWIGLU, d=64, D=256, G=8, k=3)
+    inp = S.make_inputs(cfg, T)
+    lg = orc.router(inp["x"], inp["w_r"])
+    ti = orc.topk(lg.astype(np.float32), cfg.k)
+    full = orc.backward(inp["x"], inp["w1"], inp["w2"], inp["w_r"], lg, ti, inp["dy"], cfg.act, cfg.gate)
+    for rank, grads, dx, (t0, t1), tmax in res:
+        assert tmax == 2.0                                     # max over ranks
+        for n in ("dw1", "dw2", "dw_r"):                       # SUM over ranks == full batch
+            np.testing.assert_allclose(grads[n], full[n], rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(dx, full["dx"][t0:t1], rtol=1e-12, atol=1e-12)  # per-token independence
+    # shards tile [0, T) exactly
+    assert res[0][3][0] == 0 and res[0][3][1] == res[1][3][0] and res[1][3][1] == T
+
+
+def test_shard_range_properties():
+    for T in (0, 1, 7, 4096, 32768):
+        for world in (1, 2, 3, 8):
+            r = [dp.shard_range(T, i, world) for i in range(world)]
+            assert r[0][0] == 0 and r[-1][1] == T
+            assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+            sizes = [b - a for a, b in r]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_flat_grads_views_share_storage():
+    fg = dp.FlatGrads({"dw1": (2, 3, 4), "dw2": (3, 4), "dw_r": (2, 4)}, device="cpu")
+    fg.flat.zero_()
+    fg["dw2"].fill_(1.0)
+    assert fg.flat.sum().item() == 12.0
+    assert fg["dw1"].data_ptr() == fg.flat.data_ptr()
+    assert dp.allreduce_grads(fg) is None        # single process: no-op
