@@ -61,7 +61,7 @@ cudaError_t launch_router_simt(const Geom& g, const void* x, const void* w_r, fl
 // ------------------------------------------------------------------- top-k
 // Selection key: larger |logit| bit pattern first (sign cleared, so NaN >
 // +Inf > finite), then lower block id.  key = absbits << 9 | (256 - b) >= 1.
-__global__ void __launch_bounds__(256) topk_hist_kernel(int64_t T, int G, int k, int gate_mode,
+__global__ void __launch_bounds__(1024) topk_hist_kernel(int64_t T, int G, int k, int gate_mode,
                                                         const float* __restrict__ logits,
                                                         int32_t* __restrict__ topk_idx,
                                                         float* __restrict__ topk_gate,
@@ -72,8 +72,9 @@ __global__ void __launch_bounds__(256) topk_hist_kernel(int64_t T, int G, int k,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t chunk = blockIdx.x;
   const int nslot = (G + 31) / 32;
-  for (int i = 0; i < 32; ++i) {
-    const int64_t t = chunk * kRouteChunk + warp * 32 + i;
+  const int per_warp = kRouteChunk / (blockDim.x >> 5);
+  for (int i = 0; i < per_warp; ++i) {
+    const int64_t t = chunk * kRouteChunk + warp * per_warp + i;
     if (t >= T) break;
     unsigned long long key[8];
     float lg[8];
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
 cudaError_t launch_topk_bucket(const Geom& g, const RouteView& r, const Bufs& b, cudaStream_t s) {
   const unsigned nch = (unsigned)g.n_chunks;
   prof_begin("topk_hist", s);
-  topk_hist_kernel<<<nch, 256, 0, s>>>(g.T, g.G, g.k, g.gate, r.logits, r.topk_idx, r.topk_gate,
+  topk_hist_kernel<<<nch, 1024, 0, s>>>(g.T, g.G, g.k, g.gate, r.logits, r.topk_idx, r.topk_gate,
                                        b.chunk_counts);
   prof_end(s);
   prof_begin("bucket_scan", s);

@@ -2,12 +2,18 @@
 //
 // One persistent, warp-specialised tcgen05 kernel template serves every GEMM
 // on the hot path:
-//   warp 0     TMA producer (all 32 lanes issue; gathers use tile::gather4)
-//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5  epilogue: tcgen05.ld (TMEM -> registers), fused math, stores
-// M tile = 128 bucket rows (one TMEM lane per row), K stage = 64 bf16 (one
-// 128-byte swizzle row), N <= 256 per MMA, 2 TMEM accumulators (512 columns)
-// so the epilogue of tile i overlaps the MMAs of tile i+1, 3-6 smem stages.
+//   warps 0,10,11  TMA producers.  Warp 0 lane 0 issues the tile loads; the
+//                  gather4 loads (4 token rows x 128 B each) of a stage are spread
+//                  over the lanes of all three warps (three SM sub-partitions);
+//                  each producer warp arms the stage barrier for its own bytes.
+//   warp 1         TMEM allocator (512 columns) + single-thread tcgen05.mma issuer
+//   warps 2-9      epilogue: two warps per TMEM lane quarter (column halves),
+//                  tcgen05.ld -> registers -> fused math -> global stores
+// M tile = 128 bucket rows per accumulator (one TMEM lane per row), K stage = 64
+// bf16 (one 128-byte swizzle row), N <= 256 per MMA, two TMEM accumulators so the
+// epilogue of tile i overlaps the MMAs of tile i+1 (DW1 with m'*bw = 256 instead
+// uses both accumulators for the gate and up halves of one tile, sharing the
+// gathered X stage), 3-6 smem stages.
 //
 // Kinds (Alg. 4 of PAPER.md:564-579 as grouped GEMMs over the bucket layout):
 //   ROUTER : logits = X W_R                    A = X tile,       B = w_r (K-major)
@@ -44,7 +50,7 @@ struct TcArgs {
   int64_t T;
   int G, d, D, bw, mp, act, gate, gpad;
   int NT;          // N tiles of 256 (FWD2/DX/DW*/DWR)
-  int MT;          // M tiles per block (DW*), per router (DWR)
+  int MH;          // 128-row M halves per tile (DW*: ceil(M/128) <= 2), else 1
   int n_split;     // DWR split-K factor
   int ksplit;      // DWR tokens per split (multiple of 64)
   int acc_mode;    // DW*: accumulate into output
@@ -57,11 +63,19 @@ struct TcArgs {
   void* dlg;       // DA: dense dlogits [2][T][gpad] bf16
 };
 
-constexpr int kThreads = 192;
-constexpr int kABytes = 16384;
+constexpr int kProducers = 3;                 // warps 0, 10, 11
+constexpr int kEpiWarps = 8;                  // warps 2..9
+constexpr int kThreads = 32 * (2 + kEpiWarps + kProducers - 1);  // 384
+constexpr int kABytes = 16384;                // 128 rows x 64 bf16
 
+__host__ __device__ constexpr bool kind_gather_a(int k) { return k == K_FWD1 || k == K_DA; }
+__host__ __device__ constexpr bool kind_gather_b(int k) { return k == K_DW1 || k == K_DW2; }
+__host__ __device__ constexpr bool kind_a_mn(int k) { return k == K_DW1 || k == K_DW2 || k == K_DWR; }
+__host__ __device__ constexpr bool kind_b_mn(int k) {
+  return !(k == K_ROUTER || k == K_FWD1 || k == K_DA);
+}
 __host__ __device__ constexpr int b_bytes(int kind, int BN) {
-  return (kind == K_ROUTER || kind == K_FWD1 || kind == K_DA) ? BN * 128 : 32768;
+  return kind_b_mn(kind) ? 32768 : BN * 128;
 }
 
 __device__ __forceinline__ int find_block(const int32_t* tile_offsets, int G, int t128) {
@@ -74,8 +88,8 @@ __device__ __forceinline__ int find_block(const int32_t* tile_offsets, int G, in
 }
 
 struct TileInfo {
-  int b, nt, mt;
-  int n_valid;      // valid rows of the M tile (bucket-row kinds)
+  int b, nt;
+  int n_valid;      // valid rows of the M tile (bucket-row kinds) / bucket size n_b (DW*)
   int64_t prow0;    // first padded bucket row of the M tile (bucket-row kinds)
   int64_t pos0;     // bucket position of row 0 (bucket-row kinds) / of block start (DW*)
   int nkb;          // K stages
@@ -87,8 +101,8 @@ __device__ __forceinline__ int num_tiles(const TcArgs& a) {
   if (KIND == K_ROUTER) return (int)ceil_div(a.T, 128);
   if (KIND == K_FWD1 || KIND == K_DA) return a.r.tile_offsets[a.G];
   if (KIND == K_FWD2 || KIND == K_DX) return a.r.tile_offsets[a.G] * a.NT;
-  if (KIND == K_DW1 || KIND == K_DW2) return a.G * a.MT * a.NT;
-  return a.MT * a.NT * a.n_split;  // DWR
+  if (KIND == K_DW1 || KIND == K_DW2) return a.G * a.NT;
+  return a.NT * a.n_split;  // DWR (G <= 128 rows: one M tile)
 }
 
 template <int KIND>
@@ -115,16 +129,14 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
     else ti.nkb = (a.mp * a.bw + 63) / 64;
   } else if (KIND == K_DW1 || KIND == K_DW2) {
     ti.nt = tile % a.NT;
-    ti.mt = (tile / a.NT) % a.MT;
-    ti.b = tile / (a.NT * a.MT);
+    ti.b = tile / a.NT;
     ti.pos0 = a.r.block_offsets[ti.b];
     ti.n_valid = a.r.block_offsets[ti.b + 1] - a.r.block_offsets[ti.b];  // bucket size n_b
     ti.kbase = (int64_t)a.r.tile_offsets[ti.b] * 128;
     ti.nkb = 2 * (a.r.tile_offsets[ti.b + 1] - a.r.tile_offsets[ti.b]);
-  } else {  // DWR: tile = (split, mt, nt)
+  } else {  // DWR: tile = (split, nt)
     ti.nt = tile % a.NT;
-    ti.mt = (tile / a.NT) % a.MT;
-    const int s = tile / (a.NT * a.MT);
+    const int s = tile / a.NT;
     ti.b = s;
     ti.kbase = (int64_t)s * a.ksplit;
     const int64_t t1 = a.T < ti.kbase + a.ksplit ? a.T : ti.kbase + a.ksplit;
@@ -134,86 +146,114 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
   return ti;
 }
 
+// gather4 calls per stage (each moves 4 rows x 128 B)
 template <int KIND>
-__device__ __forceinline__ uint32_t stage_tx_bytes(const TcArgs& a) {
-  if (KIND == K_FWD1) return kABytes + a.mp * a.bw * 128;
-  if (KIND == K_DA) return kABytes + a.bw * 128;
+__host__ __device__ constexpr int gather_calls() {
+  return kind_gather_a(KIND) ? 32 : (kind_gather_b(KIND) ? 64 : 0);
+}
+
+// bytes of the tile (non-gather) loads of one stage, issued by warp 0 lane 0
+template <int KIND>
+__device__ __forceinline__ uint32_t tile_tx_bytes(const TcArgs& a) {
+  if (KIND == K_FWD1) return a.mp * a.bw * 128;
+  if (KIND == K_DA) return a.bw * 128;
   if (KIND == K_ROUTER) return kABytes + a.gpad * 128;
-  return kABytes + 32768;
+  if (KIND == K_DW1 || KIND == K_DW2) return kABytes * a.MH;
+  return kABytes + 32768;  // FWD2, DX, DWR
 }
 
 // ---------------------------------------------------------------- producer
+// Tile (non-gathered) loads of one stage.  Called by warp 0 lane 0 only.
 template <int KIND>
-__device__ __forceinline__ void produce_stage(const TcArgs& a, const TileInfo& ti, int kb,
-                                              uint8_t* sA, uint8_t* sB, uint64_t* bar, int lane,
-                                              const int (&rows4)[4]) {
+__device__ __forceinline__ void produce_tiles(const TcArgs& a, const TileInfo& ti, int kb,
+                                              uint8_t* sA, uint8_t* sB, uint64_t* bar) {
   if (KIND == K_ROUTER) {
-    if (lane == 0) {
-      tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
-      tma_load_2d(sB, &a.tb, bar, kb * 64, 0);
-    }
+    tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
+    tma_load_2d(sB, &a.tb, bar, kb * 64, 0);
   } else if (KIND == K_FWD1 || KIND == K_DA) {
-    // A: 128 gathered token rows, lane l -> rows 4l..4l+3
-    tma_gather4(sA + lane * 512, &a.ta, bar, kb * 64, rows4[0], rows4[1], rows4[2], rows4[3]);
-    if (lane == 0) {
-      tma_load_2d(sB, &a.tb, bar, kb * 64, ti.b * a.bw);
-      if (KIND == K_FWD1 && a.mp == 2)
-        tma_load_2d(sB + a.bw * 128, &a.tb, bar, kb * 64, a.D + ti.b * a.bw);
-    }
+    tma_load_2d(sB, &a.tb, bar, kb * 64, ti.b * a.bw);
+    if (KIND == K_FWD1 && a.mp == 2) tma_load_2d(sB + a.bw * 128, &a.tb, bar, kb * 64, a.D + ti.b * a.bw);
   } else if (KIND == K_FWD2 || KIND == K_DX) {
-    if (lane == 0) {
-      tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
-      int krow;
-      if (KIND == K_FWD2) krow = ti.b * a.bw + kb * 64;
-      else krow = kb * 64 < a.bw ? ti.b * a.bw + kb * 64 : a.D + ti.b * a.bw + (kb * 64 - a.bw);
+    tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
+    int krow;
+    if (KIND == K_FWD2) krow = ti.b * a.bw + kb * 64;
+    else krow = kb * 64 < a.bw ? ti.b * a.bw + kb * 64 : a.D + ti.b * a.bw + (kb * 64 - a.bw);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, krow);
-    }
+    for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, krow);
   } else if (KIND == K_DW1 || KIND == K_DW2) {
-    if (lane == 0) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-        tma_load_2d(sA + j * 8192, &a.ta, bar, ti.mt * 128 + j * 64, (int)(ti.kbase + kb * 64));
-    }
-    // B: 64 gathered token rows (K) x 256 columns (N): 64 gather4 calls over 32 lanes
-#pragma unroll
-    for (int c2 = 0; c2 < 2; ++c2) {
-      const int c = lane + 32 * c2;
-      const int j = c >> 4, rg = c & 15;
-      int rr[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int e = kb * 64 + rg * 4 + i;  // entry within block bucket
-        rr[i] = e < ti.n_valid ? a.r.bucket_token[ti.pos0 + e] : (int)a.T;
-      }
-      tma_gather4(sB + j * 8192 + rg * 512, &a.tb, bar, ti.nt * 256 + j * 64, rr[0], rr[1], rr[2],
-                  rr[3]);
-    }
+    for (int j = 0; j < 2 * a.MH; ++j)  // MN-major A: 64-feature chunks x 64 bucket rows
+      tma_load_2d(sA + j * 8192, &a.ta, bar, j * 64, (int)(ti.kbase + kb * 64));
   } else {  // DWR
-    if (lane == 0) {
-      const int nk = ti.nkb / 2;
-      const int part = kb >= nk;
-      const int kk = part ? kb - nk : kb;
-      const int trow = (int)(ti.kbase + kk * 64);
+    const int nk = ti.nkb / 2;
+    const int part = kb >= nk;
+    const int kk = part ? kb - nk : kb;
+    const int trow = (int)(ti.kbase + kk * 64);
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
-        tma_load_2d(sA + j * 8192, &a.ta, bar, ti.mt * 128 + j * 64, (int)(part * a.T) + trow);
+    for (int j = 0; j < 2; ++j) tma_load_2d(sA + j * 8192, &a.ta, bar, j * 64, (int)(part * a.T) + trow);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, trow);
-    }
+    for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, trow);
+  }
+}
+
+// Gather rows of call `c` at stage kb (FWD1/DA: A rows 4c..4c+3 of the tile;
+// DW*: B row group rg = c >> 2, 64-column chunk j = c & 3, rows kb*64 + 4rg ..)
+template <int KIND>
+__device__ __forceinline__ void gather_rows(const TcArgs& a, const TileInfo& ti, int kb, int c,
+                                            int (&rr)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int e;
+    if (kind_gather_a(KIND)) e = 4 * c + i;                 // row within the M tile
+    else e = kb * 64 + (c >> 2) * 4 + i;                    // entry within the block bucket
+    rr[i] = e < ti.n_valid ? a.r.bucket_token[ti.pos0 + e] : (int)a.T;  // T -> OOB -> zeros
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ void issue_gather(const TcArgs& a, const TileInfo& ti, int kb, int c,
+                                             const int (&rr)[4], uint8_t* sA, uint8_t* sB,
+                                             uint64_t* bar) {
+  if (kind_gather_a(KIND)) {
+    tma_gather4(sA + c * 512, &a.ta, bar, kb * 64, rr[0], rr[1], rr[2], rr[3]);
+  } else {
+    const int j = c & 3, rg = c >> 2;
+    tma_gather4(sB + j * 8192 + rg * 512, &a.tb, bar, ti.nt * 256 + j * 64, rr[0], rr[1], rr[2],
+                rr[3]);
   }
 }
 
 // ---------------------------------------------------------------- epilogues
-// Row `row` of the tile is TMEM lane `row`; this thread owns it entirely.
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64], bool two) {
+  uint32_t (&lo)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[0]);
+  uint32_t (&hi)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[32]);
+  tmem_ld32(taddr, lo);
+  if (two) tmem_ld32(taddr + 32, hi);
+  tmem_ld_wait();
+}
+
+__device__ __forceinline__ void store_bf16_row(__nv_bfloat16* dst, const uint32_t* v, int n) {
+  // n in {32, 64}: pack fp32 pairs to bf16, 16-byte stores (a full line per 64 columns)
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q * 8 >= n) break;
+    d4[q] = make_uint4(pack_bf16(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1])),
+                       pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3])),
+                       pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5])),
+                       pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7])));
+  }
+}
+
+// Row `row` of the tile is TMEM lane `row`; columns [c_lo, c_hi) of it belong
+// to this thread (the other warp of the same lane quarter owns the rest).
+// tacc: TMEM address of (this warp's lane quarter, column 0) of the accumulator.
 template <int KIND>
 __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, uint32_t tacc,
-                                         int row) {
+                                         int row, int half, float* dg_xchg) {
   const bool valid = row < ti.n_valid;
   if (KIND == K_ROUTER) {
     const int64_t t = ti.prow0 + row;
-    for (int c0 = 0; c0 < a.gpad; c0 += 16) {
+    for (int c0 = half * 16; c0 < a.gpad; c0 += 32) {
       uint32_t v[16];
       tmem_ld16(tacc + c0, v);
       tmem_ld_wait();
@@ -229,7 +269,9 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     const int64_t prow = ti.prow0 + row;
     __nv_bfloat16* zr = (__nv_bfloat16*)a.out + prow * (int64_t)(a.mp * a.bw);
     __nv_bfloat16* hr = (__nv_bfloat16*)a.out2 + prow * (int64_t)a.bw;
-    for (int u0 = 0; u0 < a.bw; u0 += 32) {
+    const int hw = ((a.bw / 2) + 31) & ~31;
+    const int u_lo = half * hw, u_hi = min(a.bw, u_lo + hw);
+    for (int u0 = u_lo; u0 < u_hi; u0 += 32) {
       uint32_t vg[32], vu[32];
       tmem_ld32(tacc + u0, vg);
       if (a.mp == 2) tmem_ld32(tacc + a.bw + u0, vu);
@@ -237,8 +279,8 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
       uint32_t pz[16], pu[16], ph[16];
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
-        float z0 = valid ? __uint_as_float(vg[i]) : 0.f;
-        float z1 = valid ? __uint_as_float(vg[i + 1]) : 0.f;
+        const float z0 = valid ? __uint_as_float(vg[i]) : 0.f;
+        const float z1 = valid ? __uint_as_float(vg[i + 1]) : 0.f;
         float u0f = 0.f, u1f = 0.f;
         if (a.mp == 2) {
           u0f = valid ? __uint_as_float(vu[i]) : 0.f;
@@ -258,35 +300,29 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
       if (a.mp == 2) {
         uint4* ud = reinterpret_cast<uint4*>(zr + a.bw + u0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          ud[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
+        for (int q = 0; q < 4; ++q) ud[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
       }
     }
   } else if (KIND == K_FWD2 || KIND == K_DX) {
     const int64_t prow = ti.prow0 + row;
     __nv_bfloat16* dst = (__nv_bfloat16*)a.out + prow * (int64_t)a.d + ti.nt * 256;
     const int ncols = min(256, a.d - ti.nt * 256);
-    for (int c0 = 0; c0 < ncols; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(tacc + c0, v);
-      tmem_ld_wait();
-      if (valid) {
-        uint32_t p[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          p[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-        uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) d4[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
-      }
+    const int c_lo = half * 128, c_hi = min(ncols, c_lo + 128);
+    for (int c0 = c_lo; c0 < c_hi; c0 += 64) {
+      uint32_t v[64];
+      const bool two = c0 + 32 < c_hi;
+      tmem_ld64(tacc + c0, v, two);
+      if (valid) store_bf16_row(dst + c0, v, two ? 64 : 32);
     }
   } else if (KIND == K_DA) {
     const int64_t prow = ti.prow0 + row;
     const float g = valid ? a.r.bucket_gate[ti.pos0 + row] : 0.f;
     const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + prow * (int64_t)(a.mp * a.bw);
     __nv_bfloat16* dzr = (__nv_bfloat16*)a.out2 + prow * (int64_t)(a.mp * a.bw);
+    const int hw = ((a.bw / 2) + 31) & ~31;
+    const int u_lo = half * hw, u_hi = min(a.bw, u_lo + hw);
     float dgate = 0.f;
-    for (int u0 = 0; u0 < a.bw; u0 += 32) {
+    for (int u0 = u_lo; u0 < u_hi; u0 += 32) {
       uint32_t v[32];
       tmem_ld32(tacc + u0, v);
       tmem_ld_wait();
@@ -324,13 +360,10 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         act_fwd_bwd(a.act, zg, zu, av, dg, du);
         dgate = fmaf(dA, av, dgate);
         const float dzg = g * dA * dg, dzu = g * dA * du;
-        if (i & 1) {
-          pg[i / 2] |= (uint32_t)__bfloat16_as_ushort(__float2bfloat16(dzg)) << 16;
-          pu[i / 2] |= (uint32_t)__bfloat16_as_ushort(__float2bfloat16(dzu)) << 16;
-        } else {
-          pg[i / 2] = __bfloat16_as_ushort(__float2bfloat16(dzg));
-          pu[i / 2] = __bfloat16_as_ushort(__float2bfloat16(dzu));
-        }
+        const uint32_t bg = __bfloat16_as_ushort(__float2bfloat16(dzg));
+        const uint32_t bu = __bfloat16_as_ushort(__float2bfloat16(dzu));
+        if (i & 1) { pg[i / 2] |= bg << 16; pu[i / 2] |= bu << 16; }
+        else { pg[i / 2] = bg; pu[i / 2] = bu; }
       }
       uint4* d4 = reinterpret_cast<uint4*>(dzr + u0);
 #pragma unroll
@@ -341,64 +374,79 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         for (int q = 0; q < 4; ++q) u4[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
       }
     }
-    // dlogit = dgate * g (1 - g) = dgate * sigma(z) sigma(-z): no cancellation in 1 - g
-    float dlogit = 0.f;
-    int64_t t = 0;
-    if (valid && a.gate == SPT_GATE_SIGMOID) {
-      t = a.r.bucket_token[ti.pos0 + row];
-      const float z = a.r.logits[t * a.G + ti.b];
-      dlogit = dgate * sigmoid_pair(z);
+    // combine the two column halves' partial dgate: half 1 -> smem -> half 0
+    const int q = row >> 5;
+    if (half == 1) dg_xchg[row] = dgate;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+    if (half == 0) {
+      dgate = dgate + dg_xchg[row];
+      // dlogit = dgate * g (1 - g) = dgate * sigma(z) sigma(-z): no cancellation in 1 - g
+      float dlogit = 0.f;
+      int64_t t = 0;
+      if (valid && a.gate == SPT_GATE_SIGMOID) {
+        t = a.r.bucket_token[ti.pos0 + row];
+        dlogit = dgate * sigmoid_pair(a.r.logits[t * a.G + ti.b]);
+      }
+      a.rows_f[prow] = valid ? dgate : 0.f;
+      a.rows_g[prow] = dlogit;
+      if (valid && a.gate == SPT_GATE_SIGMOID) {
+        __nv_bfloat16* dl = (__nv_bfloat16*)a.dlg;
+        const __nv_bfloat16 hi = __float2bfloat16(dlogit);
+        const __nv_bfloat16 lo = __float2bfloat16(dlogit - __bfloat162float(hi));
+        dl[t * a.gpad + ti.b] = hi;
+        dl[(a.T + t) * a.gpad + ti.b] = lo;
+      }
     }
-    a.rows_f[prow] = valid ? dgate : 0.f;
-    a.rows_g[prow] = dlogit;
-    if (valid && a.gate == SPT_GATE_SIGMOID) {
-      __nv_bfloat16* dl = (__nv_bfloat16*)a.dlg;
-      const __nv_bfloat16 hi = __float2bfloat16(dlogit);
-      const __nv_bfloat16 lo = __float2bfloat16(dlogit - __bfloat162float(hi));
-      dl[t * a.gpad + ti.b] = hi;
-      dl[(a.T + t) * a.gpad + ti.b] = lo;
-    }
-  } else if (KIND == K_DW1 || KIND == K_DW2 || KIND == K_DWR) {
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // dg_xchg reuse next tile
+  } else {  // DW1, DW2, DWR: fp32 tiles
     // NOTE: tcgen05.ld is warp-collective (.sync.aligned): every lane executes
     // the loads; only the stores are predicated on the row being real.
     int64_t orow = 0;
     bool live;
+    int c_lo, c_hi;
+    const int ncols = min(256, a.d - ti.nt * 256);
     if (KIND == K_DWR) {  // split-K partial [split][G][d]
-      const int gb = ti.mt * 128 + row;
-      live = gb < a.G;
-      orow = (int64_t)ti.b * a.G + gb;
+      live = row < a.G;
+      orow = (int64_t)ti.b * a.G + row;
+      c_lo = half * 128;
+      c_hi = min(ncols, c_lo + 128);
     } else {
-      const int f = ti.mt * 128 + row;  // feature row within the block's m'*bw (or bw)
+      // MH == 2: this warp's half owns accumulator `half` (features half*128 + row);
+      // MH == 1: one accumulator, columns split between the halves
+      const int f = (a.MH == 2 ? half * 128 : 0) + row;
       const int M = KIND == K_DW1 ? a.mp * a.bw : a.bw;
       live = f < M;
       if (KIND == K_DW1 && a.mp == 2)
         orow = f < a.bw ? (int64_t)ti.b * a.bw + f : (int64_t)a.D + (int64_t)ti.b * a.bw + (f - a.bw);
       else
         orow = (int64_t)ti.b * a.bw + f;
+      if (a.MH == 2) { c_lo = 0; c_hi = ncols; }
+      else { c_lo = half * 128; c_hi = min(ncols, c_lo + 128); }
     }
     float* dst = (float*)a.out + orow * a.d + ti.nt * 256;
-    const int ncols = min(256, a.d - ti.nt * 256);
     const bool acc = KIND != K_DWR && a.acc_mode;
-    for (int c0 = 0; c0 < ncols; c0 += 32) {
-      uint32_t v[32];
+    for (int c0 = c_lo; c0 < c_hi; c0 += 64) {
+      uint32_t v[64];
+      const bool two = c0 + 32 < c_hi;
       if (ti.nkb > 0) {
-        tmem_ld32(tacc + c0, v);
-        tmem_ld_wait();
+        tmem_ld64(tacc + c0, v, two);
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0u;
+        for (int i = 0; i < 64; ++i) v[i] = 0u;
       }
       if (!live) continue;
       float4* d4 = reinterpret_cast<float4*>(dst + c0);
+      const int nq = two ? 16 : 8;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 o = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                               __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+      for (int qq = 0; qq < 16; ++qq) {
+        if (qq >= nq) break;
+        float4 o = make_float4(__uint_as_float(v[4 * qq]), __uint_as_float(v[4 * qq + 1]),
+                               __uint_as_float(v[4 * qq + 2]), __uint_as_float(v[4 * qq + 3]));
         if (acc) {
-          const float4 p = d4[q];
+          const float4 p = d4[qq];
           o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
         }
-        d4[q] = o;
+        d4[qq] = o;
       }
     }
   }
@@ -410,25 +458,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
                                                                int n_stages) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  constexpr bool kAmn = KIND == K_DW1 || KIND == K_DW2 || KIND == K_DWR;
-  constexpr bool kBmn = !(KIND == K_ROUTER || KIND == K_FWD1 || KIND == K_DA);
+  constexpr bool kAmn = kind_a_mn(KIND);
+  constexpr bool kBmn = kind_b_mn(KIND);
+  const int astride = kABytes * a.MH;
   const int bstride = (b_bytes(KIND, a.BN) + 1023) & ~1023;
-  const int sstride = kABytes + bstride;
+  const int sstride = astride + bstride;
   uint64_t* full = (uint64_t*)(smem + n_stages * sstride);
   uint64_t* empty = full + n_stages;
   uint64_t* tfull = empty + n_stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  float* dg_xchg = (float*)(tmem_slot + 4);  // [128] DA half-row exchange
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // two accumulators alternate between tiles unless one tile needs both (MH == 2)
+  const int n_acc = a.MH == 2 ? 1 : 2;
   if (threadIdx.x == 0) {
     for (int s = 0; s < n_stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kProducers);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -443,21 +495,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   const uint32_t tmem = *tmem_slot;
   const int ntiles = num_tiles<KIND>(a);
 
-  if (warp == 0) {
-    // ---------------------------------------------------------- producer
+  if (warp == 0 || warp >= 2 + kEpiWarps) {
+    // ---------------------------------------------------------- producers
+    const int p = warp == 0 ? 0 : warp - (2 + kEpiWarps) + 1;  // 0, 1, 2
+    const int c = lane * kProducers + p;                         // gather call of this lane
+    constexpr int kCalls = gather_calls<KIND>();
+    const bool has_call = c < kCalls;
+    // active gather calls in this warp: lanes l with l*3 + p < kCalls
+    const int my_calls = kCalls > p ? (kCalls - p + kProducers - 1) / kProducers : 0;
+    const uint32_t tx = (uint32_t)my_calls * 512u + (p == 0 ? tile_tx_bytes<KIND>(a) : 0u);
     int stage = 0;
     uint32_t phase = 0;
-    const uint32_t tx = stage_tx_bytes<KIND>(a);
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo ti = decode<KIND>(a, tile);
-      int rows4[4] = {0, 0, 0, 0};
-      if (KIND == K_FWD1 || KIND == K_DA) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int rr = lane * 4 + i;
-          rows4[i] = rr < ti.n_valid ? a.r.bucket_token[ti.pos0 + rr] : (int)a.T;
-        }
-      }
+      int rr[4] = {0, 0, 0, 0};
+      if (has_call) gather_rows<KIND>(a, ti, 0, c, rr);  // FWD1/DA: fixed for the tile
       for (int kb = 0; kb < ti.nkb; ++kb) {
         if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -465,7 +517,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
         __syncwarp();
         uint8_t* sA = smem + stage * sstride;
-        produce_stage<KIND>(a, ti, kb, sA, sA + kABytes, &full[stage], lane, rows4);
+        uint8_t* sB = sA + astride;
+        if (p == 0 && lane == 0) produce_tiles<KIND>(a, ti, kb, sA, sB, &full[stage]);
+        if (has_call) {
+          issue_gather<KIND>(a, ti, kb, c, rr, sA, sB, &full[stage]);
+          if (kind_gather_b(KIND) && kb + 1 < ti.nkb) gather_rows<KIND>(a, ti, kb + 1, c, rr);
+        }
         if (++stage == n_stages) { stage = 0; phase ^= 1; }
       }
     }
@@ -481,19 +538,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       if (lane == 0) {
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
-        const uint32_t dtm = tmem + acc * 256;
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * sstride);
-          const uint32_t sb = sa + kABytes;
+          const uint32_t sb = sa + astride;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = kAmn ? sdesc_sw128(sa + k * 2048, 8192, 1024)
-                                     : sdesc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = kBmn ? sdesc_sw128(sb + k * 2048, 8192, 1024)
                                      : sdesc_sw128(sb + k * 32, 16, 1024);
-            mma_bf16(dtm, ad, bd, idesc, (kb | k) != 0);
+            for (int h = 0; h < a.MH; ++h) {
+              const uint64_t ad = kAmn ? sdesc_sw128(sa + h * 16384 + k * 2048, 8192, 1024)
+                                       : sdesc_sw128(sa + k * 32, 16, 1024);
+              const uint32_t dtm = tmem + (n_acc == 2 ? acc : h) * 256;
+              mma_bf16(dtm, ad, bd, idesc, (kb | k) != 0);
+            }
           }
           mma_commit(&empty[stage]);
           if (++stage == n_stages) { stage = 0; phase ^= 1; }
@@ -501,11 +560,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         mma_commit(&tfull[acc]);
       }
       __syncwarp();
-      if (++acc == 2) { acc = 0; aphase ^= 1; }
+      if (++acc == n_acc) { acc = 0; aphase ^= 1; }
     }
   } else {
     // --------------------------------------------------------- epilogue
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int e = warp - 2;
+    const int q = warp & 3;   // TMEM lane quarter this warp may access
+    const int half = e >> 2;  // column half (or M half when MH == 2)
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t aphase = 0;
@@ -513,11 +574,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       const TileInfo ti = decode<KIND>(a, tile);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      epilogue<KIND>(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, row);
+      const uint32_t col0 = (n_acc == 2 ? acc : (a.MH == 2 ? half : 0)) * 256;
+      epilogue<KIND>(a, ti, tmem + ((uint32_t)(q * 32) << 16) + col0, row, half, dg_xchg);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; aphase ^= 1; }
+      if (++acc == n_acc) { acc = 0; aphase ^= 1; }
     }
   }
   __syncthreads();
@@ -551,10 +613,10 @@ static int num_sms() {
 template <int KIND>
 static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   const int bst = (b_bytes(KIND, a.BN) + 1023) & ~1023;
-  const int sst = kABytes + bst;
-  const int budget = 227 * 1024 - 1024 - 256;
-  int stages = std::min(6, budget / sst);
-  const int smem = 1024 + stages * sst + 256;
+  const int sst = kABytes * a.MH + bst;
+  const int extra = 1024 + 256 + 512;  // alignment slack + barriers + DA exchange
+  int stages = std::min(6, (227 * 1024 - extra) / sst);
+  const int smem = stages * sst + extra;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<KIND>,
@@ -572,8 +634,8 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   cudaError_t e = cudaGetLastError();
   if (debug_sync()) {
     e = cudaStreamSynchronize(s);
-    fprintf(stderr, "[spt] tc kind %d grid %d stages %d smem %d BN %d: %s\n", KIND, grid, stages,
-            smem, a.BN, cudaGetErrorString(e));
+    fprintf(stderr, "[spt] tc kind %d grid %d stages %d smem %d BN %d MH %d: %s\n", KIND, grid,
+            stages, smem, a.BN, a.MH, cudaGetErrorString(e));
   }
   return e;
 }
@@ -590,15 +652,16 @@ static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
   a.gate = g.gate;
   a.gpad = g.gpad;
   a.NT = (int)ceil_div(g.d, 256);
+  a.MH = 1;
 }
 
 static int bucket_tiles_upper(const Geom& g) { return (int)(ceil_div(g.pairs, 128) + g.G); }
 
 bool tc_supported(const Geom& g) {
   if (g.d % 64) return false;
-  if (g.mp * g.bw > 256) return false;          // FWD1 N = m' * bw in one MMA
+  if (g.mp * g.bw > 256) return false;          // FWD1 N = m' * bw in one MMA; DW1 M <= 256
   if (g.mp == 2 && g.bw % 64) return false;     // DX K stages must not straddle gate/up
-  if (g.gpad > 256) return false;
+  if (g.gpad > 128) return false;               // DWR: one 128-row M tile of blocks
   return true;
 }
 
@@ -693,17 +756,17 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   }
   cudaError_t e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
   if (e != cudaSuccess) return e;
-  {  // a9: dW1_b = dZ_b^T X[bucket_b]
+  {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features in <= 2 halves)
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
                                 (uint64_t)g.mp * g.bw, 64, 64) &&
               make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 1);
     a.BN = 256;
-    a.MT = (int)ceil_div(g.mp * g.bw, 128);
+    a.MH = (int)ceil_div(g.mp * g.bw, 128);
     a.out = dw1;
     a.acc_mode = accumulate;
-    TRY(launch<K_DW1>(a, g.G * a.MT * a.NT, s));
+    TRY(launch<K_DW1>(a, g.G * a.NT, s));
   }
   {  // a9: dW2_b = H~_b^T dY[bucket_b]
     TcArgs a{};
@@ -711,10 +774,10 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, 64) &&
               make_tmap_bf16_2d(&a.tb, dy, g.T, g.d, g.d, 64, 1);
     a.BN = 256;
-    a.MT = (int)ceil_div(g.bw, 128);
+    a.MH = (int)ceil_div(g.bw, 128);
     a.out = dw2;
     a.acc_mode = accumulate;
-    TRY(launch<K_DW2>(a, g.G * a.MT * a.NT, s));
+    TRY(launch<K_DW2>(a, g.G * a.NT, s));
   }
   // a10: dW_R = dLogits^T X  (split-K, hi + lo bf16 halves of dlogit)
   if (sig) {
@@ -723,11 +786,10 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     bool ok = make_tmap_bf16_2d(&a.ta, b.dlg, (uint64_t)2 * g.T, g.gpad, g.gpad, 64, 64) &&
               make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 64);
     a.BN = 256;
-    a.MT = (int)ceil_div(g.G, 128);
     a.n_split = b.n_split;
     a.ksplit = (int)(ceil_div(ceil_div(g.T, b.n_split), 64) * 64);
     a.out = b.dwr_part;
-    TRY(launch<K_DWR>(a, a.MT * a.NT * a.n_split, s));
+    TRY(launch<K_DWR>(a, a.NT * a.n_split, s));
     const int64_t n = (int64_t)g.G * g.d;
     prof_begin("dwr_reduce", s);
     dwr_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(b.n_split, n, b.dwr_part, dw_r,
