@@ -53,7 +53,12 @@ struct Bufs {
   int32_t* chunk_counts;  // [n_chunks, G]
   int32_t* chunk_base;    // [n_chunks, G]
   int32_t* n_b;           // [G]
+  int32_t* tile_list;     // [ceil(T*k/128) + G]: bucket tiles in (m-tile, block) order
+  int32_t* unit_offsets;  // [G+1]: prefix of weight-resident work units per block
 };
+
+constexpr int kUnitMTiles = 16;  // m-tiles per weight-resident unit (FWD2 / DX)
+constexpr int kRasterBlocks = 16;  // blocks per L2 raster group of the gathered-A GEMMs
 
 void count_launch(int n = 1);
 // optional per-kernel CUDA-event profiling (spt_ffn_profile_enable / _read)

@@ -93,7 +93,7 @@ static int dwr_splits(const Geom& g) {
 
 struct Sizes {
   size_t z, h, stash;
-  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, ws;
+  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, ws;
 };
 
 static Sizes compute_sizes(const Geom& g) {
@@ -112,7 +112,10 @@ static Sizes compute_sizes(const Geom& g) {
   s.counts = align256((size_t)g.n_chunks * g.G * 4);
   s.base = s.counts;
   s.nb = align256((size_t)g.G * 4);
-  s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb;
+  s.tl = align256((size_t)(ceil_div(g.pairs, kTileM) + g.G) * 4);
+  s.uo = align256((size_t)(g.G + 2) * 4);
+  s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb +
+         s.tl + s.uo;
   return s;
 }
 
@@ -136,6 +139,8 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
   b.chunk_counts = (int32_t*)w; w += s.counts;
   b.chunk_base = (int32_t*)w; w += s.base;
   b.n_b = (int32_t*)w; w += s.nb;
+  b.tile_list = (int32_t*)w; w += s.tl;
+  b.unit_offsets = (int32_t*)w; w += s.uo;
   return b;
 }
 

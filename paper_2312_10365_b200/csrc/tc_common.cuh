@@ -75,6 +75,28 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uin
       "r"(smem_u32(bar))
       : "memory");
 }
+// smem -> global tensor store (bulk group); source must be visible to the async
+// proxy (fence_proxy_async_smem) before the call
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// wait until at most N committed bulk groups still READ their smem source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
 // L2 cache-policy descriptors for the .L2::cache_hint variants
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;

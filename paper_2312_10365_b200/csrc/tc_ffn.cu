@@ -46,6 +46,7 @@ enum Kind : int { K_ROUTER = 0, K_FWD1, K_FWD2, K_DA, K_DX, K_DW1, K_DW2, K_DWR 
 struct TcArgs {
   CUtensorMap ta;  // A operand
   CUtensorMap tb;  // B operand
+  CUtensorMap tc;  // FWD2/DX: partials [rows, d] bf16, box 64 cols x 32 rows (TMA store)
   RouteView r;
   int64_t T;
   int G, d, D, bw, mp, act, gate, gpad;
@@ -61,6 +62,10 @@ struct TcArgs {
   float* rows_f;   // DA: dgate rows
   float* rows_g;   // DA: dlogit rows
   void* dlg;       // DA: dense dlogits [2][T][gpad] bf16
+  const int32_t* tile_list;     // FWD1/DA: (mt << 8 | b) in m-tile-major order
+  const int32_t* unit_offsets;  // FWD2/DX: weight-resident unit prefix per block
+  int n_stg;                    // FWD2/DX: 4 KB staging buffers per epilogue warp (1 or 2)
+  int exp_flag;                 // experiment switch (SPT_FFN_EXPERIMENT), timing only
 };
 
 constexpr int kProducers = 3;                 // warps 0, 10, 11
@@ -74,8 +79,11 @@ __host__ __device__ constexpr bool kind_a_mn(int k) { return k == K_DW1 || k == 
 __host__ __device__ constexpr bool kind_b_mn(int k) {
   return !(k == K_ROUTER || k == K_FWD1 || k == K_DA);
 }
+// FWD2 / DX keep one (block, 256-column) weight slab resident in smem and
+// stream up to kUnitMTiles A tiles of that block through it
+__host__ __device__ constexpr bool kind_bres(int k) { return k == K_FWD2 || k == K_DX; }
 __host__ __device__ constexpr int b_bytes(int kind, int BN) {
-  return kind_b_mn(kind) ? 32768 : BN * 128;
+  return kind_bres(kind) ? 0 : (kind_b_mn(kind) ? 32768 : BN * 128);
 }
 
 __device__ __forceinline__ int find_block(const int32_t* tile_offsets, int G, int t128) {
@@ -94,13 +102,25 @@ struct TileInfo {
   int64_t pos0;     // bucket position of row 0 (bucket-row kinds) / of block start (DW*)
   int nkb;          // K stages
   int64_t kbase;    // DW*: first padded row of the block; DWR: first token of the split
+  int rows_pad;     // bucket-row kinds: padded rows of the block from prow0 on (write limit)
 };
+
+// TMEM columns: accumulator buffer `acc`, M half `h` (each half holds BN <= 256
+// columns at a stride of 128 or 256); two buffers alternate between tiles when
+// they fit in the 512 allocated columns, else one buffer.
+__host__ __device__ __forceinline__ int tm_half_stride(int BN) { return BN > 128 ? 256 : 128; }
+__host__ __device__ __forceinline__ int tm_nacc(int BN, int MH) {
+  return 2 * MH * tm_half_stride(BN) <= 512 ? 2 : 1;
+}
+__host__ __device__ __forceinline__ uint32_t tm_col(int BN, int MH, int acc, int h) {
+  return (uint32_t)((acc * MH + h) * tm_half_stride(BN));
+}
 
 template <int KIND>
 __device__ __forceinline__ int num_tiles(const TcArgs& a) {
   if (KIND == K_ROUTER) return (int)ceil_div(a.T, 128);
-  if (KIND == K_FWD1 || KIND == K_DA) return a.r.tile_offsets[a.G];
-  if (KIND == K_FWD2 || KIND == K_DX) return a.r.tile_offsets[a.G] * a.NT;
+  if (KIND == K_FWD1 || KIND == K_DA) return a.unit_offsets[a.G + 1];  // 256-row pair tiles
+  if (KIND == K_FWD2 || KIND == K_DX) return a.unit_offsets[a.G];  // units
   if (KIND == K_DW1 || KIND == K_DW2) return a.G * a.NT;
   return a.NT * a.n_split;  // DWR (G <= 128 rows: one M tile)
 }
@@ -112,21 +132,18 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
     ti.prow0 = (int64_t)tile * 128;
     ti.n_valid = (int)(a.T - ti.prow0 < 128 ? a.T - ti.prow0 : 128);
     ti.nkb = a.d / 64;
-  } else if (KIND == K_FWD1 || KIND == K_DA || KIND == K_FWD2 || KIND == K_DX) {
-    int t128 = tile;
-    if (KIND == K_FWD2 || KIND == K_DX) {
-      t128 = tile / a.NT;
-      ti.nt = tile % a.NT;
-    }
-    ti.b = find_block(a.r.tile_offsets, a.G, t128);
-    const int mt = t128 - a.r.tile_offsets[ti.b];
+  } else if (KIND == K_FWD1 || KIND == K_DA) {
+    // pair tiles (two 128-row m-tiles sharing each B stage) in the raster order
+    // of tile_sched_kernel
+    const int e = a.tile_list[tile];
+    ti.b = e & 255;
+    const int mt = 2 * (e >> 8);
     const int nb = a.r.block_offsets[ti.b + 1] - a.r.block_offsets[ti.b];
     ti.n_valid = nb - mt * 128;
-    ti.prow0 = (int64_t)t128 * 128;
+    ti.prow0 = (int64_t)(a.r.tile_offsets[ti.b] + mt) * 128;
     ti.pos0 = a.r.block_offsets[ti.b] + mt * 128;
-    if (KIND == K_FWD1 || KIND == K_DA) ti.nkb = a.d / 64;
-    else if (KIND == K_FWD2) ti.nkb = (a.bw + 63) / 64;
-    else ti.nkb = (a.mp * a.bw + 63) / 64;
+    ti.rows_pad = (a.r.tile_offsets[ti.b + 1] - a.r.tile_offsets[ti.b] - mt) * 128;
+    ti.nkb = a.d / 64;
   } else if (KIND == K_DW1 || KIND == K_DW2) {
     ti.nt = tile % a.NT;
     ti.b = tile / a.NT;
@@ -146,10 +163,38 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
   return ti;
 }
 
+// FWD2 / DX work unit u -> (block b, m-tiles [mt0, mt1), N tile nt)
+struct UnitInfo {
+  int b, nt, mt0, mt1;
+};
+__device__ __forceinline__ UnitInfo decode_unit(const TcArgs& a, int u) {
+  UnitInfo ui;
+  ui.b = find_block(a.unit_offsets, a.G, u);
+  const int r = u - a.unit_offsets[ui.b];
+  ui.nt = r % a.NT;
+  const int mc = r / a.NT;
+  const int ntb = a.r.tile_offsets[ui.b + 1] - a.r.tile_offsets[ui.b];
+  ui.mt0 = mc * kUnitMTiles;
+  ui.mt1 = min(ntb, ui.mt0 + kUnitMTiles);
+  return ui;
+}
+template <int KIND>
+__device__ __forceinline__ TileInfo decode_mtile(const TcArgs& a, const UnitInfo& u, int mt) {
+  TileInfo ti{};
+  ti.b = u.b;
+  ti.nt = u.nt;
+  const int nb = a.r.block_offsets[u.b + 1] - a.r.block_offsets[u.b];
+  ti.n_valid = nb - mt * 128;
+  ti.prow0 = (int64_t)(a.r.tile_offsets[u.b] + mt) * 128;
+  ti.pos0 = a.r.block_offsets[u.b] + mt * 128;
+  ti.nkb = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
+  return ti;
+}
+
 // gather4 calls per stage (each moves 4 rows x 128 B)
 template <int KIND>
-__host__ __device__ constexpr int gather_calls() {
-  return kind_gather_a(KIND) ? 32 : (kind_gather_b(KIND) ? 64 : 0);
+__host__ __device__ constexpr int gather_calls(int MH) {
+  return kind_gather_a(KIND) ? 32 * MH : (kind_gather_b(KIND) ? 64 : 0);
 }
 
 // bytes of the tile (non-gather) loads of one stage, issued by warp 0 lane 0
@@ -270,7 +315,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     __nv_bfloat16* zr = (__nv_bfloat16*)a.out + prow * (int64_t)(a.mp * a.bw);
     __nv_bfloat16* hr = (__nv_bfloat16*)a.out2 + prow * (int64_t)a.bw;
     const int hw = ((a.bw / 2) + 31) & ~31;
-    const int u_lo = half * hw, u_hi = min(a.bw, u_lo + hw);
+    const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? a.bw : min(a.bw, u_lo + hw);
     for (int u0 = u_lo; u0 < u_hi; u0 += 32) {
       uint32_t vg[32], vu[32];
       tmem_ld32(tacc + u0, vg);
@@ -320,7 +365,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + prow * (int64_t)(a.mp * a.bw);
     __nv_bfloat16* dzr = (__nv_bfloat16*)a.out2 + prow * (int64_t)(a.mp * a.bw);
     const int hw = ((a.bw / 2) + 31) & ~31;
-    const int u_lo = half * hw, u_hi = min(a.bw, u_lo + hw);
+    const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? a.bw : min(a.bw, u_lo + hw);
     float dgate = 0.f;
     for (int u0 = u_lo; u0 < u_hi; u0 += 32) {
       uint32_t v[32];
@@ -374,12 +419,15 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         for (int q = 0; q < 4; ++q) u4[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
       }
     }
-    // combine the two column halves' partial dgate: half 1 -> smem -> half 0
+    // column-split epilogue: combine the two halves' partial dgate (half 1 ->
+    // smem -> half 0); half < 0: this thread saw the whole row
     const int q = row >> 5;
-    if (half == 1) dg_xchg[row] = dgate;
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-    if (half == 0) {
-      dgate = dgate + dg_xchg[row];
+    if (half >= 0) {
+      if (half == 1) dg_xchg[row] = dgate;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      if (half == 0) dgate = dgate + dg_xchg[row];
+    }
+    if (half <= 0) {
       // dlogit = dgate * g (1 - g) = dgate * sigma(z) sigma(-z): no cancellation in 1 - g
       float dlogit = 0.f;
       int64_t t = 0;
@@ -397,7 +445,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         dl[(a.T + t) * a.gpad + ti.b] = lo;
       }
     }
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // dg_xchg reuse next tile
+    if (half >= 0) asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // dg_xchg reuse
   } else {  // DW1, DW2, DWR: fp32 tiles
     // NOTE: tcgen05.ld is warp-collective (.sync.aligned): every lane executes
     // the loads; only the stores are predicated on the row being real.
@@ -452,6 +500,42 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
   }
 }
 
+// FWD2 / DX epilogue: the 32 rows x 128 columns of this warp go out as two
+// 32 x 64 TMA tensor stores from a 128-byte-swizzled smem staging buffer
+// (full-line writes, no per-thread strided stores).  Padding rows of the tile
+// are written too: they lie inside the block's own padded bucket rows, which
+// no consumer reads.
+__device__ __forceinline__ void epilogue_tma_store(const TcArgs& a, const TileInfo& ti,
+                                                   uint32_t tacc, int q, int lane, int half,
+                                                   uint8_t* stg, int& stg_i) {
+  const int ncols = min(256, a.d - ti.nt * 256);
+  const int c_lo = half * 128, c_hi = min(ncols, c_lo + 128);
+  for (int c0 = c_lo; c0 < c_hi; c0 += 64) {
+    uint32_t v[64];
+    tmem_ld64(tacc + c0, v, true);
+    uint8_t* buf = stg + stg_i * 4096;
+    if (lane == 0) {
+      if (a.n_stg == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of this row, swizzled by row & 7
+      const uint4 w = make_uint4(pack_bf16(__uint_as_float(v[8 * c + 0]), __uint_as_float(v[8 * c + 1])),
+                                 pack_bf16(__uint_as_float(v[8 * c + 2]), __uint_as_float(v[8 * c + 3])),
+                                 pack_bf16(__uint_as_float(v[8 * c + 4]), __uint_as_float(v[8 * c + 5])),
+                                 pack_bf16(__uint_as_float(v[8 * c + 6]), __uint_as_float(v[8 * c + 7])));
+      *reinterpret_cast<uint4*>(buf + lane * 128 + ((c ^ (lane & 7)) << 4)) = w;
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(&a.tc, buf, ti.nt * 256 + c0, (int)(ti.prow0 + q * 32));
+      bulk_commit();
+    }
+    stg_i = (stg_i + 1) % a.n_stg;
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcArgs a,
@@ -463,21 +547,33 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   const int astride = kABytes * a.MH;
   const int bstride = (b_bytes(KIND, a.BN) + 1023) & ~1023;
   const int sstride = astride + bstride;
-  uint64_t* full = (uint64_t*)(smem + n_stages * sstride);
+  // barrier area after the stage ring (weight-resident kinds: after slab + ring)
+  const int ring_bytes = kind_bres(KIND)
+                             ? (KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64) * 32768 +
+                                   n_stages * kABytes
+                             : n_stages * sstride;
+  uint64_t* full = (uint64_t*)(smem + ring_bytes);
   uint64_t* empty = full + n_stages;
   uint64_t* tfull = empty + n_stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* bres_full = tempty + 2;
+  uint64_t* bres_empty = bres_full + 1;
+  uint32_t* tmem_slot = (uint32_t*)(bres_empty + 1);
   float* dg_xchg = (float*)(tmem_slot + 4);  // [128] DA half-row exchange
+  uint8_t* stg_base = (uint8_t*)(((uintptr_t)(dg_xchg + 128) + 1023) & ~(uintptr_t)1023);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // two accumulators alternate between tiles unless one tile needs both (MH == 2)
-  const int n_acc = a.MH == 2 ? 1 : 2;
+  // two accumulators alternate between tiles when both fit in TMEM
+  const int n_acc = tm_nacc(a.BN, a.MH);
   if (threadIdx.x == 0) {
+    // gathering kinds: each of the 3 producer warps arms its own bytes
+    const int n_prod = (kind_gather_a(KIND) || kind_gather_b(KIND)) ? kProducers : 1;
     for (int s = 0; s < n_stages; ++s) {
-      mbar_init(&full[s], kProducers);
+      mbar_init(&full[s], n_prod);
       mbar_init(&empty[s], 1);
     }
+    mbar_init(bres_full, 1);
+    mbar_init(bres_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kEpiWarps);
@@ -495,18 +591,107 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   const uint32_t tmem = *tmem_slot;
   const int ntiles = num_tiles<KIND>(a);
 
-  if (warp == 0 || warp >= 2 + kEpiWarps) {
+  if (kind_bres(KIND)) {
+    // ============ weight-resident units (FWD2 / DX): B slab once per unit
+    const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;  // K stages
+    uint8_t* sBres = smem;                                   // kbu x 32 KB
+    uint8_t* ring = smem + kbu * 32768;                      // A stages of 16 KB
+    if (warp == 0) {
+      if (lane == 0) {
+        int stage = 0;
+        uint32_t phase = 0, uph = 0;
+        for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+          const UnitInfo ui = decode_unit(a, u);
+          mbar_wait(bres_empty, uph ^ 1);
+          mbar_arrive_expect_tx(bres_full, kbu * 32768u);
+          for (int kb = 0; kb < kbu; ++kb) {
+            int krow;
+            if (KIND == K_FWD2) krow = ui.b * a.bw + kb * 64;
+            else krow = kb * 64 < a.bw ? ui.b * a.bw + kb * 64 : a.D + ui.b * a.bw + (kb * 64 - a.bw);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              tma_load_2d(sBres + kb * 32768 + j * 8192, &a.tb, bres_full, ui.nt * 256 + j * 64, krow);
+          }
+          uph ^= 1;
+          for (int mt = ui.mt0; mt < ui.mt1; ++mt) {
+            const int64_t prow0 = (int64_t)(a.r.tile_offsets[ui.b] + mt) * 128;
+            for (int kb = 0; kb < kbu; ++kb) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_arrive_expect_tx(&full[stage], kABytes);
+              tma_load_2d(ring + stage * kABytes, &a.ta, &full[stage], kb * 64, (int)prow0);
+              if (++stage == n_stages) { stage = 0; phase ^= 1; }
+            }
+          }
+        }
+      }
+    } else if (warp == 1) {
+      if (lane == 0) {
+        const uint32_t idesc = idesc_bf16(128, 256, false, true);
+        int stage = 0, acc = 0;
+        uint32_t phase = 0, aphase = 0, uph = 0;
+        for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+          const UnitInfo ui = decode_unit(a, u);
+          mbar_wait(bres_full, uph);
+          uph ^= 1;
+          for (int mt = ui.mt0; mt < ui.mt1; ++mt) {
+            mbar_wait(&tempty[acc], aphase ^ 1);
+            tc_fence_after();
+            const uint32_t dtm = tmem + acc * 256;
+            for (int kb = 0; kb < kbu; ++kb) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint32_t sa = smem_u32(ring + stage * kABytes);
+              const uint32_t sb = smem_u32(sBres + kb * 32768);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16(dtm, sdesc_sw128(sa + k * 32, 16, 1024),
+                         sdesc_sw128(sb + k * 2048, 8192, 1024), idesc, (kb | k) != 0);
+              mma_commit(&empty[stage]);
+              if (++stage == n_stages) { stage = 0; phase ^= 1; }
+            }
+            mma_commit(&tfull[acc]);
+            if (++acc == 2) { acc = 0; aphase ^= 1; }
+          }
+          mma_commit(bres_empty);  // weight slab free once this unit's MMAs retire
+        }
+      }
+      __syncwarp();
+    } else if (warp >= 2 && warp < 2 + kEpiWarps) {
+      const int e = warp - 2;
+      const int q = warp & 3;
+      const int half = e >> 2;
+      int acc = 0, stg_i = 0;
+      uint32_t aphase = 0;
+      for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+        const UnitInfo ui = decode_unit(a, u);
+        for (int mt = ui.mt0; mt < ui.mt1; ++mt) {
+          const TileInfo ti = decode_mtile<KIND>(a, ui, mt);
+          mbar_wait(&tfull[acc], aphase);
+          tc_fence_after();
+          epilogue_tma_store(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, q, lane, half,
+                             stg_base + e * a.n_stg * 4096, stg_i);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
+      }
+      if (lane == 0) bulk_wait<0>();  // all partial tiles written before exit
+    }
+  } else if (warp == 0 || warp >= 2 + kEpiWarps) {
     // ---------------------------------------------------------- producers
     const int p = warp == 0 ? 0 : warp - (2 + kEpiWarps) + 1;  // 0, 1, 2
     const int c = lane * kProducers + p;                         // gather call of this lane
-    constexpr int kCalls = gather_calls<KIND>();
+    const int kCalls = gather_calls<KIND>(a.MH);
     const bool has_call = c < kCalls;
     // active gather calls in this warp: lanes l with l*3 + p < kCalls
     const int my_calls = kCalls > p ? (kCalls - p + kProducers - 1) / kProducers : 0;
-    const uint32_t tx = (uint32_t)my_calls * 512u + (p == 0 ? tile_tx_bytes<KIND>(a) : 0u);
+    uint32_t tx = (uint32_t)my_calls * 512u + (p == 0 ? tile_tx_bytes<KIND>(a) : 0u);
+    if (kind_gather_a(KIND) && a.exp_flag == 1) tx = p == 0 ? kABytes + tile_tx_bytes<KIND>(a) : 0u;
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int ntiles_p = (p == 0 || kCalls > 0) ? ntiles : 0;  // non-gathering kinds: warp 0 only
+    for (int tile = blockIdx.x; tile < ntiles_p; tile += gridDim.x) {
       const TileInfo ti = decode<KIND>(a, tile);
       int rr[4] = {0, 0, 0, 0};
       if (has_call) gather_rows<KIND>(a, ti, 0, c, rr);  // FWD1/DA: fixed for the tile
@@ -519,7 +704,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         uint8_t* sA = smem + stage * sstride;
         uint8_t* sB = sA + astride;
         if (p == 0 && lane == 0) produce_tiles<KIND>(a, ti, kb, sA, sB, &full[stage]);
-        if (has_call) {
+        if (kind_gather_a(KIND) && a.exp_flag == 1) {  // EXPERIMENT: contiguous A instead of gather
+          if (has_call && c == 0)
+            tma_load_2d(sA, &a.tc, &full[stage], kb * 64, (int)(ti.prow0 % (a.T - 128 > 0 ? a.T - 128 : 1)));
+        } else if (has_call) {
           issue_gather<KIND>(a, ti, kb, c, rr, sA, sB, &full[stage]);
           if (kind_gather_b(KIND) && kb + 1 < ti.nkb) gather_rows<KIND>(a, ti, kb + 1, c, rr);
         }
@@ -549,8 +737,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
                                      : sdesc_sw128(sb + k * 32, 16, 1024);
             for (int h = 0; h < a.MH; ++h) {
               const uint64_t ad = kAmn ? sdesc_sw128(sa + h * 16384 + k * 2048, 8192, 1024)
-                                       : sdesc_sw128(sa + k * 32, 16, 1024);
-              const uint32_t dtm = tmem + (n_acc == 2 ? acc : h) * 256;
+                                       : sdesc_sw128(sa + h * 16384 + k * 32, 16, 1024);
+              const uint32_t dtm = tmem + tm_col(a.BN, a.MH, acc, h);
               mma_bf16(dtm, ad, bd, idesc, (kb | k) != 0);
             }
           }
@@ -574,8 +762,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       const TileInfo ti = decode<KIND>(a, tile);
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const uint32_t col0 = (n_acc == 2 ? acc : (a.MH == 2 ? half : 0)) * 256;
-      epilogue<KIND>(a, ti, tmem + ((uint32_t)(q * 32) << 16) + col0, row, half, dg_xchg);
+      const uint32_t lanes = (uint32_t)(q * 32) << 16;
+      if (kind_gather_a(KIND) && a.MH == 2) {
+        // M half `half` of a pair tile: this warp group owns its rows, all columns
+        TileInfo th = ti;
+        th.n_valid -= half * 128;
+        th.prow0 += half * 128;
+        th.pos0 += half * 128;
+        if (half * 128 < ti.rows_pad)  // the second m-tile may not exist: write nothing
+          epilogue<KIND>(a, th, tmem + lanes + tm_col(a.BN, a.MH, acc, half), row, -1, dg_xchg);
+      } else {
+        const uint32_t col0 = tm_col(a.BN, a.MH, acc, a.MH == 2 ? half : 0);
+        epilogue<KIND>(a, ti, tmem + lanes + col0, row, half, dg_xchg);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -615,8 +814,15 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   const int bst = (b_bytes(KIND, a.BN) + 1023) & ~1023;
   const int sst = kABytes * a.MH + bst;
   const int extra = 1024 + 256 + 512;  // alignment slack + barriers + DA exchange
-  int stages = std::min(6, (227 * 1024 - extra) / sst);
-  const int smem = stages * sst + extra;
+  // weight-resident kinds: the slab (K stages x 32 KB) is carved before the A ring
+  const int slab = kind_bres(KIND)
+                       ? (KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64) * 32768
+                       : 0;
+  // FWD2 keeps 2 staging buffers per epilogue warp, DX (128 KB slab) keeps 1
+  if (kind_bres(KIND)) a.n_stg = slab > 65536 ? 1 : 2;
+  const int stg = kind_bres(KIND) ? kEpiWarps * a.n_stg * 4096 + 1024 : 0;
+  int stages = std::min(kind_bres(KIND) ? 8 : 6, (227 * 1024 - extra - slab - stg) / sst);
+  const int smem = slab + stages * sst + extra + stg;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<KIND>,
@@ -653,6 +859,12 @@ static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
   a.gpad = g.gpad;
   a.NT = (int)ceil_div(g.d, 256);
   a.MH = 1;
+  static int exp_flag = -1;
+  if (exp_flag < 0) {
+    const char* e = getenv("SPT_FFN_EXPERIMENT");
+    exp_flag = e ? atoi(e) : 0;
+  }
+  a.exp_flag = exp_flag;
 }
 
 static int bucket_tiles_upper(const Geom& g) { return (int)(ceil_div(g.pairs, 128) + g.G); }
@@ -689,27 +901,90 @@ cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logi
   return cudaSuccess;
 }
 
+// Device-side tile schedules from the bucket layout (no host sync):
+//  tile_list[P(mt) + rank_b(mt)] = mt << 8 | b, i.e. bucket tiles in (m-tile,
+//  block) order with P(mt) = sum_b min(nt_b, mt) and rank_b(mt) = #{b' < b :
+//  nt_b' > mt};  unit_offsets = prefix over blocks of ceil(nt_b/16) * NT.
+__global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, const int32_t* __restrict__ tile_offsets,
+                                                         int32_t* __restrict__ tile_list,
+                                                         int32_t* __restrict__ unit_offsets) {
+  __shared__ int ntb[kMaxBlocks];
+  __shared__ int ntu[kMaxBlocks];  // 128-row tiles per block (units) ...
+  for (int i = threadIdx.x; i < G; i += blockDim.x) {
+    ntu[i] = tile_offsets[i + 1] - tile_offsets[i];
+    ntb[i] = (ntu[i] + 1) / 2;  // ... and 256-row pair tiles (gathered-A kinds)
+  }
+  __syncthreads();
+  // 2-D raster: groups of kRasterBlocks blocks, inside a group (m-tile, block)
+  // order.  The group's weights (<= 32 MB of W1 rows) and the window of tokens
+  // the in-flight m-levels gather both stay in L2.
+  const int b = blockIdx.x;
+  const int g0 = (b / kRasterBlocks) * kRasterBlocks, g1 = min(G, g0 + kRasterBlocks);
+  int base = 0;
+  for (int bb = 0; bb < g0; ++bb) base += ntb[bb];
+  for (int mt = threadIdx.x; mt < ntb[b]; mt += blockDim.x) {
+    int P = base, rank = 0;
+    for (int bb = g0; bb < g1; ++bb) {
+      P += min(ntb[bb], mt);
+      rank += (bb < b) && (ntb[bb] > mt);
+    }
+    tile_list[P + rank] = (mt << 8) | b;
+  }
+  if (b == 0 && threadIdx.x == 0) {
+    int run = 0;
+    for (int bb = 0; bb < G; ++bb) {
+      unit_offsets[bb] = run;
+      run += (int)ceil_div(ntu[bb], kUnitMTiles) * NT;
+    }
+    unit_offsets[G] = run;
+    int pairs = 0;
+    for (int bb = 0; bb < G; ++bb) pairs += ntb[bb];
+    unit_offsets[G + 1] = pairs;
+  }
+}
+
+static cudaError_t build_schedules(const Geom& g, const RouteView& r, const Bufs& b, cudaStream_t s) {
+  prof_begin("tile_sched", s);
+  tile_sched_kernel<<<g.G, 256, 0, s>>>(g.G, (int)ceil_div(g.d, 256), r.tile_offsets, b.tile_list,
+                                        b.unit_offsets);
+  prof_end(s);
+  count_launch();
+  return cudaGetLastError();
+}
+
+static int units_upper(const Geom& g) {
+  return (int)((ceil_div(bucket_tiles_upper(g), kUnitMTiles) + g.G) * ceil_div(g.d, 256));
+}
+
 cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void* w2,
                        const RouteView& r, void* y, const Bufs& b, cudaStream_t s) {
   const int up = bucket_tiles_upper(g);
+  cudaError_t e0 = build_schedules(g, r, b, s);
+  if (e0 != cudaSuccess) return e0;
   {
     TcArgs a{};
     base_args(a, g, r);
+    a.tile_list = b.tile_list;
     bool ok = make_tmap_bf16_2d(&a.ta, x, g.T, g.d, g.d, 64, 1) &&
-              make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, g.bw);
+              make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, g.bw) &&
+              make_tmap_bf16_2d(&a.tc, x, g.T, g.d, g.d, 64, 128);  // experiment only
     a.BN = g.mp * g.bw;
+    a.MH = 2;
     a.out = b.z;
     a.out2 = b.h;
-    TRY(launch<K_FWD1>(a, up, s));
+    a.unit_offsets = b.unit_offsets;
+    TRY(launch<K_FWD1>(a, up / 2 + g.G, s));
   }
   {
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, 128) &&
               make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, 64);
+    ok = ok && make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
     a.BN = 256;
     a.out = b.part;
-    TRY(launch<K_FWD2>(a, up * a.NT, s));
+    a.unit_offsets = b.unit_offsets;
+    TRY(launch<K_FWD2>(a, units_upper(g), s));
   }
   return launch_combine_fwd(g, r, b.part, y, s);
 }
@@ -729,20 +1004,26 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
                         cudaStream_t s) {
   const int up = bucket_tiles_upper(g);
   const bool sig = g.gate == SPT_GATE_SIGMOID;
+  cudaError_t e0 = build_schedules(g, r, b, s);
+  if (e0 != cudaSuccess) return e0;
   if (sig && cudaMemsetAsync(b.dlg, 0, (size_t)2 * g.T * g.gpad * 2, s) != cudaSuccess)
     return cudaErrorUnknown;
   {  // a7: dA = dY[bucket] W2_b^T with the dgate / dZ / dlogit epilogue
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, dy, g.T, g.d, g.d, 64, 1) &&
-              make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, g.bw);
+              make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, g.bw) &&
+              make_tmap_bf16_2d(&a.tc, dy, g.T, g.d, g.d, 64, 128);  // experiment only
     a.BN = g.bw;
     a.aux = b.z;
     a.out2 = b.dz;
     a.rows_f = b.dgate;
     a.rows_g = b.dlogit;
     a.dlg = b.dlg;
-    TRY(launch<K_DA>(a, up, s));
+    a.tile_list = b.tile_list;
+    a.MH = 2;
+    a.unit_offsets = b.unit_offsets;
+    TRY(launch<K_DA>(a, up / 2 + g.G, s));
   }
   {  // a8: dXp = dZ W1_b, then combine with the router term
     TcArgs a{};
@@ -750,9 +1031,11 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
                                 (uint64_t)g.mp * g.bw, 64, 128) &&
               make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, 64);
+    ok = ok && make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
     a.BN = 256;
     a.out = b.part;
-    TRY(launch<K_DX>(a, up * a.NT, s));
+    a.unit_offsets = b.unit_offsets;
+    TRY(launch<K_DX>(a, units_upper(g), s));
   }
   cudaError_t e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
   if (e != cudaSuccess) return e;
