@@ -75,6 +75,23 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uin
       "r"(smem_u32(bar))
       : "memory");
 }
+// --------------------------------------------------- cp.async (LSU) gathers
+// 16-byte global -> shared copy, zero-filled when src_bytes == 0 (L2-only .cg)
+__device__ __forceinline__ void cp_async_16(uint32_t dst_smem, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+// arrive on `bar` once all of this thread's prior cp.async have landed; the
+// arrival counts toward the barrier's expected count (.noinc)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // smem -> global tensor store (bulk group); source must be visible to the async
 // proxy (fence_proxy_async_smem) before the call
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0,

@@ -2,7 +2,7 @@
 //
 // One persistent, warp-specialised tcgen05 kernel template serves every GEMM
 // on the hot path:
-//   warps 0,10,11  TMA producers.  Warp 0 lane 0 issues the tile loads; the
+//   warp 0         TMA tile producer (weights / contiguous operands)
 //                  gather4 loads (4 token rows x 128 B each) of a stage are spread
 //                  over the lanes of all three warps (three SM sub-partitions);
 //                  each producer warp arms the stage barrier for its own bytes.
@@ -59,18 +59,29 @@ struct TcArgs {
   void* out;       // kind-specific primary output
   void* out2;      // secondary output (FWD1: h; DA: dz)
   const void* aux; // DA: z stash
+  const void* aux2;  // gathering kinds: the tensor whose rows are gathered (x or dy)
   float* rows_f;   // DA: dgate rows
   float* rows_g;   // DA: dlogit rows
   void* dlg;       // DA: dense dlogits [2][T][gpad] bf16
   const int32_t* tile_list;     // FWD1/DA: (mt << 8 | b) in m-tile-major order
   const int32_t* unit_offsets;  // FWD2/DX: weight-resident unit prefix per block
   int n_stg;                    // FWD2/DX: 4 KB staging buffers per epilogue warp (1 or 2)
-  int exp_flag;                 // experiment switch (SPT_FFN_EXPERIMENT), timing only
+
 };
 
-constexpr int kProducers = 3;                 // warps 0, 10, 11
-constexpr int kEpiWarps = 8;                  // warps 2..9
-constexpr int kThreads = 32 * (2 + kEpiWarps + kProducers - 1);  // 384
+// 12 warps.  warp 0: TMA tile producer; warp 1: TMEM alloc + MMA issuer.
+//  FWD1 / DA (rows of A gathered): warps 0, 2, 3 issue TMA tile::gather4 (each
+//    arms the stage barrier for its own bytes); warps 4-11 epilogue.
+//  DW1 / DW2 (rows of B gathered along K): warps 2, 3, 8-11 copy rows with
+//    cp.async (16 B per thread, straight into the swizzled layout); warps 4-7
+//    epilogue (it is short next to the K = n_b mainloop).
+//  other kinds: warps 4-11 epilogue.
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;                  // warps 4..11
+constexpr int kGEpiWarps = 4;                 // DW kinds: warps 4..7
+constexpr int kGatherWarps = 6;               // DW kinds: warps 2, 3, 8..11
+constexpr int kGatherThreads = 32 * kGatherWarps;
+constexpr int kTmaGatherWarps = 3;            // FWD1 / DA: warps 0, 2, 3
 constexpr int kABytes = 16384;                // 128 rows x 64 bf16
 
 __host__ __device__ constexpr bool kind_gather_a(int k) { return k == K_FWD1 || k == K_DA; }
@@ -191,12 +202,6 @@ __device__ __forceinline__ TileInfo decode_mtile(const TcArgs& a, const UnitInfo
   return ti;
 }
 
-// gather4 calls per stage (each moves 4 rows x 128 B)
-template <int KIND>
-__host__ __device__ constexpr int gather_calls(int MH) {
-  return kind_gather_a(KIND) ? 32 * MH : (kind_gather_b(KIND) ? 64 : 0);
-}
-
 // bytes of the tile (non-gather) loads of one stage, issued by warp 0 lane 0
 template <int KIND>
 __device__ __forceinline__ uint32_t tile_tx_bytes(const TcArgs& a) {
@@ -237,33 +242,6 @@ __device__ __forceinline__ void produce_tiles(const TcArgs& a, const TileInfo& t
     for (int j = 0; j < 2; ++j) tma_load_2d(sA + j * 8192, &a.ta, bar, j * 64, (int)(part * a.T) + trow);
 #pragma unroll
     for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, trow);
-  }
-}
-
-// Gather rows of call `c` at stage kb (FWD1/DA: A rows 4c..4c+3 of the tile;
-// DW*: B row group rg = c >> 2, 64-column chunk j = c & 3, rows kb*64 + 4rg ..)
-template <int KIND>
-__device__ __forceinline__ void gather_rows(const TcArgs& a, const TileInfo& ti, int kb, int c,
-                                            int (&rr)[4]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int e;
-    if (kind_gather_a(KIND)) e = 4 * c + i;                 // row within the M tile
-    else e = kb * 64 + (c >> 2) * 4 + i;                    // entry within the block bucket
-    rr[i] = e < ti.n_valid ? a.r.bucket_token[ti.pos0 + e] : (int)a.T;  // T -> OOB -> zeros
-  }
-}
-
-template <int KIND>
-__device__ __forceinline__ void issue_gather(const TcArgs& a, const TileInfo& ti, int kb, int c,
-                                             const int (&rr)[4], uint8_t* sA, uint8_t* sB,
-                                             uint64_t* bar) {
-  if (kind_gather_a(KIND)) {
-    tma_gather4(sA + c * 512, &a.ta, bar, kb * 64, rr[0], rr[1], rr[2], rr[3]);
-  } else {
-    const int j = c & 3, rg = c >> 2;
-    tma_gather4(sB + j * 8192 + rg * 512, &a.tb, bar, ti.nt * 256 + j * 64, rr[0], rr[1], rr[2],
-                rr[3]);
   }
 }
 
@@ -565,18 +543,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // two accumulators alternate between tiles when both fit in TMEM
   const int n_acc = tm_nacc(a.BN, a.MH);
+  constexpr bool kGather = kind_gather_b(KIND);  // cp.async row gathers
+  const int n_epi = kGather ? kGEpiWarps : kEpiWarps;
   if (threadIdx.x == 0) {
-    // gathering kinds: each of the 3 producer warps arms its own bytes
-    const int n_prod = (kind_gather_a(KIND) || kind_gather_b(KIND)) ? kProducers : 1;
+    // stage barrier: warp 0's TMA arm (+ expected bytes); FWD1 / DA: one arm
+    // per gather4 warp; DW*: one cp.async completion arrival per gather thread
     for (int s = 0; s < n_stages; ++s) {
-      mbar_init(&full[s], n_prod);
+      mbar_init(&full[s], kGather ? 1 + kGatherThreads
+                                  : (kind_gather_a(KIND) ? kTmaGatherWarps : 1));
       mbar_init(&empty[s], 1);
     }
     mbar_init(bres_full, 1);
     mbar_init(bres_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
+      mbar_init(&tempty[i], n_epi);
     }
     fence_barrier_init();
   }
@@ -656,8 +637,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
       }
       __syncwarp();
-    } else if (warp >= 2 && warp < 2 + kEpiWarps) {
-      const int e = warp - 2;
+    } else if (warp >= 4 && warp < 4 + kEpiWarps) {
+      const int e = warp - 4;
       const int q = warp & 3;
       const int half = e >> 2;
       int acc = 0, stg_i = 0;
@@ -678,23 +659,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       }
       if (lane == 0) bulk_wait<0>();  // all partial tiles written before exit
     }
-  } else if (warp == 0 || warp >= 2 + kEpiWarps) {
-    // ---------------------------------------------------------- producers
-    const int p = warp == 0 ? 0 : warp - (2 + kEpiWarps) + 1;  // 0, 1, 2
-    const int c = lane * kProducers + p;                         // gather call of this lane
-    const int kCalls = gather_calls<KIND>(a.MH);
-    const bool has_call = c < kCalls;
-    // active gather calls in this warp: lanes l with l*3 + p < kCalls
-    const int my_calls = kCalls > p ? (kCalls - p + kProducers - 1) / kProducers : 0;
-    uint32_t tx = (uint32_t)my_calls * 512u + (p == 0 ? tile_tx_bytes<KIND>(a) : 0u);
-    if (kind_gather_a(KIND) && a.exp_flag == 1) tx = p == 0 ? kABytes + tile_tx_bytes<KIND>(a) : 0u;
+  } else if (kind_gather_a(KIND) && (warp == 0 || warp == 2 || warp == 3)) {
+    // ------------------------ FWD1 / DA: TMA tile::gather4 of 256 token rows
+    const int p = warp == 0 ? 0 : warp - 1;   // 0, 1, 2
+    const int c = lane * kTmaGatherWarps + p;  // gather call of this lane: rows 4c..4c+3
+    const int n_calls = 32 * a.MH;
+    const bool has_call = c < n_calls;
+    const int my_calls = n_calls > p ? (n_calls - p + kTmaGatherWarps - 1) / kTmaGatherWarps : 0;
+    const uint32_t tx = (uint32_t)my_calls * 512u + (p == 0 ? tile_tx_bytes<KIND>(a) : 0u);
     int stage = 0;
     uint32_t phase = 0;
-    const int ntiles_p = (p == 0 || kCalls > 0) ? ntiles : 0;  // non-gathering kinds: warp 0 only
-    for (int tile = blockIdx.x; tile < ntiles_p; tile += gridDim.x) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo ti = decode<KIND>(a, tile);
-      int rr[4] = {0, 0, 0, 0};
-      if (has_call) gather_rows<KIND>(a, ti, 0, c, rr);  // FWD1/DA: fixed for the tile
+      int rr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * c + i;
+        rr[i] = (has_call && r < ti.n_valid) ? a.r.bucket_token[ti.pos0 + r] : (int)a.T;
+      }
       for (int kb = 0; kb < ti.nkb; ++kb) {
         if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -702,15 +684,68 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
         __syncwarp();
         uint8_t* sA = smem + stage * sstride;
-        uint8_t* sB = sA + astride;
-        if (p == 0 && lane == 0) produce_tiles<KIND>(a, ti, kb, sA, sB, &full[stage]);
-        if (kind_gather_a(KIND) && a.exp_flag == 1) {  // EXPERIMENT: contiguous A instead of gather
-          if (has_call && c == 0)
-            tma_load_2d(sA, &a.tc, &full[stage], kb * 64, (int)(ti.prow0 % (a.T - 128 > 0 ? a.T - 128 : 1)));
-        } else if (has_call) {
-          issue_gather<KIND>(a, ti, kb, c, rr, sA, sB, &full[stage]);
-          if (kind_gather_b(KIND) && kb + 1 < ti.nkb) gather_rows<KIND>(a, ti, kb + 1, c, rr);
+        if (p == 0 && lane == 0) produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
+        if (has_call)
+          tma_gather4(sA + c * 512, &a.ta, &full[stage], kb * 64, rr[0], rr[1], rr[2], rr[3]);
+        if (++stage == n_stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 0) {
+    // ------------------------------------------------- TMA tile producer
+    if (lane == 0) {
+      const uint32_t tx = tile_tx_bytes<KIND>(a);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const TileInfo ti = decode<KIND>(a, tile);
+        for (int kb = 0; kb < ti.nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], tx);
+          uint8_t* sA = smem + stage * sstride;
+          produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
+          if (++stage == n_stages) { stage = 0; phase ^= 1; }
         }
+      }
+    }
+  } else if (kGather && (warp == 2 || warp == 3 || warp >= 8)) {
+    // -------------------------- DW*: cp.async row gathers of B (6 warps)
+    // B: 64 bucket rows (K) x 256 columns (N) per stage, MN-major: 64-column
+    // chunk j at +8 KB*j, K row r at +128 B*r, 16-byte piece p swizzled by r.
+    // This thread: piece (gt & 31) of rows r_i = (gt >> 5) + 6 i.  Its
+    // arrival on the stage barrier fires when its copies have landed.
+    const int gt = (warp < 4 ? warp - 2 : warp - 6) * 32 + lane;  // 0..191
+    const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
+    const int j = (gt & 31) >> 3, pc = gt & 7;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const TileInfo ti = decode<KIND>(a, tile);
+      int tok[11];
+      auto load_idx = [&](int kb) {
+#pragma unroll
+        for (int i = 0; i < 11; ++i) {
+          const int r = (gt >> 5) + 6 * i;
+          const int e = kb * 64 + r;
+          tok[i] = (r < 64 && e < ti.n_valid) ? a.r.bucket_token[ti.pos0 + e] : -1;
+        }
+      };
+      if (ti.nkb > 0) load_idx(0);
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
+        __syncwarp();
+        const uint32_t sB = smem_u32(smem + stage * sstride + astride);
+#pragma unroll
+        for (int i = 0; i < 11; ++i) {
+          const int r = (gt >> 5) + 6 * i;
+          if (r < 64) {
+            const uint32_t dst = sB + j * 8192 + r * 128 + ((pc ^ (r & 7)) << 4);
+            const __nv_bfloat16* g =
+                src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + ti.nt * 256 + j * 64 + pc * 8;
+            cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
+          }
+        }
+        cp_async_arrive_noinc(&full[stage]);
+        if (kb + 1 < ti.nkb) load_idx(kb + 1);
         if (++stage == n_stages) { stage = 0; phase ^= 1; }
       }
     }
@@ -728,6 +763,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         tc_fence_after();
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(&full[stage], phase);
+          // cp.async writes are generic-proxy: order them before the UMMA reads
+          if (kGather) fence_proxy_async_smem();
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * sstride);
           const uint32_t sb = sa + astride;
@@ -750,11 +787,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       __syncwarp();
       if (++acc == n_acc) { acc = 0; aphase ^= 1; }
     }
-  } else {
+  } else if (warp >= 4 && warp < 4 + n_epi) {
     // --------------------------------------------------------- epilogue
-    const int e = warp - 2;
+    const int e = warp - 4;
     const int q = warp & 3;   // TMEM lane quarter this warp may access
-    const int half = e >> 2;  // column half (or M half when MH == 2)
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t aphase = 0;
@@ -763,17 +799,25 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const uint32_t lanes = (uint32_t)(q * 32) << 16;
-      if (kind_gather_a(KIND) && a.MH == 2) {
-        // M half `half` of a pair tile: this warp group owns its rows, all columns
-        TileInfo th = ti;
-        th.n_valid -= half * 128;
-        th.prow0 += half * 128;
-        th.pos0 += half * 128;
-        if (half * 128 < ti.rows_pad)  // the second m-tile may not exist: write nothing
-          epilogue<KIND>(a, th, tmem + lanes + tm_col(a.BN, a.MH, acc, half), row, -1, dg_xchg);
+      if (kGather) {
+        // DW*: 4 warps (one per lane quarter) cover both halves:
+        // MH == 2 -> accumulator h (features h*128 + row); MH == 1 -> column half h
+        for (int h = 0; h < 2; ++h)
+          epilogue<KIND>(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, a.MH == 2 ? h : 0), row, h,
+                         dg_xchg);
       } else {
-        const uint32_t col0 = tm_col(a.BN, a.MH, acc, a.MH == 2 ? half : 0);
-        epilogue<KIND>(a, ti, tmem + lanes + col0, row, half, dg_xchg);
+        const int half = e >> 2;  // warp group: M half (pair tiles) or column half
+        if (kind_gather_a(KIND) && a.MH == 2) {
+          // M half `half` of a pair tile: this warp group owns its rows, all columns
+          TileInfo th = ti;
+          th.n_valid -= half * 128;
+          th.prow0 += half * 128;
+          th.pos0 += half * 128;
+          if (half * 128 < ti.rows_pad)  // the second m-tile may not exist: write nothing
+            epilogue<KIND>(a, th, tmem + lanes + tm_col(a.BN, a.MH, acc, half), row, -1, dg_xchg);
+        } else {
+          epilogue<KIND>(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, 0), row, half, dg_xchg);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -859,12 +903,7 @@ static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
   a.gpad = g.gpad;
   a.NT = (int)ceil_div(g.d, 256);
   a.MH = 1;
-  static int exp_flag = -1;
-  if (exp_flag < 0) {
-    const char* e = getenv("SPT_FFN_EXPERIMENT");
-    exp_flag = e ? atoi(e) : 0;
-  }
-  a.exp_flag = exp_flag;
+
 }
 
 static int bucket_tiles_upper(const Geom& g) { return (int)(ceil_div(g.pairs, 128) + g.G); }
@@ -970,6 +1009,7 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
               make_tmap_bf16_2d(&a.tc, x, g.T, g.d, g.d, 64, 128);  // experiment only
     a.BN = g.mp * g.bw;
     a.MH = 2;
+    a.aux2 = x;
     a.out = b.z;
     a.out2 = b.h;
     a.unit_offsets = b.unit_offsets;
@@ -1022,6 +1062,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.dlg = b.dlg;
     a.tile_list = b.tile_list;
     a.MH = 2;
+    a.aux2 = dy;
     a.unit_offsets = b.unit_offsets;
     TRY(launch<K_DA>(a, up / 2 + g.G, s));
   }
@@ -1047,6 +1088,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
               make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 1);
     a.BN = 256;
     a.MH = (int)ceil_div(g.mp * g.bw, 128);
+    a.aux2 = x;
     a.out = dw1;
     a.acc_mode = accumulate;
     TRY(launch<K_DW1>(a, g.G * a.NT, s));
@@ -1058,6 +1100,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
               make_tmap_bf16_2d(&a.tb, dy, g.T, g.d, g.d, 64, 1);
     a.BN = 256;
     a.MH = (int)ceil_div(g.bw, 128);
+    a.aux2 = dy;
     a.out = dw2;
     a.acc_mode = accumulate;
     TRY(launch<K_DW2>(a, g.G * a.NT, s));
