@@ -114,6 +114,19 @@ template <int N>
 __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+// L2 prefetch of 4 gathered rows x box[0] columns (no smem, no barrier)
+__device__ __forceinline__ void tma_prefetch_gather4(const CUtensorMap* m, int32_t c0, int32_t r0,
+                                                     int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+// L2 prefetch of a contiguous global range (bytes: multiple of 16)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 // L2 cache-policy descriptors for the .L2::cache_hint variants
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;

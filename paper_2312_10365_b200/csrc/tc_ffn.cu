@@ -66,22 +66,27 @@ struct TcArgs {
   const int32_t* tile_list;     // FWD1/DA: (mt << 8 | b) in m-tile-major order
   const int32_t* unit_offsets;  // FWD2/DX: weight-resident unit prefix per block
   int n_stg;                    // FWD2/DX: 4 KB staging buffers per epilogue warp (1 or 2)
+  int prefetch;                 // gathering kinds: L2 prefetch of gathered rows (SPT_FFN_PREFETCH)
+  unsigned long long* trace;    // SPT_FFN_TRACE: per-CTA role cycle counters (diagnostics)
+  int ablate;                   // SPT_FFN_ABLATE (timing experiments only; results wrong):
+                                //  1 = skip gathered-row copies, 2 = skip FWD1 epilogue stores
 
 };
 
-// 12 warps.  warp 0: TMA tile producer; warp 1: TMEM alloc + MMA issuer.
-//  FWD1 / DA (rows of A gathered): warps 0, 2, 3 issue TMA tile::gather4 (each
-//    arms the stage barrier for its own bytes); warps 4-11 epilogue.
-//  DW1 / DW2 (rows of B gathered along K): warps 2, 3, 8-11 copy rows with
-//    cp.async (16 B per thread, straight into the swizzled layout); warps 4-7
-//    epilogue (it is short next to the K = n_b mainloop).
-//  other kinds: warps 4-11 epilogue.
-constexpr int kThreads = 384;
+// 16 warps.  warp 0: TMA tile producer; warp 1: TMEM alloc + MMA issuer;
+// warps 4-11: epilogue (two warps per TMEM lane quarter).  Row gathers use both
+// copy engines (measured on B200, tools/gather_bench.cu: TMA gather4 from 3
+// warps ~16-20 B/clk/SM, cp.async from 8 warps ~22-24 B/clk/SM; independent):
+//  FWD1 / DA (rows of A gathered): rows [0,128) of a 256-row stage by TMA
+//    tile::gather4 from warps 0, 2, 3 (each arms the stage barrier for its own
+//    bytes), rows [128,256) by cp.async from warps 12-15.
+//  DW1 / DW2 (rows of B gathered along K): cp.async from warps 2, 3, 12-15.
+constexpr int kThreads = 512;
 constexpr int kEpiWarps = 8;                  // warps 4..11
-constexpr int kGEpiWarps = 4;                 // DW kinds: warps 4..7
-constexpr int kGatherWarps = 6;               // DW kinds: warps 2, 3, 8..11
-constexpr int kGatherThreads = 32 * kGatherWarps;
 constexpr int kTmaGatherWarps = 3;            // FWD1 / DA: warps 0, 2, 3
+constexpr int kTmaRows = 128;                 // FWD1 / DA: rows per stage gathered by TMA
+constexpr int kCpThreadsA = 128;              // FWD1 / DA: cp.async warps 12..15
+constexpr int kCpThreadsB = 192;              // DW*: cp.async warps 2, 3, 12..15
 constexpr int kABytes = 16384;                // 128 rows x 64 bf16
 
 __host__ __device__ constexpr bool kind_gather_a(int k) { return k == K_FWD1 || k == K_DA; }
@@ -288,20 +293,21 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
       }
     }
   } else if (KIND == K_FWD1) {
+    // 16 units per step (register budget: the kernel runs 512 threads)
     const float g = valid ? a.r.bucket_gate[ti.pos0 + row] : 0.f;
     const int64_t prow = ti.prow0 + row;
     __nv_bfloat16* zr = (__nv_bfloat16*)a.out + prow * (int64_t)(a.mp * a.bw);
     __nv_bfloat16* hr = (__nv_bfloat16*)a.out2 + prow * (int64_t)a.bw;
-    const int hw = ((a.bw / 2) + 31) & ~31;
+    const int hw = ((a.bw / 2) + 15) & ~15;
     const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? a.bw : min(a.bw, u_lo + hw);
-    for (int u0 = u_lo; u0 < u_hi; u0 += 32) {
-      uint32_t vg[32], vu[32];
-      tmem_ld32(tacc + u0, vg);
-      if (a.mp == 2) tmem_ld32(tacc + a.bw + u0, vu);
+    for (int u0 = u_lo; u0 < u_hi; u0 += 16) {
+      uint32_t vg[16], vu[16];
+      tmem_ld16(tacc + u0, vg);
+      if (a.mp == 2) tmem_ld16(tacc + a.bw + u0, vu);
       tmem_ld_wait();
-      uint32_t pz[16], pu[16], ph[16];
+      uint32_t pz[8], pu[8], ph[8];
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
+      for (int i = 0; i < 16; i += 2) {
         const float z0 = valid ? __uint_as_float(vg[i]) : 0.f;
         const float z1 = valid ? __uint_as_float(vg[i + 1]) : 0.f;
         float u0f = 0.f, u1f = 0.f;
@@ -311,19 +317,20 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
           pu[i / 2] = pack_bf16(u0f, u1f);
         }
         pz[i / 2] = pack_bf16(z0, z1);
-        ph[i / 2] = pack_bf16(g * act_fwd(a.act, z0, u0f), g * act_fwd(a.act, z1, u1f));
+        ph[i / 2] = pack_bf16(g * act_fwd<true>(a.act, z0, u0f), g * act_fwd<true>(a.act, z1, u1f));
       }
+      if (a.ablate == 2) continue;
       uint4* zd = reinterpret_cast<uint4*>(zr + u0);
       uint4* hd = reinterpret_cast<uint4*>(hr + u0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 2; ++q) {
         zd[q] = make_uint4(pz[4 * q], pz[4 * q + 1], pz[4 * q + 2], pz[4 * q + 3]);
         hd[q] = make_uint4(ph[4 * q], ph[4 * q + 1], ph[4 * q + 2], ph[4 * q + 3]);
       }
       if (a.mp == 2) {
         uint4* ud = reinterpret_cast<uint4*>(zr + a.bw + u0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ud[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
+        for (int q = 0; q < 2; ++q) ud[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
       }
     }
   } else if (KIND == K_FWD2 || KIND == K_DX) {
@@ -342,33 +349,33 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     const float g = valid ? a.r.bucket_gate[ti.pos0 + row] : 0.f;
     const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + prow * (int64_t)(a.mp * a.bw);
     __nv_bfloat16* dzr = (__nv_bfloat16*)a.out2 + prow * (int64_t)(a.mp * a.bw);
-    const int hw = ((a.bw / 2) + 31) & ~31;
+    const int hw = ((a.bw / 2) + 15) & ~15;
     const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? a.bw : min(a.bw, u_lo + hw);
     float dgate = 0.f;
-    for (int u0 = u_lo; u0 < u_hi; u0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(tacc + u0, v);
+    for (int u0 = u_lo; u0 < u_hi; u0 += 16) {  // 16 units per step (register budget)
+      uint32_t v[16];
+      tmem_ld16(tacc + u0, v);
       tmem_ld_wait();
-      uint32_t zg4[16], zu4[16];
+      uint32_t zg4[8], zu4[8];
       if (valid) {
         const uint4* zs = reinterpret_cast<const uint4*>(zr + u0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 2; ++q) {
           const uint4 w = zs[q];
           zg4[4 * q] = w.x; zg4[4 * q + 1] = w.y; zg4[4 * q + 2] = w.z; zg4[4 * q + 3] = w.w;
         }
         if (a.mp == 2) {
           const uint4* us = reinterpret_cast<const uint4*>(zr + a.bw + u0);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 2; ++q) {
             const uint4 w = us[q];
             zu4[4 * q] = w.x; zu4[4 * q + 1] = w.y; zu4[4 * q + 2] = w.z; zu4[4 * q + 3] = w.w;
           }
         }
       }
-      uint32_t pg[16], pu[16];
+      uint32_t pg[8], pu[8];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < 16; ++i) {
         float dA = 0.f, zg = 0.f, zu = 0.f;
         if (valid) {
           dA = __uint_as_float(v[i]);
@@ -380,7 +387,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
           }
         }
         float av, dg, du;
-        act_fwd_bwd(a.act, zg, zu, av, dg, du);
+        act_fwd_bwd<true>(a.act, zg, zu, av, dg, du);
         dgate = fmaf(dA, av, dgate);
         const float dzg = g * dA * dg, dzu = g * dA * du;
         const uint32_t bg = __bfloat16_as_ushort(__float2bfloat16(dzg));
@@ -390,11 +397,11 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
       }
       uint4* d4 = reinterpret_cast<uint4*>(dzr + u0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) d4[q] = make_uint4(pg[4 * q], pg[4 * q + 1], pg[4 * q + 2], pg[4 * q + 3]);
+      for (int q = 0; q < 2; ++q) d4[q] = make_uint4(pg[4 * q], pg[4 * q + 1], pg[4 * q + 2], pg[4 * q + 3]);
       if (a.mp == 2) {
         uint4* u4 = reinterpret_cast<uint4*>(dzr + a.bw + u0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) u4[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
+        for (int q = 0; q < 2; ++q) u4[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
       }
     }
     // column-split epilogue: combine the two halves' partial dgate (half 1 ->
@@ -514,6 +521,20 @@ __device__ __forceinline__ void epilogue_tma_store(const TcArgs& a, const TileIn
   }
 }
 
+// diagnostics: cycles spent in an mbarrier wait, accumulated into trace slot
+__device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, unsigned long long* tr, int slot) {
+  if (tr) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    tr[slot] += (unsigned long long)(clock64() - t0);
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
+// trace slots (per CTA, 8 x u64): 0 MMA wait full, 1 MMA wait tempty, 2 epi wait tfull,
+// 3 epi busy, 4 TMA producer wait empty, 5 gather wait empty, 6 total cycles, 7 tiles
+constexpr int kTraceSlots = 8;
+
 // ------------------------------------------------------------------ kernel
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcArgs a,
@@ -543,14 +564,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // two accumulators alternate between tiles when both fit in TMEM
   const int n_acc = tm_nacc(a.BN, a.MH);
-  constexpr bool kGather = kind_gather_b(KIND);  // cp.async row gathers
-  const int n_epi = kGather ? kGEpiWarps : kEpiWarps;
+  constexpr bool kGather = kind_gather_a(KIND) || kind_gather_b(KIND);  // uses cp.async
+  const int n_epi = kEpiWarps;
   if (threadIdx.x == 0) {
     // stage barrier: warp 0's TMA arm (+ expected bytes); FWD1 / DA: one arm
     // per gather4 warp; DW*: one cp.async completion arrival per gather thread
     for (int s = 0; s < n_stages; ++s) {
-      mbar_init(&full[s], kGather ? 1 + kGatherThreads
-                                  : (kind_gather_a(KIND) ? kTmaGatherWarps : 1));
+      mbar_init(&full[s], kind_gather_b(KIND) ? 1 + kCpThreadsB
+                          : (kind_gather_a(KIND) ? kTmaGatherWarps + kCpThreadsA : 1));
       mbar_init(&empty[s], 1);
     }
     mbar_init(bres_full, 1);
@@ -571,6 +592,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int ntiles = num_tiles<KIND>(a);
+  unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  const long long t_start = clock64();
 
   if (kind_bres(KIND)) {
     // ============ weight-resident units (FWD2 / DX): B slab once per unit
@@ -663,10 +686,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     // ------------------------ FWD1 / DA: TMA tile::gather4 of 256 token rows
     const int p = warp == 0 ? 0 : warp - 1;   // 0, 1, 2
     const int c = lane * kTmaGatherWarps + p;  // gather call of this lane: rows 4c..4c+3
-    const int n_calls = 32 * a.MH;
+    const int n_calls = kTmaRows / 4;
     const bool has_call = c < n_calls;
     const int my_calls = n_calls > p ? (n_calls - p + kTmaGatherWarps - 1) / kTmaGatherWarps : 0;
-    const uint32_t tx = (uint32_t)my_calls * 512u + (p == 0 ? tile_tx_bytes<KIND>(a) : 0u);
+    const uint32_t tx = (a.ablate == 1 ? 0u : (uint32_t)my_calls * 512u) +
+                        (p == 0 ? tile_tx_bytes<KIND>(a) : 0u);
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -677,16 +701,28 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const int r = 4 * c + i;
         rr[i] = (has_call && r < ti.n_valid) ? a.r.bucket_token[ti.pos0 + r] : (int)a.T;
       }
+      if (KIND == K_DA) {
+        // the epilogue reads this tile's Z stash rows (m'*bw bf16 each, written by
+        // the forward and long evicted): warm L2 now, a whole mainloop ahead
+        const int zrow = a.mp * a.bw * 2;
+        for (int r = lane * kTmaGatherWarps + p; r < 256 && r < ti.rows_pad; r += 32 * kTmaGatherWarps)
+          prefetch_l2_bulk((const uint8_t*)a.aux + (ti.prow0 + r) * zrow, zrow);
+      }
       for (int kb = 0; kb < ti.nkb; ++kb) {
         if (lane == 0) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          twait(&empty[stage], phase ^ 1, (tr && warp == 0) ? tr : nullptr, 4);
           mbar_arrive_expect_tx(&full[stage], tx);
         }
         __syncwarp();
         uint8_t* sA = smem + stage * sstride;
         if (p == 0 && lane == 0) produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
-        if (has_call)
+        if (has_call && a.ablate != 1) {
           tma_gather4(sA + c * 512, &a.ta, &full[stage], kb * 64, rr[0], rr[1], rr[2], rr[3]);
+          // warm L2 with the next 256 columns of these rows in one 512-byte run per
+          // row (DRAM-friendly), 4..7 stages ahead of their gathers
+          if (a.prefetch && (kb & 3) == 0 && kb + 4 < ti.nkb)
+            tma_prefetch_gather4(&a.tc, (kb + 4) * 64, rr[0], rr[1], rr[2], rr[3]);
+        }
         if (++stage == n_stages) { stage = 0; phase ^= 1; }
       }
     }
@@ -699,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const TileInfo ti = decode<KIND>(a, tile);
         for (int kb = 0; kb < ti.nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          twait(&empty[stage], phase ^ 1, tr, 4);
           mbar_arrive_expect_tx(&full[stage], tx);
           uint8_t* sA = smem + stage * sstride;
           produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
@@ -707,13 +743,46 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
       }
     }
-  } else if (kGather && (warp == 2 || warp == 3 || warp >= 8)) {
+  } else if (kind_gather_a(KIND) && warp >= 12) {
+    // ------------ FWD1 / DA: cp.async of rows [kTmaRows, 256) of each stage
+    // thread t: 16-byte piece (t & 7) of rows kTmaRows + (t >> 3) + 16 i
+    const int t = threadIdx.x - 12 * 32;  // 0..127
+    const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
+    const int ch = t & 7;
+    constexpr int kRowsPer = (256 - kTmaRows) * 8 / kCpThreadsA;  // rows per thread (8)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const TileInfo ti = decode<KIND>(a, tile);
+      int tok[kRowsPer];
+#pragma unroll
+      for (int i = 0; i < kRowsPer; ++i) {
+        const int r = kTmaRows + (t >> 3) + 16 * i;
+        tok[i] = r < ti.n_valid ? a.r.bucket_token[ti.pos0 + r] : -1;
+      }
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
+        __syncwarp();
+        const uint32_t sA = smem_u32(smem + stage * sstride);
+#pragma unroll
+        for (int i = 0; i < kRowsPer; ++i) {
+          if (a.ablate == 1) break;
+          const int r = kTmaRows + (t >> 3) + 16 * i;
+          const uint32_t dst = sA + (r >> 7) * 16384 + (r & 127) * 128 + ((ch ^ (r & 7)) << 4);
+          const __nv_bfloat16* g = src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kb * 64 + ch * 8;
+          cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
+        }
+        cp_async_arrive_noinc(&full[stage]);
+        if (++stage == n_stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (kind_gather_b(KIND) && (warp == 2 || warp == 3 || warp >= 12)) {
     // -------------------------- DW*: cp.async row gathers of B (6 warps)
     // B: 64 bucket rows (K) x 256 columns (N) per stage, MN-major: 64-column
     // chunk j at +8 KB*j, K row r at +128 B*r, 16-byte piece p swizzled by r.
     // This thread: piece (gt & 31) of rows r_i = (gt >> 5) + 6 i.  Its
     // arrival on the stage barrier fires when its copies have landed.
-    const int gt = (warp < 4 ? warp - 2 : warp - 6) * 32 + lane;  // 0..191
+    const int gt = (warp < 4 ? warp - 2 : warp - 10) * 32 + lane;  // 0..191
     const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
     const int j = (gt & 31) >> 3, pc = gt & 7;
     int stage = 0;
@@ -730,6 +799,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
       };
       if (ti.nkb > 0) load_idx(0);
+      // one thread per row warms L2 with the row's 512-byte N slice, a stage ahead
+      auto prefetch_rows = [&]() {
+        if (a.prefetch && (gt & 31) == 0) {
+#pragma unroll
+          for (int i = 0; i < 11; ++i)
+            if (tok[i] >= 0) prefetch_l2_bulk(src + (int64_t)tok[i] * a.d + ti.nt * 256, 512);
+        }
+      };
+      prefetch_rows();
       for (int kb = 0; kb < ti.nkb; ++kb) {
         if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
         __syncwarp();
@@ -745,7 +823,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           }
         }
         cp_async_arrive_noinc(&full[stage]);
-        if (kb + 1 < ti.nkb) load_idx(kb + 1);
+        if (kb + 1 < ti.nkb) {
+          load_idx(kb + 1);
+          prefetch_rows();
+        }
         if (++stage == n_stages) { stage = 0; phase ^= 1; }
       }
     }
@@ -759,13 +840,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo ti = decode<KIND>(a, tile);
       if (lane == 0) {
-        mbar_wait(&tempty[acc], aphase ^ 1);
+        twait(&tempty[acc], aphase ^ 1, tr, 1);
         tc_fence_after();
+        if (tr) tr[7] += 1;
         for (int kb = 0; kb < ti.nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
+          twait(&full[stage], phase, tr, 0);
+          const long long tf0 = tr ? clock64() : 0;
           // cp.async writes are generic-proxy: order them before the UMMA reads
           if (kGather) fence_proxy_async_smem();
           tc_fence_after();
+          if (tr) tr[5] += (unsigned long long)(clock64() - tf0);
           const uint32_t sa = smem_u32(smem + stage * sstride);
           const uint32_t sb = sa + astride;
 #pragma unroll
@@ -796,36 +880,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo ti = decode<KIND>(a, tile);
-      mbar_wait(&tfull[acc], aphase);
+      twait(&tfull[acc], aphase, (tr && threadIdx.x == 4 * 32) ? tr : nullptr, 2);
       tc_fence_after();
+      const long long te0 = clock64();
       const uint32_t lanes = (uint32_t)(q * 32) << 16;
-      if (kGather) {
-        // DW*: 4 warps (one per lane quarter) cover both halves:
-        // MH == 2 -> accumulator h (features h*128 + row); MH == 1 -> column half h
-        for (int h = 0; h < 2; ++h)
-          epilogue<KIND>(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, a.MH == 2 ? h : 0), row, h,
-                         dg_xchg);
+      const int half = e >> 2;  // warp group: M half (pair tiles, DW1) or column half
+      if (kind_gather_a(KIND) && a.MH == 2) {
+        // M half `half` of a pair tile: this warp group owns its rows, all columns
+        TileInfo th = ti;
+        th.n_valid -= half * 128;
+        th.prow0 += half * 128;
+        th.pos0 += half * 128;
+        if (half * 128 < ti.rows_pad)  // the second m-tile may not exist: write nothing
+          epilogue<KIND>(a, th, tmem + lanes + tm_col(a.BN, a.MH, acc, half), row, -1, dg_xchg);
       } else {
-        const int half = e >> 2;  // warp group: M half (pair tiles) or column half
-        if (kind_gather_a(KIND) && a.MH == 2) {
-          // M half `half` of a pair tile: this warp group owns its rows, all columns
-          TileInfo th = ti;
-          th.n_valid -= half * 128;
-          th.prow0 += half * 128;
-          th.pos0 += half * 128;
-          if (half * 128 < ti.rows_pad)  // the second m-tile may not exist: write nothing
-            epilogue<KIND>(a, th, tmem + lanes + tm_col(a.BN, a.MH, acc, half), row, -1, dg_xchg);
-        } else {
-          epilogue<KIND>(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, 0), row, half, dg_xchg);
-        }
+        const uint32_t col0 = tm_col(a.BN, a.MH, acc, a.MH == 2 ? half : 0);
+        epilogue<KIND>(a, ti, tmem + lanes + col0, row, half, dg_xchg);
       }
       tc_fence_before();
       __syncwarp();
+      if (tr && threadIdx.x == 4 * 32) tr[3] += (unsigned long long)(clock64() - te0);
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == n_acc) { acc = 0; aphase ^= 1; }
     }
   }
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[6] += (unsigned long long)(clock64() - t_start);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -877,9 +957,36 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   const int grid = std::max(1, std::min(tiles_upper, num_sms()));
   static const char* kNames[] = {"tc_router", "tc_fwd1_gate_up", "tc_fwd2_down", "tc_bwd_dA",
                                  "tc_bwd_dX", "tc_bwd_dW1", "tc_bwd_dW2", "tc_bwd_dWR"};
+  static unsigned long long* trace_buf = nullptr;
+  static int trace_on = -1;
+  if (trace_on < 0) {
+    const char* e = getenv("SPT_FFN_TRACE");
+    trace_on = (e && e[0] == '1') ? 1 : 0;
+    if (trace_on) cudaMalloc(&trace_buf, 1024 * kTraceSlots * sizeof(unsigned long long));
+  }
+  if (trace_on) {
+    cudaMemsetAsync(trace_buf, 0, 1024 * kTraceSlots * sizeof(unsigned long long), s);
+    a.trace = trace_buf;
+  }
   prof_begin(kNames[KIND], s);
   tc_gemm_kernel<KIND><<<grid, kThreads, smem, s>>>(a, stages);
   prof_end(s);
+  if (trace_on) {
+    unsigned long long h[1024 * kTraceSlots];
+    cudaMemcpyAsync(h, trace_buf, sizeof(unsigned long long) * grid * kTraceSlots,
+                    cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double sum[kTraceSlots] = {0};
+    for (int b = 0; b < grid; ++b)
+      for (int i = 0; i < kTraceSlots; ++i) sum[i] += (double)h[b * kTraceSlots + i];
+    const double tot = sum[6] > 0 ? sum[6] : 1;
+    fprintf(stderr,
+            "[spt-trace] %-16s tiles/cta %.1f | MMA wait full %.0f%% wait tempty %.0f%% fences "
+            "%.0f%% | epi wait %.0f%% busy %.0f%% | tma prod wait empty %.0f%% | cta cycles %.0f\n",
+            kNames[KIND], sum[7] / grid, 100 * sum[0] / tot, 100 * sum[1] / tot, 100 * sum[5] / tot,
+            100 * sum[2] / tot, 100 * sum[3] / tot, 100 * sum[4] / tot, tot / grid);
+    a.trace = nullptr;
+  }
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (debug_sync()) {
@@ -903,6 +1010,18 @@ static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
   a.gpad = g.gpad;
   a.NT = (int)ceil_div(g.d, 256);
   a.MH = 1;
+  static int pf = -1;  // SPT_FFN_PREFETCH=1 enables the L2 prefetch of gathered rows
+  if (pf < 0) {
+    const char* e = getenv("SPT_FFN_PREFETCH");
+    pf = (e && e[0] == '1') ? 1 : 0;  // measured slower on B200 (r01): off by default
+  }
+  a.prefetch = pf;
+  static int abl = -1;
+  if (abl < 0) {
+    const char* e = getenv("SPT_FFN_ABLATE");
+    abl = e ? atoi(e) : 0;
+  }
+  a.ablate = abl;
 
 }
 
@@ -1006,7 +1125,8 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
     a.tile_list = b.tile_list;
     bool ok = make_tmap_bf16_2d(&a.ta, x, g.T, g.d, g.d, 64, 1) &&
               make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, g.bw) &&
-              make_tmap_bf16_2d(&a.tc, x, g.T, g.d, g.d, 64, 128);  // experiment only
+              make_tmap_bf16_2d(&a.tc, x, g.T, g.d, g.d, 256, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_SWIZZLE_NONE);  // L2 prefetch rows
     a.BN = g.mp * g.bw;
     a.MH = 2;
     a.aux2 = x;
@@ -1053,7 +1173,8 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, dy, g.T, g.d, g.d, 64, 1) &&
               make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, g.bw) &&
-              make_tmap_bf16_2d(&a.tc, dy, g.T, g.d, g.d, 64, 128);  // experiment only
+              make_tmap_bf16_2d(&a.tc, dy, g.T, g.d, g.d, 256, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_SWIZZLE_NONE);  // L2 prefetch rows
     a.BN = g.bw;
     a.aux = b.z;
     a.out2 = b.dz;

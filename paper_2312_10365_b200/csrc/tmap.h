@@ -22,11 +22,12 @@ inline PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 // 2-D row-major bf16 matrix [rows][cols] with row pitch `pitch_elems`; box =
-// box_cols x box_rows, 128-byte swizzle (box_cols * 2 must be 128).
+// box_cols x box_rows, 128-byte swizzle by default (then box_cols * 2 must be 128).
 // Out-of-bounds elements of a box are zero-filled by the TMA unit.
 inline bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
                               uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
-                              CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+                              CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = get_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
@@ -34,7 +35,7 @@ inline bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, u
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

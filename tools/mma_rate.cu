@@ -1,0 +1,87 @@
+// mma_rate.cu -- raw tcgen05.mma throughput on B200 (tool, not the library).
+// One CTA per SM; one thread issues back-to-back kind::f16 MMAs (bf16 -> fp32)
+// from fixed 128B-swizzled smem operands into TMEM, committing to an mbarrier
+// every `per_commit` MMAs.  Reports FLOP/clk/SM vs the 8192 nominal.
+// Variants: N = 64/128/256, M halves (1 or 2 accumulators sharing B), K-major
+// vs MN-major B.
+#include <cstdio>
+#include "tc_common.cuh"
+
+using namespace spt::tc;
+
+__global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int N, int MH, int bmn,
+                                                      long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16(128, N, false, bmn != 0);
+    const uint32_t sa = smem_u32(smem), sb = sa + 32768;
+    const long long t0 = clock64();
+    uint32_t ph = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t bd = bmn ? sdesc_sw128(sb + k * 2048, 8192, 1024) : sdesc_sw128(sb + k * 32, 16, 1024);
+        for (int h = 0; h < MH; ++h)
+          mma_bf16(tmem + h * 256, sdesc_sw128(sa + h * 16384 + k * 32, 16, 1024), bd, idesc,
+                   (it | k) != 0);
+      }
+      if ((it & 3) == 3) {  // commit + wait every 4 stages (like a 4-deep ring)
+        mma_commit(&bar);
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, ph);
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+int main() {
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  long long* d;
+  cudaMalloc(&d, nsm * sizeof(long long));
+  const int smem = 1024 + 32768 + 32768;
+  cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  struct C { int N, MH, bmn; } cs[] = {{64, 1, 0}, {128, 1, 0}, {256, 1, 0}, {128, 2, 0},
+                                       {256, 2, 0}, {256, 1, 1}, {128, 2, 1}};
+  for (auto c : cs) {
+    const int iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    mma_kernel<<<nsm, 128, smem>>>(64, c.N, c.MH, c.bmn, d);
+    cudaEventRecord(e0);
+    mma_kernel<<<nsm, 128, smem>>>(iters, c.N, c.MH, c.bmn, d);
+    cudaEventRecord(e1);
+    if (cudaEventSynchronize(e1) != cudaSuccess) { printf("error\n"); return 1; }
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long h[1024];
+    cudaMemcpy(h, d, nsm * sizeof(long long), cudaMemcpyDeviceToHost);
+    double cyc = 0;
+    for (int i = 0; i < nsm; ++i) cyc += h[i];
+    cyc /= nsm;
+    const double flop_sm = 2.0 * 128 * c.N * 64 * c.MH * iters;
+    printf("N=%3d MH=%d Bmn=%d: %.1f FLOP/clk/SM (%.0f%% of 8192), %.0f TFLOP/s chip (%.3f ms)\n", c.N,
+           c.MH, c.bmn, flop_sm / cyc, 100 * flop_sm / cyc / 8192, flop_sm * nsm / ms / 1e9, ms);
+  }
+  return 0;
+}
