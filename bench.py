@@ -143,9 +143,13 @@ def oracle_sample(cfg, n_tok):
 
 
 def cpu_baseline(cfg, target_s=15.0):
-    t0, _ = oracle_sample(cfg, 16)
-    n = int(max(16, min(4096, 16 * target_s / max(t0, 1e-3))))
-    secs, cores = oracle_sample(cfg, n)
+    """Oracle on a token sample sized (two calibration rounds) to ~target_s."""
+    n, (secs, cores) = 16, oracle_sample(cfg, 16)
+    for _ in range(2):
+        if secs >= 0.6 * target_s or n >= 8192:
+            break
+        n = int(max(16, min(8192, n * target_s / max(secs, 1e-3))))
+        secs, cores = oracle_sample(cfg, n)
     return {"value": n / secs, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{n} tokens of {cfg.name} (route+fwd+bwd, all {cfg.G} blocks' dW), "
                       f"{secs:.1f} s, fp64 C oracle, OpenMP"}
@@ -273,38 +277,36 @@ def main():
         P.profile_enable(False)
     clocks = sampler.stop()
 
-    # ---- end to end through the public API, host buffers
+    # ---- end to end through the public API, host buffers: every step copies its
+    # inputs x, dy from pinned host memory and its outputs y, dx back; the copies
+    # of neighbouring steps overlap the kernels (paper_2312_10365_b200.pipeline)
     e2e = None
     if not args.no_e2e:
+        from paper_2312_10365_b200.pipeline import HostStepPipeline
         xh = torch.empty_like(x, device="cpu").pin_memory()
         dyh = torch.empty_like(dy, device="cpu").pin_memory()
         xh.copy_(x)
         dyh.copy_(dy)
         yh = torch.empty_like(x, device="cpu").pin_memory()
         dxh = torch.empty_like(x, device="cpu").pin_memory()
-
-        def e2e_step():
-            x.copy_(xh, non_blocking=True)
-            dy.copy_(dyh, non_blocking=True)
-            step()
-            yh.copy_(f.y, non_blocking=True)
-            dxh.copy_(f.dx, non_blocking=True)
-
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
+        pipe = HostStepPipeline(f, w1, w2, w_r, grad_hook=lambda: dp.allreduce_grads(fg))
+        for i in range(3):
+            pipe.step(i, xh, dyh, yh, dxh)
+        pipe.synchronize()
         barrier()
-        k2 = max(3, args.steps // 3)
-        ev0.record(stream)
-        for _ in range(k2):
-            e2e_step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        ms_e = dp.max_over_ranks(ev0.elapsed_time(ev1) / k2, device="cuda")
-        nb = x.numel() * x.element_size()
+        k2 = max(6, args.steps // 2)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(pipe.s_h2d)
+        for i in range(k2):
+            pipe.step(3 + i, xh, dyh, yh, dxh)
+        e1.record(pipe.s_d2h)
+        pipe.synchronize()
+        ms_e = dp.max_over_ranks(e0.elapsed_time(e1) / k2, device="cuda")
+        hb, db = pipe.bytes_per_step()
         e2e = {"value": T * world / (ms_e / 1e3), "unit": UNIT, "ms_per_step": ms_e,
-               "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
-               "what": "H2D x, dy from pinned host + route/fwd/bwd(+allreduce) + D2H y, dx to pinned host"}
+               "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db,
+               "what": "per step: H2D x, dy from pinned host -> route/fwd/bwd(+allreduce) -> D2H y, dx "
+                       "to pinned host; copies of adjacent steps overlap the kernels (copy streams)"}
 
     if rank != 0:
         if world > 1:
@@ -330,17 +332,24 @@ def main():
         cnt, tot = prof[dom]
         per = tot / cnt
         kind, amt = work.get(dom, ("tensor", 0.0))
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+        if os.path.exists(tp) and cfg.name == "llama_scale" and T == 32768:
+            kt = json.load(open(tp))["kernels"].get(dom)
+            if kt:
+                traffic = kt["dram_read_bytes"] + kt["dram_write_bytes"]
         if kind == "tensor":
             ach = amt / (per / 1e3) / 1e12
             roofline = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk["bf16_sustained"],
-                        "unit": "TFLOP/s", "frac": ach / pk["bf16_sustained"], "traffic": None,
+                        "unit": "TFLOP/s", "frac": ach / pk["bf16_sustained"], "traffic": traffic,
+                        "traffic_src": "profiles/r01_ncu_traffic.json (dram read+write bytes per launch)",
                         "peak_src": pk["src"] + " bf16 sustained",
                         "algorithmic_per_launch": amt, "ms_per_launch": per,
                         "share_of_step": tot / args.steps / step_ms_prof}
         else:
             ach = amt / (per / 1e3) / 1e9
             roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                        "frac": ach / pk["hbm_gbs"], "traffic": None, "peak_src": pk["src"],
+                        "frac": ach / pk["hbm_gbs"], "traffic": traffic, "peak_src": pk["src"],
                         "algorithmic_per_launch": amt, "ms_per_launch": per,
                         "share_of_step": tot / args.steps / step_ms_prof}
     step_tf = step_gemm_flops(cfg, T) / (ms_max / 1e3) / 1e12
