@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int N, int MH, i
           mma_bf16(tmem + h * 256, sdesc_sw128(sa + h * 16384 + k * 32, 16, 1024), bd, idesc,
                    (it | k) != 0);
       }
-      if ((it & 3) == 3) {  // commit + wait every 4 stages (like a 4-deep ring)
+      if ((it & 63) == 63) {  // commit + wait every 64 stages
         mma_commit(&bar);
         mbar_wait(&bar, ph);
         ph ^= 1;
@@ -51,6 +51,80 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int N, int MH, i
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// CTA-pair variant: cluster of 2, M = 256 (128 rows per CTA), each CTA holds
+// its half of A and N/2 rows of B at the same smem offsets; the leader issues
+// tcgen05.mma.cta_group::2 and commits to both CTAs' barriers.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    mma2_kernel(int iters, int N, int MH, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0 && rank == 0) {
+    const uint32_t idesc = idesc_bf16(256, N, false, false);
+    const uint32_t sa = smem_u32(smem), sb = sa + 32768;
+    const long long t0 = clock64();
+    uint32_t ph = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t bd = sdesc_sw128(sb + k * 32, 16, 1024);
+        for (int h = 0; h < MH; ++h) {
+          const uint64_t ad = sdesc_sw128(sa + h * 16384 + k * 32, 16, 1024);
+          const uint32_t acc = (it | k) != 0;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + h * 256),
+              "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+              : "memory");
+        }
+      }
+      if ((it & 63) == 63) {
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(&bar)),
+            "h"((uint16_t)3)
+            : "memory");
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(&bar)),
+        "h"((uint16_t)3)
+        : "memory");
+    mbar_wait(&bar, ph);
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+  if (threadIdx.x == 0 && rank == 1) {  // peer: consume the same commits to keep phases aligned
+    uint32_t ph = 0;
+    for (int it = 0; it < iters; ++it)
+      if ((it & 63) == 63) { mbar_wait(&bar, ph); ph ^= 1; }
+    mbar_wait(&bar, ph);
+    cycles[blockIdx.x] = 0;
+  }
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 int main() {
@@ -82,6 +156,32 @@ int main() {
     const double flop_sm = 2.0 * 128 * c.N * 64 * c.MH * iters;
     printf("N=%3d MH=%d Bmn=%d: %.1f FLOP/clk/SM (%.0f%% of 8192), %.0f TFLOP/s chip (%.3f ms)\n", c.N,
            c.MH, c.bmn, flop_sm / cyc, 100 * flop_sm / cyc / 8192, flop_sm * nsm / ms / 1e9, ms);
+  }
+  // CTA pairs: per SM work = 128 rows x N x K per instruction
+  cudaFuncSetAttribute(mma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  struct C2 { int N, MH; } c2s[] = {{128, 1}, {256, 1}, {256, 2}, {128, 2}};
+  for (auto c : c2s) {
+    const int iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    mma2_kernel<<<nsm, 128, smem>>>(64, c.N, c.MH, d);
+    cudaEventRecord(e0);
+    mma2_kernel<<<nsm, 128, smem>>>(iters, c.N, c.MH, d);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaEventSynchronize(e1);
+    if (err != cudaSuccess) { printf("pair error %s\n", cudaGetErrorString(err)); return 1; }
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long h[1024];
+    cudaMemcpy(h, d, nsm * sizeof(long long), cudaMemcpyDeviceToHost);
+    double cyc = 0;
+    int n = 0;
+    for (int i = 0; i < nsm; ++i) if (h[i] > 0) { cyc += h[i]; ++n; }
+    cyc /= n;
+    const double flop_sm = 2.0 * 128 * c.N * 64 * c.MH * iters;  // per SM
+    printf("PAIR N=%3d MH=%d: %.1f FLOP/clk/SM (%.0f%% of 8192), %.0f TFLOP/s chip (%.3f ms)\n", c.N, c.MH,
+           flop_sm / cyc, 100 * flop_sm / cyc / 8192, flop_sm * nsm / ms / 1e9, ms);
   }
   return 0;
 }
