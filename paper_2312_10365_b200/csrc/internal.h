@@ -54,7 +54,8 @@ struct Bufs {
   int32_t* chunk_base;    // [n_chunks, G]
   int32_t* n_b;           // [G]
   int32_t* tile_list;     // [ceil(T*k/128) + G]: bucket tiles in (m-tile, block) order
-  int32_t* unit_offsets;  // [G+1]: prefix of weight-resident work units per block
+  int32_t* unit_offsets;  // [G+2]: prefix of weight-resident work units per block; [G+1] = pair tiles
+  int32_t* tile_block;    // [ceil(T*k/128) + G]: block of each 128-row bucket tile
 };
 
 constexpr int kUnitMTiles = 16;  // m-tiles per weight-resident unit (FWD2 / DX)

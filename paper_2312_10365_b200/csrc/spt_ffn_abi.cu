@@ -93,7 +93,7 @@ static int dwr_splits(const Geom& g) {
 
 struct Sizes {
   size_t z, h, stash;
-  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, ws;
+  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, tb, ws;
 };
 
 static Sizes compute_sizes(const Geom& g) {
@@ -104,7 +104,7 @@ static Sizes compute_sizes(const Geom& g) {
   s.stash = s.z + s.h;
   s.part = align256((size_t)g.rows_cap * g.d * e);
   s.dz = align256((size_t)g.rows_cap * g.mp * g.bw * e);
-  s.da = g.dtype == SPT_F32 ? align256((size_t)g.rows_cap * g.bw * 4) : 0;
+  s.da = align256((size_t)g.rows_cap * g.bw * 4);  // fp32 dA rows (both paths)
   s.dlogit = align256((size_t)g.rows_cap * 4);
   s.dgate = align256((size_t)g.rows_cap * 4);
   s.dlg = g.dtype == SPT_BF16 ? align256((size_t)2 * g.T * g.gpad * 2) : 0;
@@ -114,8 +114,9 @@ static Sizes compute_sizes(const Geom& g) {
   s.nb = align256((size_t)g.G * 4);
   s.tl = align256((size_t)(ceil_div(g.pairs, kTileM) + g.G) * 4);
   s.uo = align256((size_t)(g.G + 2) * 4);
+  s.tb = s.tl;
   s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb +
-         s.tl + s.uo;
+         s.tl + s.uo + s.tb;
   return s;
 }
 
@@ -141,6 +142,7 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
   b.n_b = (int32_t*)w; w += s.nb;
   b.tile_list = (int32_t*)w; w += s.tl;
   b.unit_offsets = (int32_t*)w; w += s.uo;
+  b.tile_block = (int32_t*)w; w += s.tb;
   return b;
 }
 

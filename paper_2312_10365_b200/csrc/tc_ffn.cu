@@ -41,7 +41,7 @@ namespace spt {
 
 using namespace tc;
 
-enum Kind : int { K_ROUTER = 0, K_FWD1, K_FWD2, K_DA, K_DX, K_DW1, K_DW2, K_DWR };
+enum Kind : int { K_ROUTER = 0, K_FWD1, K_FWD2, K_DA, K_DX, K_DW1, K_DW2, K_DWR, K_DAT };
 
 struct TcArgs {
   CUtensorMap ta;  // A operand
@@ -89,11 +89,14 @@ constexpr int kCpThreadsA = 128;              // FWD1 / DA: cp.async warps 12..1
 constexpr int kCpThreadsB = 192;              // DW*: cp.async warps 2, 3, 12..15
 constexpr int kABytes = 16384;                // 128 rows x 64 bf16
 
-__host__ __device__ constexpr bool kind_gather_a(int k) { return k == K_FWD1 || k == K_DA; }
+// kinds whose 256 gathered token rows per stage come from the pair-tile list:
+// FWD1 / DA gather them as the A (M) operand, DAT as the B (N) operand
+__host__ __device__ constexpr bool kind_gather_a(int k) { return k == K_FWD1 || k == K_DA || k == K_DAT; }
+__host__ __device__ constexpr bool kind_rows_on_b(int k) { return k == K_DAT; }
 __host__ __device__ constexpr bool kind_gather_b(int k) { return k == K_DW1 || k == K_DW2; }
 __host__ __device__ constexpr bool kind_a_mn(int k) { return k == K_DW1 || k == K_DW2 || k == K_DWR; }
 __host__ __device__ constexpr bool kind_b_mn(int k) {
-  return !(k == K_ROUTER || k == K_FWD1 || k == K_DA);
+  return !(k == K_ROUTER || k == K_FWD1 || k == K_DA || k == K_DAT);
 }
 // FWD2 / DX keep one (block, 256-column) weight slab resident in smem and
 // stream up to kUnitMTiles A tiles of that block through it
@@ -135,7 +138,7 @@ __host__ __device__ __forceinline__ uint32_t tm_col(int BN, int MH, int acc, int
 template <int KIND>
 __device__ __forceinline__ int num_tiles(const TcArgs& a) {
   if (KIND == K_ROUTER) return (int)ceil_div(a.T, 128);
-  if (KIND == K_FWD1 || KIND == K_DA) return a.unit_offsets[a.G + 1];  // 256-row pair tiles
+  if (kind_gather_a(KIND)) return a.unit_offsets[a.G + 1];  // 256-row pair tiles
   if (KIND == K_FWD2 || KIND == K_DX) return a.unit_offsets[a.G];  // units
   if (KIND == K_DW1 || KIND == K_DW2) return a.G * a.NT;
   return a.NT * a.n_split;  // DWR (G <= 128 rows: one M tile)
@@ -148,7 +151,7 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
     ti.prow0 = (int64_t)tile * 128;
     ti.n_valid = (int)(a.T - ti.prow0 < 128 ? a.T - ti.prow0 : 128);
     ti.nkb = a.d / 64;
-  } else if (KIND == K_FWD1 || KIND == K_DA) {
+  } else if (kind_gather_a(KIND)) {
     // pair tiles (two 128-row m-tiles sharing each B stage) in the raster order
     // of tile_sched_kernel
     const int e = a.tile_list[tile];
@@ -212,6 +215,7 @@ template <int KIND>
 __device__ __forceinline__ uint32_t tile_tx_bytes(const TcArgs& a) {
   if (KIND == K_FWD1) return a.mp * a.bw * 128;
   if (KIND == K_DA) return a.bw * 128;
+  if (KIND == K_DAT) return 128 * 128;  // the W2 box is always 128 unit rows (rows >= bw unused)
   if (KIND == K_ROUTER) return kABytes + a.gpad * 128;
   if (KIND == K_DW1 || KIND == K_DW2) return kABytes * a.MH;
   return kABytes + 32768;  // FWD2, DX, DWR
@@ -225,6 +229,8 @@ __device__ __forceinline__ void produce_tiles(const TcArgs& a, const TileInfo& t
   if (KIND == K_ROUTER) {
     tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
     tma_load_2d(sB, &a.tb, bar, kb * 64, 0);
+  } else if (KIND == K_DAT) {  // A = the block's W2 rows (units) x 64 columns
+    tma_load_2d(sA, &a.tb, bar, kb * 64, ti.b * a.bw);
   } else if (KIND == K_FWD1 || KIND == K_DA) {
     tma_load_2d(sB, &a.tb, bar, kb * 64, ti.b * a.bw);
     if (KIND == K_FWD1 && a.mp == 2) tma_load_2d(sB + a.bw * 128, &a.tb, bar, kb * 64, a.D + ti.b * a.bw);
@@ -521,6 +527,32 @@ __device__ __forceinline__ void epilogue_tma_store(const TcArgs& a, const TileIn
   }
 }
 
+// DAT epilogue: the accumulator is dA^T (TMEM lane = unit of the block, column =
+// token row of the pair tile).  Each warp stages 32 tokens x 32 units of fp32
+// row-major in smem and TMA-stores the box into dA[row][unit]; dgate / dZ are
+// computed from dA and the Z stash by da_post_kernel (a streaming pass).
+__device__ __forceinline__ void epilogue_dat(const TcArgs& a, const TileInfo& ti, uint32_t tacc,
+                                             int q, int lane, int half, uint8_t* stg) {
+  const bool units_live = q * 32 < a.bw;
+  float* buf = reinterpret_cast<float*>(stg);
+  for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld32(tacc + c0, v);
+    tmem_ld_wait();
+    if (!units_live || c0 >= ti.rows_pad) continue;  // warp-uniform
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) buf[j * 32 + lane] = __uint_as_float(v[j]);  // [token j][unit]
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(&a.tc, buf, q * 32, (int)(ti.prow0 + c0));
+      bulk_commit();
+    }
+  }
+}
+
 // diagnostics: cycles spent in an mbarrier wait, accumulated into trace slot
 __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, unsigned long long* tr, int slot) {
   if (tr) {
@@ -717,10 +749,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         uint8_t* sA = smem + stage * sstride;
         if (p == 0 && lane == 0) produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
         if (has_call && a.ablate != 1) {
-          tma_gather4(sA + c * 512, &a.ta, &full[stage], kb * 64, rr[0], rr[1], rr[2], rr[3]);
+          tma_gather4((kind_rows_on_b(KIND) ? sA + astride : sA) + c * 512, &a.ta, &full[stage],
+                      kb * 64, rr[0], rr[1], rr[2], rr[3]);
           // warm L2 with the next 256 columns of these rows in one 512-byte run per
           // row (DRAM-friendly), 4..7 stages ahead of their gathers
-          if (a.prefetch && (kb & 3) == 0 && kb + 4 < ti.nkb)
+          if (a.prefetch && !kind_rows_on_b(KIND) && (kb & 3) == 0 && kb + 4 < ti.nkb)
             tma_prefetch_gather4(&a.tc, (kb + 4) * 64, rr[0], rr[1], rr[2], rr[3]);
         }
         if (++stage == n_stages) { stage = 0; phase ^= 1; }
@@ -763,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       for (int kb = 0; kb < ti.nkb; ++kb) {
         if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
         __syncwarp();
-        const uint32_t sA = smem_u32(smem + stage * sstride);
+        const uint32_t sA = smem_u32(smem + stage * sstride + (kind_rows_on_b(KIND) ? astride : 0));
 #pragma unroll
         for (int i = 0; i < kRowsPer; ++i) {
           if (a.ablate == 1) break;
@@ -893,6 +926,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         th.pos0 += half * 128;
         if (half * 128 < ti.rows_pad)  // the second m-tile may not exist: write nothing
           epilogue<KIND>(a, th, tmem + lanes + tm_col(a.BN, a.MH, acc, half), row, -1, dg_xchg);
+      } else if (KIND == K_DAT) {
+        epilogue_dat(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, 0), q, lane, half,
+                     stg_base + e * 4096);
       } else {
         const uint32_t col0 = tm_col(a.BN, a.MH, acc, a.MH == 2 ? half : 0);
         epilogue<KIND>(a, ti, tmem + lanes + col0, row, half, dg_xchg);
@@ -903,6 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == n_acc) { acc = 0; aphase ^= 1; }
     }
+    if (KIND == K_DAT && lane == 0) bulk_wait<0>();  // dA tiles written before exit
   }
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[6] += (unsigned long long)(clock64() - t_start);
@@ -944,7 +981,8 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
                        : 0;
   // FWD2 keeps 2 staging buffers per epilogue warp, DX (128 KB slab) keeps 1
   if (kind_bres(KIND)) a.n_stg = slab > 65536 ? 1 : 2;
-  const int stg = kind_bres(KIND) ? kEpiWarps * a.n_stg * 4096 + 1024 : 0;
+  const int stg = kind_bres(KIND) ? kEpiWarps * a.n_stg * 4096 + 1024
+                                  : (KIND == K_DAT ? kEpiWarps * 4096 + 1024 : 0);
   int stages = std::min(kind_bres(KIND) ? 8 : 6, (227 * 1024 - extra - slab - stg) / sst);
   const int smem = slab + stages * sst + extra + stg;
   static bool attr_set = false;
@@ -956,7 +994,8 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   }
   const int grid = std::max(1, std::min(tiles_upper, num_sms()));
   static const char* kNames[] = {"tc_router", "tc_fwd1_gate_up", "tc_fwd2_down", "tc_bwd_dA",
-                                 "tc_bwd_dX", "tc_bwd_dW1", "tc_bwd_dW2", "tc_bwd_dWR"};
+                                 "tc_bwd_dX", "tc_bwd_dW1", "tc_bwd_dW2", "tc_bwd_dWR",
+                                 "tc_bwd_dAT"};
   static unsigned long long* trace_buf = nullptr;
   static int trace_on = -1;
   if (trace_on < 0) {
@@ -1027,6 +1066,19 @@ static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
 
 static int bucket_tiles_upper(const Geom& g) { return (int)(ceil_div(g.pairs, 128) + g.G); }
 
+// a7 variant.  Default: the fused dA kernel (tokens on M, N = bw, dgate/dZ in the
+// epilogue).  SPT_FFN_DAT=1: tokens on N (N = 256, transposed dA via TMA store)
+// + da_post_kernel; measured at parity on B200 in round 1 (both ~1.7 ms at
+// LLaMA scale: the gathered-row supply, not the MMA shape, bounds a7).
+static bool use_fused_da() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_DAT");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 bool tc_supported(const Geom& g) {
   if (g.d % 64) return false;
   if (g.mp * g.bw > 256) return false;          // FWD1 N = m' * bw in one MMA; DW1 M <= 256
@@ -1065,7 +1117,8 @@ cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logi
 //  nt_b' > mt};  unit_offsets = prefix over blocks of ceil(nt_b/16) * NT.
 __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, const int32_t* __restrict__ tile_offsets,
                                                          int32_t* __restrict__ tile_list,
-                                                         int32_t* __restrict__ unit_offsets) {
+                                                         int32_t* __restrict__ unit_offsets,
+                                                         int32_t* __restrict__ tile_block) {
   __shared__ int ntb[kMaxBlocks];
   __shared__ int ntu[kMaxBlocks];  // 128-row tiles per block (units) ...
   for (int i = threadIdx.x; i < G; i += blockDim.x) {
@@ -1077,6 +1130,7 @@ __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, const in
   // order.  The group's weights (<= 32 MB of W1 rows) and the window of tokens
   // the in-flight m-levels gather both stay in L2.
   const int b = blockIdx.x;
+  for (int t = tile_offsets[b] + threadIdx.x; t < tile_offsets[b + 1]; t += blockDim.x) tile_block[t] = b;
   const int g0 = (b / kRasterBlocks) * kRasterBlocks, g1 = min(G, g0 + kRasterBlocks);
   int base = 0;
   for (int bb = 0; bb < g0; ++bb) base += ntb[bb];
@@ -1104,7 +1158,7 @@ __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, const in
 static cudaError_t build_schedules(const Geom& g, const RouteView& r, const Bufs& b, cudaStream_t s) {
   prof_begin("tile_sched", s);
   tile_sched_kernel<<<g.G, 256, 0, s>>>(g.G, (int)ceil_div(g.d, 256), r.tile_offsets, b.tile_list,
-                                        b.unit_offsets);
+                                        b.unit_offsets, b.tile_block);
   prof_end(s);
   count_launch();
   return cudaGetLastError();
@@ -1149,6 +1203,107 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
   return launch_combine_fwd(g, r, b.part, y, s);
 }
 
+// a7 second half: per padded bucket row (one warp), from dA (fp32) and the Z
+// stash: dgate = sum_u dA_u act(z_u); dZ = g dA act'(Z); dlogit = dgate g (1-g)
+// (as sigma(z) sigma(-z)); dense hi/lo bf16 dlogits for the dW_R GEMM.  Padding
+// rows get dZ = 0 (the K tails of the dW1 GEMM rely on it).
+__global__ void __launch_bounds__(256) da_post_kernel(int64_t T, int G, int bw, int mp, int act,
+                                                      int gate, int gpad, RouteView r,
+                                                      const int32_t* __restrict__ tile_block,
+                                                      const float* __restrict__ da,
+                                                      const __nv_bfloat16* __restrict__ z,
+                                                      __nv_bfloat16* __restrict__ dz,
+                                                      float* __restrict__ dgate_rows,
+                                                      float* __restrict__ dlogit_rows,
+                                                      __nv_bfloat16* __restrict__ dlg) {
+  // one warp per 4 padded rows; lane covers units lane*4 + 128 i; all loads of
+  // the 4 rows are issued before any math (memory-level parallelism)
+  constexpr int R = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t row0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * R;
+  const int64_t nrows = (int64_t)r.tile_offsets[G] * 128;
+  if (row0 >= nrows) return;
+  for (int u0 = lane * 4; u0 < ((bw + 127) / 128) * 128; u0 += 128) {
+    const bool ul = u0 < bw;
+    float4 dA[R];
+    uint2 zg2[R], zu2[R];
+    bool valid[R];
+    float g[R];
+    int bidx[R];
+    int64_t pos[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int64_t row = row0 + i;
+      valid[i] = false;
+      g[i] = 0.f;
+      bidx[i] = 0;
+      pos[i] = 0;
+      dA[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      zg2[i] = zu2[i] = make_uint2(0u, 0u);
+      if (row < nrows) {
+        const int b = tile_block[row >> 7];
+        const int e = (int)(row - (int64_t)r.tile_offsets[b] * 128);
+        bidx[i] = b;
+        pos[i] = r.block_offsets[b] + e;
+        valid[i] = e < r.block_offsets[b + 1] - r.block_offsets[b];
+        if (valid[i]) {
+          g[i] = r.bucket_gate[pos[i]];
+          if (ul) {
+            dA[i] = *reinterpret_cast<const float4*>(da + row * bw + u0);
+            const __nv_bfloat16* zr = z + row * (int64_t)(mp * bw);
+            zg2[i] = *reinterpret_cast<const uint2*>(zr + u0);
+            if (mp == 2) zu2[i] = *reinterpret_cast<const uint2*>(zr + bw + u0);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int64_t row = row0 + i;
+      float dgate = 0.f;
+      if (row < nrows) {
+        const float a4[4] = {dA[i].x, dA[i].y, dA[i].z, dA[i].w};
+        const float zg[4] = {__uint_as_float(zg2[i].x << 16), __uint_as_float(zg2[i].x & 0xffff0000u),
+                             __uint_as_float(zg2[i].y << 16), __uint_as_float(zg2[i].y & 0xffff0000u)};
+        const float zu[4] = {__uint_as_float(zu2[i].x << 16), __uint_as_float(zu2[i].x & 0xffff0000u),
+                             __uint_as_float(zu2[i].y << 16), __uint_as_float(zu2[i].y & 0xffff0000u)};
+        float dzg[4], dzu[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float av, dg, du;
+          act_fwd_bwd<true>(act, zg[j], zu[j], av, dg, du);
+          dgate = fmaf(a4[j], av, dgate);
+          dzg[j] = g[i] * a4[j] * dg;
+          dzu[j] = g[i] * a4[j] * du;
+        }
+        if (ul) {
+          __nv_bfloat16* dzr = dz + row * (int64_t)(mp * bw);
+          *reinterpret_cast<uint2*>(dzr + u0) = make_uint2(pack_bf16(dzg[0], dzg[1]), pack_bf16(dzg[2], dzg[3]));
+          if (mp == 2)
+            *reinterpret_cast<uint2*>(dzr + bw + u0) =
+                make_uint2(pack_bf16(dzu[0], dzu[1]), pack_bf16(dzu[2], dzu[3]));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) dgate += __shfl_xor_sync(0xffffffffu, dgate, o);
+      // bw <= 128 for the tensor-core path, so one pass covers the row
+      if (lane == 0 && row < nrows) {
+        float dlogit = 0.f;
+        if (valid[i] && gate == SPT_GATE_SIGMOID) {
+          const int64_t t = r.bucket_token[pos[i]];
+          dlogit = dgate * sigmoid_pair(r.logits[t * G + bidx[i]]);
+          const __nv_bfloat16 hi = __float2bfloat16(dlogit);
+          const __nv_bfloat16 lo = __float2bfloat16(dlogit - __bfloat162float(hi));
+          dlg[t * gpad + bidx[i]] = hi;
+          dlg[(T + t) * gpad + bidx[i]] = lo;
+        }
+        dgate_rows[row] = valid[i] ? dgate : 0.f;
+        dlogit_rows[row] = dlogit;
+      }
+    }
+  }
+}
+
 __global__ void dwr_reduce_kernel(int n_split, int64_t n, const float* __restrict__ part,
                                   float* __restrict__ out, int acc) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1168,7 +1323,25 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   if (e0 != cudaSuccess) return e0;
   if (sig && cudaMemsetAsync(b.dlg, 0, (size_t)2 * g.T * g.gpad * 2, s) != cudaSuccess)
     return cudaErrorUnknown;
-  {  // a7: dA = dY[bucket] W2_b^T with the dgate / dZ / dlogit epilogue
+  if (!use_fused_da()) {  // a7: dA^T = W2_b dY[bucket]^T (tokens on N), then the dgate/dZ pass
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, dy, g.T, g.d, g.d, 64, 1) &&
+              make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, 128) &&
+              make_tmap_f32_2d(&a.tc, b.da, g.rows_cap, g.bw, g.bw, 32, 32);
+    a.BN = 256;
+    a.MH = 1;
+    a.aux2 = dy;
+    a.tile_list = b.tile_list;
+    a.unit_offsets = b.unit_offsets;
+    TRY(launch<K_DAT>(a, up / 2 + g.G, s));
+    prof_begin("da_post", s);
+    da_post_kernel<<<(unsigned)ceil_div(g.rows_cap, 32), 256, 0, s>>>(
+        g.T, g.G, g.bw, g.mp, g.act, g.gate, g.gpad, r, b.tile_block, b.da, (const __nv_bfloat16*)b.z,
+        (__nv_bfloat16*)b.dz, b.dgate, b.dlogit, (__nv_bfloat16*)b.dlg);
+    prof_end(s);
+    count_launch();
+  } else {  // a7 fused variant: dA = dY[bucket] W2_b^T with the dgate / dZ / dlogit epilogue
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, dy, g.T, g.d, g.d, 64, 1) &&

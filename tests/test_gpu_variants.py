@@ -1,0 +1,38 @@
+"""GPU parity of the library's alternative kernel paths (selected by environment
+knobs read once per process, so each case runs in its own interpreter):
+  SPT_FFN_DAT=1       a7 with tokens on N + da_post_kernel
+  SPT_FFN_PREFETCH=1  L2 prefetch of gathered rows
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import oracle, synthetic as S
+from helpers import TOL, gpu_run, oracle_run, relerr
+for name, T in (("bert", 700), ("llama", 300)):
+    cfg = S.CONFIGS[name]
+    inp = S.make_inputs(cfg, T)
+    got = gpu_run(cfg, T, inp)
+    lg = oracle.router(inp["x"], inp["w_r"])
+    ref = oracle_run(oracle, cfg, inp, lg, got["topk_idx"])
+    errs = {{n: relerr(got[n], ref[n]) for n in ("y", "dx", "dw1", "dw2", "dw_r", "dgate")}}
+    assert all(e <= TOL[cfg.dtype] for e in errs.values()), (name, errs)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_PREFETCH": "1"}])
+def test_variant_parity(env):
+    code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
