@@ -233,11 +233,17 @@ def main():
     f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, dt, cfg.act, cfg.gate)
     fg = dp.attach_flat_grads(f)
 
+    # N > 1: the dW all-reduce starts (side stream) at the event the backward
+    # records once dw1/dw2/dw_r are final and overlaps its grad-input kernels;
+    # the next step's backward waits for it before overwriting the gradients.
+    ar = dp.OverlappedAllReduce(fg)
+
     def step():
         f.route(x, w_r)
         f.forward(x, w1, w2)
-        f.backward(x, w1, w2, w_r, dy)
-        dp.allreduce_grads(fg)
+        ar.wait()
+        f.backward(x, w1, w2, w_r, dy, dw_event=ar.event)
+        ar.launch()
 
     def barrier():
         if world > 1:
@@ -246,6 +252,7 @@ def main():
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         step()
+    ar.wait()
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local)
@@ -258,6 +265,7 @@ def main():
     ev0.record(stream)
     for _ in range(args.steps):
         step()
+    ar.wait()
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -272,6 +280,7 @@ def main():
         P.profile_enable(True)
         for _ in range(args.steps):
             step()
+        ar.wait()
         torch.cuda.synchronize()
         prof = P.profile_read()
         P.profile_enable(False)

@@ -128,12 +128,17 @@ spt_status spt_ffn_forward(const spt_ffn_desc* desc, const void* x, const void* 
  *   dw_r [G,d]   = sum over pairs of dlogit * x_t  (fp32; 0 for GATE_NONE)
  *   dgate [T,k]  = dL/dg per pair (fp32, optional: may be NULL)
  * with dlogit = dgate * g (1 - g) for GATE_SIGMOID.  stash must be the one the
- * matching spt_ffn_forward wrote.  flags: SPT_BWD_ACCUMULATE_DW. */
+ * matching spt_ffn_forward wrote.  flags: SPT_BWD_ACCUMULATE_DW.
+ * dw_event: optional cudaEvent_t (void*, may be NULL).  The weight gradients
+ * dw1, dw2, dw_r are computed first; the library records dw_event on `stream`
+ * as soon as all three are final and only then computes dx.  A data-parallel
+ * caller can start the gradient all-reduce on another stream at that event so
+ * it overlaps the grad-input kernels. */
 spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void* w1,
                             const void* w2, const void* w_r, const spt_route_buf* r,
                             const void* stash, const void* dy, void* dx, float* dw1, float* dw2,
                             float* dw_r, float* dgate, unsigned flags, void* ws, size_t ws_bytes,
-                            void* stream);
+                            void* dw_event, void* stream);
 
 /* Static string for a status code (never NULL). */
 const char* spt_status_string(spt_status s);

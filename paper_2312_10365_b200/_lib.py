@@ -59,7 +59,7 @@ def lib() -> ctypes.CDLL:
         L.spt_ffn_route.argtypes = [D, P, P, ctypes.c_uint, R, P, ctypes.c_size_t, P]
         L.spt_ffn_forward.argtypes = [D, P, P, P, R, P, P, P, ctypes.c_size_t, P]
         L.spt_ffn_backward.argtypes = [D, P, P, P, P, R, P, P, P, P, P, P, P, ctypes.c_uint, P,
-                                       ctypes.c_size_t, P]
+                                       ctypes.c_size_t, P, P]
         for f in ("spt_ffn_sizes", "spt_ffn_route", "spt_ffn_forward", "spt_ffn_backward"):
             getattr(L, f).restype = ctypes.c_int
         L.spt_status_string.argtypes = [ctypes.c_int]

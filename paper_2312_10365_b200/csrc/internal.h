@@ -77,7 +77,7 @@ cudaError_t simt_forward(const Geom& g, const void* x, const void* w1, const voi
 cudaError_t simt_backward(const Geom& g, const void* x, const void* w1, const void* w2,
                           const void* w_r, const RouteView& r, const void* dy, void* dx,
                           float* dw1, float* dw2, float* dw_r, float* dgate_out, bool accumulate,
-                          const Bufs& b, cudaStream_t s);
+                          const Bufs& b, cudaEvent_t dw_ev, cudaStream_t s);
 
 // shared HBM-bound kernels (combine.cu)
 cudaError_t launch_combine_fwd(const Geom& g, const RouteView& r, const void* part, void* y,
@@ -96,7 +96,7 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
 cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void* w2,
                         const void* w_r, const RouteView& r, const void* dy, void* dx, float* dw1,
                         float* dw2, float* dw_r, float* dgate_out, bool accumulate, const Bufs& b,
-                        cudaStream_t s);
+                        cudaEvent_t dw_ev, cudaStream_t s);
 
 // device helpers shared by kernels
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

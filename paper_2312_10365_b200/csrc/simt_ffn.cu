@@ -332,7 +332,7 @@ cudaError_t fwd_impl(const Geom& g, const T* x, const T* w1, const T* w2, const 
 template <typename T>
 cudaError_t bwd_impl(const Geom& g, const T* x, const T* w1, const T* w2, const T* w_r,
                      const RouteView& r, const T* dy, T* dx, float* dw1, float* dw2, float* dw_r,
-                     float* dgate_out, bool acc, const Bufs& b, cudaStream_t s) {
+                     float* dgate_out, bool acc, const Bufs& b, cudaEvent_t dw_ev, cudaStream_t s) {
   const unsigned tiles64 = (unsigned)((ceil_div(g.pairs, kTileM) + g.G) * (kTileM / 64));
   OpDA<T> oda{r, dy, w2, b.da, g.d, g.bw};
   prof_begin("simt_b1", s);
@@ -342,14 +342,6 @@ cudaError_t bwd_impl(const Geom& g, const T* x, const T* w1, const T* w2, const 
   k_b1b<T><<<tiles64, 256, 0, s>>>(r, g.G, g.bw, g.mp, g.act, g.gate, (const T*)b.z, b.da,
                                    (T*)b.dz, b.dgate, b.dlogit);
   prof_end(s);
-  OpDX<T> odx{(const T*)b.dz, w1, (T*)b.part, g.d, g.D, g.bw, g.mp};
-  prof_begin("simt_b2", s);
-  k_b2<T><<<dim3(tiles64, (unsigned)ceil_div(g.d, 64)), 256, 0, s>>>(odx, r, g.G);
-  prof_end(s);
-  count_launch(3);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  if ((e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s)) != cudaSuccess) return e;
   const int M1 = g.mp * g.bw;
   OpDW<T> o1{r, (const T*)b.dz, x, dw1, g.d, g.D, g.bw, M1, acc ? 1 : 0, g.mp == 2 ? 1 : 0, 0};
   prof_begin("simt_dw", s);
@@ -363,8 +355,17 @@ cudaError_t bwd_impl(const Geom& g, const T* x, const T* w1, const T* w2, const 
   k_dwr<T><<<dim3((unsigned)ceil_div(g.d, 128), g.G), 128, 0, s>>>(r, g.d, x, b.dlogit, dw_r,
                                                                   acc ? 1 : 0);
   prof_end(s);
-  count_launch(3);
+  count_launch(5);  // b1, b1b, dw x2, dwr
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
+  OpDX<T> odx{(const T*)b.dz, w1, (T*)b.part, g.d, g.D, g.bw, g.mp};
+  prof_begin("simt_b2", s);
+  k_b2<T><<<dim3(tiles64, (unsigned)ceil_div(g.d, 64)), 256, 0, s>>>(odx, r, g.G);
+  prof_end(s);
+  count_launch(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s)) != cudaSuccess) return e;
   if (dgate_out) return launch_gather_dgate(g, r, b.dgate, dgate_out, s);
   return cudaSuccess;
 }
@@ -382,15 +383,15 @@ cudaError_t simt_forward(const Geom& g, const void* x, const void* w1, const voi
 cudaError_t simt_backward(const Geom& g, const void* x, const void* w1, const void* w2,
                           const void* w_r, const RouteView& r, const void* dy, void* dx,
                           float* dw1, float* dw2, float* dw_r, float* dgate_out, bool accumulate,
-                          const Bufs& b, cudaStream_t s) {
+                          const Bufs& b, cudaEvent_t dw_ev, cudaStream_t s) {
   if (g.dtype == SPT_F32)
     return bwd_impl<float>(g, (const float*)x, (const float*)w1, (const float*)w2,
                            (const float*)w_r, r, (const float*)dy, (float*)dx, dw1, dw2, dw_r,
-                           dgate_out, accumulate, b, s);
+                           dgate_out, accumulate, b, dw_ev, s);
   return bwd_impl<__nv_bfloat16>(g, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w1,
                                  (const __nv_bfloat16*)w2, (const __nv_bfloat16*)w_r, r,
                                  (const __nv_bfloat16*)dy, (__nv_bfloat16*)dx, dw1, dw2, dw_r,
-                                 dgate_out, accumulate, b, s);
+                                 dgate_out, accumulate, b, dw_ev, s);
 }
 
 }  // namespace spt

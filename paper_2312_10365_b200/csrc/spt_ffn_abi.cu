@@ -304,7 +304,7 @@ spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void*
                             const void* w_r, const spt_route_buf* r, const void* stash,
                             const void* dy, void* dx, float* dw1, float* dw2, float* dw_r,
                             float* dgate, unsigned flags, void* ws, size_t ws_bytes,
-                            void* stream) {
+                            void* dw_event, void* stream) {
   Geom g;
   spt_status st = make_geom(desc, &g);
   if (st != SPT_OK) return st;
@@ -316,20 +316,25 @@ spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void*
   cudaStream_t s = (cudaStream_t)stream;
   const bool acc = flags & SPT_BWD_ACCUMULATE_DW;
   if (g.T == 0) {
-    if (acc) return SPT_OK;
+    if (acc) {
+      if (dw_event && cudaEventRecord((cudaEvent_t)dw_event, s) != cudaSuccess) return SPT_ERR_CUDA;
+      return SPT_OK;
+    }
     const size_t w1b = (size_t)g.mp * g.D * g.d * 4, w2b = (size_t)g.D * g.d * 4,
                  wrb = (size_t)g.G * g.d * 4;
     if (cudaMemsetAsync(dw1, 0, w1b, s) != cudaSuccess || cudaMemsetAsync(dw2, 0, w2b, s) ||
         cudaMemsetAsync(dw_r, 0, wrb, s))
       return SPT_ERR_CUDA;
+    if (dw_event && cudaEventRecord((cudaEvent_t)dw_event, s) != cudaSuccess) return SPT_ERR_CUDA;
     return SPT_OK;
   }
   Bufs b = carve(g, const_cast<void*>(stash), ws);
   RouteView rv = view(r);
+  cudaEvent_t ev = (cudaEvent_t)dw_event;
   cudaError_t e = g.dtype == SPT_BF16
-                      ? tc_backward(g, x, w1, w2, w_r, rv, dy, dx, dw1, dw2, dw_r, dgate, acc, b, s)
+                      ? tc_backward(g, x, w1, w2, w_r, rv, dy, dx, dw1, dw2, dw_r, dgate, acc, b, ev, s)
                       : simt_backward(g, x, w1, w2, w_r, rv, dy, dx, dw1, dw2, dw_r, dgate, acc, b,
-                                      s);
+                                      ev, s);
   return to_status(e);
 }
 

@@ -1316,7 +1316,7 @@ __global__ void dwr_reduce_kernel(int n_split, int64_t n, const float* __restric
 cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void* w2,
                         const void* w_r, const RouteView& r, const void* dy, void* dx, float* dw1,
                         float* dw2, float* dw_r, float* dgate_out, bool accumulate, const Bufs& b,
-                        cudaStream_t s) {
+                        cudaEvent_t dw_ev, cudaStream_t s) {
   const int up = bucket_tiles_upper(g);
   const bool sig = g.gate == SPT_GATE_SIGMOID;
   cudaError_t e0 = build_schedules(g, r, b, s);
@@ -1360,20 +1360,6 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.unit_offsets = b.unit_offsets;
     TRY(launch<K_DA>(a, up / 2 + g.G, s));
   }
-  {  // a8: dXp = dZ W1_b, then combine with the router term
-    TcArgs a{};
-    base_args(a, g, r);
-    bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
-                                (uint64_t)g.mp * g.bw, 64, 128) &&
-              make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, 64);
-    ok = ok && make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
-    a.BN = 256;
-    a.out = b.part;
-    a.unit_offsets = b.unit_offsets;
-    TRY(launch<K_DX>(a, units_upper(g), s));
-  }
-  cudaError_t e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
-  if (e != cudaSuccess) return e;
   {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features in <= 2 halves)
     TcArgs a{};
     base_args(a, g, r);
@@ -1419,6 +1405,25 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   } else if (!accumulate) {
     if (cudaMemsetAsync(dw_r, 0, (size_t)g.G * g.d * 4, s) != cudaSuccess) return cudaErrorUnknown;
   }
+  // all of dw1 | dw2 | dw_r are final here: a data-parallel caller can start the
+  // gradient all-reduce at this event while dX is computed below
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
+  {  // a8: dXp = dZ W1_b, then combine with the router term
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
+                                (uint64_t)g.mp * g.bw, 64, 128) &&
+              make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, 64);
+    ok = ok && make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
+    a.BN = 256;
+    a.out = b.part;
+    a.unit_offsets = b.unit_offsets;
+    TRY(launch<K_DX>(a, units_upper(g), s));
+  }
+  e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
+  if (e != cudaSuccess) return e;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (dgate_out) return launch_gather_dgate(g, r, b.dgate, dgate_out, s);
   return cudaSuccess;

@@ -56,6 +56,31 @@ def allreduce_grads(fg: FlatGrads, group=None, async_op: bool = False):
     return dist.all_reduce(fg.flat, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
 
 
+class OverlappedAllReduce:
+    """SUM all-reduce of the flat gradients that starts, on its own stream, at
+    the event spt_ffn_backward records once dw1/dw2/dw_r are final, so it runs
+    concurrently with the grad-input kernels of the same backward call."""
+
+    def __init__(self, fg: FlatGrads, group=None):
+        self.fg, self.group = fg, group
+        self.event = torch.cuda.Event()
+        self.stream = torch.cuda.Stream()
+        self.active = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+
+    def launch(self):
+        """Call right after spt_ffn_backward(..., dw_event=self.event)."""
+        if not self.active:
+            return
+        with torch.cuda.stream(self.stream):
+            self.stream.wait_event(self.event)
+            dist.all_reduce(self.fg.flat, op=dist.ReduceOp.SUM, group=self.group)
+
+    def wait(self, stream=None):
+        """Make `stream` (default: current) wait for the all-reduce."""
+        if self.active:
+            (stream or torch.cuda.current_stream()).wait_stream(self.stream)
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a per-rank scalar (device timing is reported as the max over ranks)."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:

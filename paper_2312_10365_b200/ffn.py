@@ -84,11 +84,14 @@ def spt_ffn_forward(desc, x, w1, w2, route: RouteBuffers, y, stash, ws, stream=N
 
 
 def spt_ffn_backward(desc, x, w1, w2, w_r, route: RouteBuffers, stash, dy, dx, dw1, dw2, dw_r,
-                     ws, dgate=None, flags: int = 0, stream=None):
+                     ws, dgate=None, flags: int = 0, stream=None, dw_event=None):
+    """dw_event: optional torch.cuda.Event recorded once dw1/dw2/dw_r are final
+    (before dx is computed) -- start a gradient all-reduce there."""
     rb = route.as_c()
+    ev = None if dw_event is None else ctypes.c_void_p(dw_event.cuda_event)
     L.check("spt_ffn_backward", L.lib().spt_ffn_backward(
         ctypes.byref(desc), _p(x), _p(w1), _p(w2), _p(w_r), ctypes.byref(rb), _p(stash), _p(dy), _p(dx),
-        _p(dw1), _p(dw2), _p(dw_r), _p(dgate), flags, _p(ws), ws.numel() * ws.element_size(),
+        _p(dw1), _p(dw2), _p(dw_r), _p(dgate), flags, _p(ws), ws.numel() * ws.element_size(), ev,
         _stream(stream)))
 
 
@@ -146,7 +149,8 @@ class RoutedFFN:
         spt_ffn_forward(self.desc, x, w1, w2, self.route_buf, self.y, self.stash, self.ws, stream)
         return self.y
 
-    def backward(self, x, w1, w2, w_r, dy, flags=0, want_dgate=False, stream=None):
+    def backward(self, x, w1, w2, w_r, dy, flags=0, want_dgate=False, stream=None, dw_event=None):
         spt_ffn_backward(self.desc, x, w1, w2, w_r, self.route_buf, self.stash, dy, self.dx, self.dw1,
-                         self.dw2, self.dw_r, self.ws, self.dgate if want_dgate else None, flags, stream)
+                         self.dw2, self.dw_r, self.ws, self.dgate if want_dgate else None, flags, stream,
+                         dw_event)
         return self.dx, self.dw1, self.dw2, self.dw_r

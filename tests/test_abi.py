@@ -77,7 +77,7 @@ def test_null_pointers_rejected_before_any_launch():
     assert L.spt_ffn_forward(ctypes.byref(d), None, None, None, ctypes.byref(rb), None, None,
                              None, 0, None) == 1
     assert L.spt_ffn_backward(ctypes.byref(d), *([None] * 4), ctypes.byref(rb), *([None] * 7),
-                              0, None, 0, None) == 1
+                              0, None, 0, None, None) == 1
     s = ctypes.c_size_t()
     assert L.spt_ffn_sizes(None, ctypes.byref(s), ctypes.byref(s)) == 1
     assert L.spt_ffn_sizes(ctypes.byref(d), None, ctypes.byref(s)) == 1

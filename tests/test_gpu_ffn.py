@@ -125,3 +125,28 @@ def test_deterministic(orc, name):
     b = gpu_run(cfg, T, inp)
     for n in NAMES + ("logits", "bucket_token"):
         assert np.array_equal(a[n], b[n]), n
+
+
+@pytest.mark.parametrize("name", ["tiny", "llama"])
+def test_dw_event_marks_final_gradients(orc, name):
+    """spt_ffn_backward records dw_event once dw1/dw2/dw_r are final (before dx):
+    snapshots taken on another stream right after the event equal the results."""
+    import torch
+    import paper_2312_10365_b200 as P
+    from helpers import to_dev, torch_dtype
+    cfg = S.CONFIGS[name]
+    T = 700
+    inp = S.make_inputs(cfg, T)
+    f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, torch_dtype(cfg), cfg.act, cfg.gate)
+    x, w1, w2, w_r, dy = (to_dev(inp[n], cfg) for n in ("x", "w1", "w2", "w_r", "dy"))
+    f.route(x, w_r)
+    f.forward(x, w1, w2)
+    ev = torch.cuda.Event()
+    f.backward(x, w1, w2, w_r, dy, dw_event=ev)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        side.wait_event(ev)
+        snap = [t.clone() for t in (f.dw1, f.dw2, f.dw_r)]
+    torch.cuda.synchronize()
+    for a, b in zip(snap, (f.dw1, f.dw2, f.dw_r)):
+        assert torch.equal(a, b)
