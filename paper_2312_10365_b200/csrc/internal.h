@@ -58,7 +58,7 @@ struct Bufs {
   int32_t* tile_block;    // [ceil(T*k/128) + G]: block of each 128-row bucket tile
 };
 
-constexpr int kUnitMTiles = 16;  // m-tiles per weight-resident unit (FWD2 / DX)
+int unit_mtiles();  // m-tiles per weight-resident unit (FWD2 / DX); SPT_FFN_UNIT_MT, default 128
 constexpr int kRasterBlocks = 16;  // blocks per L2 raster group of the gathered-A GEMMs
 
 void count_launch(int n = 1);

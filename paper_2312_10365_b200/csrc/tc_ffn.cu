@@ -66,6 +66,7 @@ struct TcArgs {
   const int32_t* tile_list;     // FWD1/DA: (mt << 8 | b) in m-tile-major order
   const int32_t* unit_offsets;  // FWD2/DX: weight-resident unit prefix per block
   int n_stg;                    // FWD2/DX: 4 KB staging buffers per epilogue warp (1 or 2)
+  int unit_mt;                  // FWD2/DX: m-tiles per weight-resident unit
   int prefetch;                 // gathering kinds: L2 prefetch of gathered rows (SPT_FFN_PREFETCH)
   unsigned long long* trace;    // SPT_FFN_TRACE: per-CTA role cycle counters (diagnostics)
   int ablate;                   // SPT_FFN_ABLATE (timing experiments only; results wrong):
@@ -99,7 +100,7 @@ __host__ __device__ constexpr bool kind_b_mn(int k) {
   return !(k == K_ROUTER || k == K_FWD1 || k == K_DA || k == K_DAT);
 }
 // FWD2 / DX keep one (block, 256-column) weight slab resident in smem and
-// stream up to kUnitMTiles A tiles of that block through it
+// stream up to unit_mtiles() A tiles of that block through it
 __host__ __device__ constexpr bool kind_bres(int k) { return k == K_FWD2 || k == K_DX; }
 __host__ __device__ constexpr int b_bytes(int kind, int BN) {
   return kind_bres(kind) ? 0 : (kind_b_mn(kind) ? 32768 : BN * 128);
@@ -193,8 +194,8 @@ __device__ __forceinline__ UnitInfo decode_unit(const TcArgs& a, int u) {
   ui.nt = r % a.NT;
   const int mc = r / a.NT;
   const int ntb = a.r.tile_offsets[ui.b + 1] - a.r.tile_offsets[ui.b];
-  ui.mt0 = mc * kUnitMTiles;
-  ui.mt1 = min(ntb, ui.mt0 + kUnitMTiles);
+  ui.mt0 = mc * a.unit_mt;
+  ui.mt1 = min(ntb, ui.mt0 + a.unit_mt);
   return ui;
 }
 template <int KIND>
@@ -638,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         uint32_t phase = 0, uph = 0;
         for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
           const UnitInfo ui = decode_unit(a, u);
-          mbar_wait(bres_empty, uph ^ 1);
+          twait(bres_empty, uph ^ 1, tr, 4);
           mbar_arrive_expect_tx(bres_full, kbu * 32768u);
           for (int kb = 0; kb < kbu; ++kb) {
             int krow;
@@ -652,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           for (int mt = ui.mt0; mt < ui.mt1; ++mt) {
             const int64_t prow0 = (int64_t)(a.r.tile_offsets[ui.b] + mt) * 128;
             for (int kb = 0; kb < kbu; ++kb) {
-              mbar_wait(&empty[stage], phase ^ 1);
+              twait(&empty[stage], phase ^ 1, tr, 4);
               mbar_arrive_expect_tx(&full[stage], kABytes);
               tma_load_2d(ring + stage * kABytes, &a.ta, &full[stage], kb * 64, (int)prow0);
               if (++stage == n_stages) { stage = 0; phase ^= 1; }
@@ -667,14 +668,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         uint32_t phase = 0, aphase = 0, uph = 0;
         for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
           const UnitInfo ui = decode_unit(a, u);
-          mbar_wait(bres_full, uph);
+          twait(bres_full, uph, tr, 5);
           uph ^= 1;
           for (int mt = ui.mt0; mt < ui.mt1; ++mt) {
-            mbar_wait(&tempty[acc], aphase ^ 1);
+            twait(&tempty[acc], aphase ^ 1, tr, 1);
             tc_fence_after();
+            if (tr) tr[7] += 1;
             const uint32_t dtm = tmem + acc * 256;
             for (int kb = 0; kb < kbu; ++kb) {
-              mbar_wait(&full[stage], phase);
+              twait(&full[stage], phase, tr, 0);
               tc_fence_after();
               const uint32_t sa = smem_u32(ring + stage * kABytes);
               const uint32_t sb = smem_u32(sBres + kb * 32768);
@@ -702,12 +704,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const UnitInfo ui = decode_unit(a, u);
         for (int mt = ui.mt0; mt < ui.mt1; ++mt) {
           const TileInfo ti = decode_mtile<KIND>(a, ui, mt);
-          mbar_wait(&tfull[acc], aphase);
+          twait(&tfull[acc], aphase, (tr && threadIdx.x == 4 * 32) ? tr : nullptr, 2);
           tc_fence_after();
+          const long long te0 = clock64();
           epilogue_tma_store(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, q, lane, half,
                              stg_base + e * a.n_stg * 4096, stg_i);
           tc_fence_before();
           __syncwarp();
+          if (tr && threadIdx.x == 4 * 32) tr[3] += (unsigned long long)(clock64() - te0);
           if (lane == 0) mbar_arrive(&tempty[acc]);
           if (++acc == 2) { acc = 0; aphase ^= 1; }
         }
@@ -1049,6 +1053,7 @@ static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
   a.gpad = g.gpad;
   a.NT = (int)ceil_div(g.d, 256);
   a.MH = 1;
+  a.unit_mt = unit_mtiles();
   static int pf = -1;  // SPT_FFN_PREFETCH=1 enables the L2 prefetch of gathered rows
   if (pf < 0) {
     const char* e = getenv("SPT_FFN_PREFETCH");
@@ -1065,6 +1070,16 @@ static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
 }
 
 static int bucket_tiles_upper(const Geom& g) { return (int)(ceil_div(g.pairs, 128) + g.G); }
+
+int unit_mtiles() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("SPT_FFN_UNIT_MT");
+    v = e ? atoi(e) : 128;  // measured r01: 128 (~ a whole block per unit) best at LLaMA scale
+    if (v < 1) v = 128;
+  }
+  return v;
+}
 
 // a7 variant.  Default: the fused dA kernel (tokens on M, N = bw, dgate/dZ in the
 // epilogue).  SPT_FFN_DAT=1: tokens on N (N = 256, transposed dA via TMA store)
@@ -1115,7 +1130,8 @@ cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logi
 //  tile_list[P(mt) + rank_b(mt)] = mt << 8 | b, i.e. bucket tiles in (m-tile,
 //  block) order with P(mt) = sum_b min(nt_b, mt) and rank_b(mt) = #{b' < b :
 //  nt_b' > mt};  unit_offsets = prefix over blocks of ceil(nt_b/16) * NT.
-__global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, const int32_t* __restrict__ tile_offsets,
+__global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, int unit_mt,
+                                                         const int32_t* __restrict__ tile_offsets,
                                                          int32_t* __restrict__ tile_list,
                                                          int32_t* __restrict__ unit_offsets,
                                                          int32_t* __restrict__ tile_block) {
@@ -1146,7 +1162,7 @@ __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, const in
     int run = 0;
     for (int bb = 0; bb < G; ++bb) {
       unit_offsets[bb] = run;
-      run += (int)ceil_div(ntu[bb], kUnitMTiles) * NT;
+      run += (int)ceil_div(ntu[bb], unit_mt) * NT;
     }
     unit_offsets[G] = run;
     int pairs = 0;
@@ -1157,7 +1173,8 @@ __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, const in
 
 static cudaError_t build_schedules(const Geom& g, const RouteView& r, const Bufs& b, cudaStream_t s) {
   prof_begin("tile_sched", s);
-  tile_sched_kernel<<<g.G, 256, 0, s>>>(g.G, (int)ceil_div(g.d, 256), r.tile_offsets, b.tile_list,
+  tile_sched_kernel<<<g.G, 256, 0, s>>>(g.G, (int)ceil_div(g.d, 256), unit_mtiles(), r.tile_offsets,
+                                        b.tile_list,
                                         b.unit_offsets, b.tile_block);
   prof_end(s);
   count_launch();
@@ -1165,7 +1182,7 @@ static cudaError_t build_schedules(const Geom& g, const RouteView& r, const Bufs
 }
 
 static int units_upper(const Geom& g) {
-  return (int)((ceil_div(bucket_tiles_upper(g), kUnitMTiles) + g.G) * ceil_div(g.d, 256));
+  return (int)((ceil_div(bucket_tiles_upper(g), unit_mtiles()) + g.G) * ceil_div(g.d, 256));
 }
 
 cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void* w2,
