@@ -91,21 +91,28 @@ __global__ void __launch_bounds__(1024) topk_hist_kernel(int64_t T, int G, int k
         key[s] = ((unsigned long long)ab << 9) | (unsigned long long)(256 - b);
       }
     }
+    // k rounds of a warp argmax in two 32-bit redux steps: the largest |logit|
+    // bit key (+1, so 0 means "no candidate"), then the lowest block id among
+    // the lanes holding it.  A lane's candidate is its lowest unselected slot
+    // with its largest key, so the order is exactly (key desc, id asc).
     for (int r = 0; r < k; ++r) {
-      unsigned long long best = 0ull;
+      uint32_t bk = 0u;
+      int bs = -1;
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
-        if (!sel[s] && key[s] > best) best = key[s];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-        best = other > best ? other : best;
+      for (int s = 0; s < 8; ++s) {
+        const uint32_t ks = (uint32_t)(key[s] >> 9);  // |logit| bit pattern
+        if (key[s] != 0ull && !sel[s] && (bs < 0 || ks > bk)) {
+          bk = ks;
+          bs = s;
+        }
       }
-      const int bsel = 256 - (int)(best & 511ull);
-      if ((bsel & 31) == lane) {
+      const uint32_t m = __reduce_max_sync(0xffffffffu, bs >= 0 ? bk + 1u : 0u);
+      const uint32_t mine = (bs >= 0 && bk + 1u == m) ? (uint32_t)(bs * 32 + lane) : 0xffffffffu;
+      const uint32_t w = __reduce_min_sync(0xffffffffu, mine);
+      if ((int)(w & 31u) == lane) {
 #pragma unroll
         for (int s = 0; s < 8; ++s)
-          if (s == (bsel >> 5)) sel[s] = true;
+          if (s == (int)(w >> 5)) sel[s] = true;
       }
     }
     // emit ascending block ids: slot-major ballots

@@ -70,7 +70,9 @@ struct TcArgs {
   int prefetch;                 // gathering kinds: L2 prefetch of gathered rows (SPT_FFN_PREFETCH)
   unsigned long long* trace;    // SPT_FFN_TRACE: per-CTA role cycle counters (diagnostics)
   int ablate;                   // SPT_FFN_ABLATE (timing experiments only; results wrong):
-                                //  1 = skip gathered-row copies, 2 = skip FWD1 epilogue stores
+                                //  1 = skip gathered-row copies, 2 = skip FWD1 epilogue stores,
+                                //  3 = no operand loads at all, 4 = 3 + no epilogue work,
+                                //  5 = 4 + no proxy fence before the MMAs, 6 = 5 + no full waits
 
 };
 
@@ -554,6 +556,21 @@ __device__ __forceinline__ void epilogue_dat(const TcArgs& a, const TileInfo& ti
   }
 }
 
+// One K stage (4 x K=16) of MMAs into MH accumulator halves: descriptors are
+// advanced by constant adds (start address field, 16-byte units; no carry:
+// smem offsets < 256 KB), the A half h lives 16 KB after half 0.
+template <int MH>
+__device__ __forceinline__ void issue_kstage(uint32_t dtm, uint32_t hstride, uint64_t ad,
+                                             uint64_t bd, uint32_t a_kstep, uint32_t b_kstep,
+                                             uint32_t idesc, bool accumulate) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int h = 0; h < MH; ++h)
+      mma_bf16(dtm + h * hstride, ad + h * (16384 >> 4) + k * a_kstep, bd + k * b_kstep, idesc,
+               (accumulate || k != 0) ? 1u : 0u);
+}
+
 // diagnostics: cycles spent in an mbarrier wait, accumulated into trace slot
 __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, unsigned long long* tr, int slot) {
   if (tr) {
@@ -662,38 +679,41 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
       }
     } else if (warp == 1) {
-      if (lane == 0) {
-        const uint32_t idesc = idesc_bf16(128, 256, false, true);
-        int stage = 0, acc = 0;
-        uint32_t phase = 0, aphase = 0, uph = 0;
-        for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
-          const UnitInfo ui = decode_unit(a, u);
-          twait(bres_full, uph, tr, 5);
-          uph ^= 1;
-          for (int mt = ui.mt0; mt < ui.mt1; ++mt) {
-            twait(&tempty[acc], aphase ^ 1, tr, 1);
+      // whole warp, one elected issuer (see the MMA issuer below)
+      const uint32_t idesc = idesc_bf16(128, 256, false, true);
+      const uint64_t adesc0 = sdesc_sw128(smem_u32(ring), 16, 1024);
+      const uint64_t bdesc0 = sdesc_sw128(smem_u32(sBres), 8192, 1024);
+      unsigned long long* trl = lane == 0 ? tr : nullptr;
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0, uph = 0;
+      for (int u = blockIdx.x; u < ntiles; u += gridDim.x) {
+        const UnitInfo ui = decode_unit(a, u);
+        twait(bres_full, uph, trl, 5);
+        uph ^= 1;
+        for (int mt = ui.mt0; mt < ui.mt1; ++mt) {
+          twait(&tempty[acc], aphase ^ 1, trl, 1);
+          tc_fence_after();
+          if (trl) trl[7] += 1;
+          const uint32_t dtm = tmem + acc * 256;
+          for (int kb = 0; kb < kbu; ++kb) {
+            twait(&full[stage], phase, trl, 0);
             tc_fence_after();
-            if (tr) tr[7] += 1;
-            const uint32_t dtm = tmem + acc * 256;
-            for (int kb = 0; kb < kbu; ++kb) {
-              twait(&full[stage], phase, tr, 0);
-              tc_fence_after();
-              const uint32_t sa = smem_u32(ring + stage * kABytes);
-              const uint32_t sb = smem_u32(sBres + kb * 32768);
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_bf16(dtm, sdesc_sw128(sa + k * 32, 16, 1024),
-                         sdesc_sw128(sb + k * 2048, 8192, 1024), idesc, (kb | k) != 0);
+            if (elect_one()) {
+              issue_kstage<1>(dtm, 0, adesc0 + (uint64_t)((stage * kABytes) >> 4),
+                              bdesc0 + (uint64_t)((kb * 32768) >> 4), 32 >> 4, 2048 >> 4, idesc,
+                              kb != 0);
               mma_commit(&empty[stage]);
-              if (++stage == n_stages) { stage = 0; phase ^= 1; }
             }
-            mma_commit(&tfull[acc]);
-            if (++acc == 2) { acc = 0; aphase ^= 1; }
+            __syncwarp();
+            if (++stage == n_stages) { stage = 0; phase ^= 1; }
           }
-          mma_commit(bres_empty);  // weight slab free once this unit's MMAs retire
+          if (elect_one()) mma_commit(&tfull[acc]);
+          __syncwarp();
+          if (++acc == 2) { acc = 0; aphase ^= 1; }
         }
+        if (elect_one()) mma_commit(bres_empty);  // weight slab free once this unit's MMAs retire
+        __syncwarp();
       }
-      __syncwarp();
     } else if (warp >= 4 && warp < 4 + kEpiWarps) {
       const int e = warp - 4;
       const int q = warp & 3;
@@ -725,8 +745,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     const int n_calls = kTmaRows / 4;
     const bool has_call = c < n_calls;
     const int my_calls = n_calls > p ? (n_calls - p + kTmaGatherWarps - 1) / kTmaGatherWarps : 0;
-    const uint32_t tx = (a.ablate == 1 ? 0u : (uint32_t)my_calls * 512u) +
-                        (p == 0 ? tile_tx_bytes<KIND>(a) : 0u);
+    const uint32_t tx = (a.ablate == 1 || a.ablate >= 3 ? 0u : (uint32_t)my_calls * 512u) +
+                        (p == 0 && a.ablate < 3 ? tile_tx_bytes<KIND>(a) : 0u);
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -751,8 +771,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
         __syncwarp();
         uint8_t* sA = smem + stage * sstride;
-        if (p == 0 && lane == 0) produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
-        if (has_call && a.ablate != 1) {
+        if (p == 0 && lane == 0 && a.ablate < 3)
+          produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
+        if (has_call && a.ablate != 1 && a.ablate < 3) {
           tma_gather4((kind_rows_on_b(KIND) ? sA + astride : sA) + c * 512, &a.ta, &full[stage],
                       kb * 64, rr[0], rr[1], rr[2], rr[3]);
           // warm L2 with the next 256 columns of these rows in one 512-byte run per
@@ -766,7 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   } else if (warp == 0) {
     // ------------------------------------------------- TMA tile producer
     if (lane == 0) {
-      const uint32_t tx = tile_tx_bytes<KIND>(a);
+      const uint32_t tx = a.ablate >= 3 ? 0u : tile_tx_bytes<KIND>(a);
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -775,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           twait(&empty[stage], phase ^ 1, tr, 4);
           mbar_arrive_expect_tx(&full[stage], tx);
           uint8_t* sA = smem + stage * sstride;
-          produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
+          if (a.ablate < 3) produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
           if (++stage == n_stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -803,7 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const uint32_t sA = smem_u32(smem + stage * sstride + (kind_rows_on_b(KIND) ? astride : 0));
 #pragma unroll
         for (int i = 0; i < kRowsPer; ++i) {
-          if (a.ablate == 1) break;
+          if (a.ablate == 1 || a.ablate >= 3) break;
           const int r = kTmaRows + (t >> 3) + 16 * i;
           const uint32_t dst = sA + (r >> 7) * 16384 + (r & 127) * 128 + ((ch ^ (r & 7)) << 4);
           const __nv_bfloat16* g = src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kb * 64 + ch * 8;
@@ -869,42 +890,47 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     }
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer
+    // The whole warp runs the loop (every value warp-uniform, so descriptors
+    // live in uniform registers) and one elected lane issues: a lean issue
+    // loop matters, at 8 MMAs per ~1024-clk k-stage a generic one is slower
+    // than the tensor pipe (measured: 58% vs 90% of the MMA rate).
     const uint32_t idesc = idesc_bf16(128, a.BN, kAmn, kBmn);
+    const uint32_t a_kstep = kAmn ? 2048 >> 4 : 32 >> 4;  // descriptor units (16 B)
+    const uint32_t b_kstep = kBmn ? 2048 >> 4 : 32 >> 4;
+    const uint32_t hstride = (uint32_t)tm_half_stride(a.BN);
+    const uint64_t adesc0 = sdesc_sw128(smem_u32(smem), kAmn ? 8192 : 16, 1024);
+    const uint64_t bdesc0 = kBmn ? sdesc_sw128(smem_u32(smem) + astride, 8192, 1024)
+                                 : sdesc_sw128(smem_u32(smem) + astride, 16, 1024);
+    unsigned long long* trl = lane == 0 ? tr : nullptr;
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo ti = decode<KIND>(a, tile);
-      if (lane == 0) {
-        twait(&tempty[acc], aphase ^ 1, tr, 1);
+      twait(&tempty[acc], aphase ^ 1, trl, 1);
+      tc_fence_after();
+      if (trl) trl[7] += 1;
+      const uint32_t dtm = tmem + tm_col(a.BN, a.MH, acc, 0);
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        if (a.ablate < 6) twait(&full[stage], phase, trl, 0);
+        const long long tf0 = trl ? clock64() : 0;
+        // cp.async writes are generic-proxy: order them before the UMMA reads
+        if (kGather && a.ablate < 5) fence_proxy_async_smem();
         tc_fence_after();
-        if (tr) tr[7] += 1;
-        for (int kb = 0; kb < ti.nkb; ++kb) {
-          twait(&full[stage], phase, tr, 0);
-          const long long tf0 = tr ? clock64() : 0;
-          // cp.async writes are generic-proxy: order them before the UMMA reads
-          if (kGather) fence_proxy_async_smem();
-          tc_fence_after();
-          if (tr) tr[5] += (unsigned long long)(clock64() - tf0);
-          const uint32_t sa = smem_u32(smem + stage * sstride);
-          const uint32_t sb = sa + astride;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t bd = kBmn ? sdesc_sw128(sb + k * 2048, 8192, 1024)
-                                     : sdesc_sw128(sb + k * 32, 16, 1024);
-            for (int h = 0; h < a.MH; ++h) {
-              const uint64_t ad = kAmn ? sdesc_sw128(sa + h * 16384 + k * 2048, 8192, 1024)
-                                       : sdesc_sw128(sa + h * 16384 + k * 32, 16, 1024);
-              const uint32_t dtm = tmem + tm_col(a.BN, a.MH, acc, h);
-              mma_bf16(dtm, ad, bd, idesc, (kb | k) != 0);
-            }
-          }
+        if (trl) trl[5] += (unsigned long long)(clock64() - tf0);
+        const uint64_t soff = (uint64_t)((stage * sstride) >> 4);
+        if (elect_one()) {
+          if (a.MH == 2)
+            issue_kstage<2>(dtm, hstride, adesc0 + soff, bdesc0 + soff, a_kstep, b_kstep, idesc, kb != 0);
+          else
+            issue_kstage<1>(dtm, hstride, adesc0 + soff, bdesc0 + soff, a_kstep, b_kstep, idesc, kb != 0);
           mma_commit(&empty[stage]);
-          if (++stage == n_stages) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        __syncwarp();
+        if (++stage == n_stages) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) mma_commit(&tfull[acc]);
       __syncwarp();
       if (++acc == n_acc) { acc = 0; aphase ^= 1; }
     }
@@ -922,7 +948,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       const long long te0 = clock64();
       const uint32_t lanes = (uint32_t)(q * 32) << 16;
       const int half = e >> 2;  // warp group: M half (pair tiles, DW1) or column half
-      if (kind_gather_a(KIND) && a.MH == 2) {
+      if (a.ablate >= 4) {
+      } else if (kind_gather_a(KIND) && a.MH == 2) {
         // M half `half` of a pair tile: this warp group owns its rows, all columns
         TileInfo th = ti;
         th.n_valid -= half * 128;
@@ -953,6 +980,166 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
 }
 
+// ============================================= CTA-pair weight-resident GEMMs
+// FWD2 / DX on CTA pairs (cta_group::2): a unit (block b, 256 output columns,
+// its m-tiles) runs on a 2-CTA cluster; CTA r computes m-tiles 2p + r, keeps
+// the N-half [r*128, r*128+128) of the weight slab resident (half the smem of
+// the 1-CTA kernel, so the A ring is twice as deep) and the leader issues
+// M = 256, N = 256 MMAs.  Barriers: stage / slab "full" live in the leader
+// (both CTAs' TMA bytes land there), "empty" / "tfull" are multicast to both
+// CTAs by tcgen05.commit, "tempty" lives in the leader and counts the epilogue
+// warps of both CTAs (the peer arrives remotely).
+template <int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_pair_kernel(const __grid_constant__ TcArgs a, int n_stages) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;  // K stages
+  uint8_t* sBres = smem;                       // kbu x 16 KB (this CTA's 128 columns)
+  uint8_t* ring = smem + kbu * 16384;          // n_stages x 16 KB A stages
+  uint64_t* full = (uint64_t*)(ring + n_stages * kABytes);
+  uint64_t* empty = full + n_stages;
+  uint64_t* tfull = empty + n_stages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bres_full = tempty + 2;
+  uint64_t* bres_empty = bres_full + 1;
+  uint32_t* tmem_slot = (uint32_t*)(bres_empty + 1);
+  uint8_t* stg_base = (uint8_t*)(((uintptr_t)(tmem_slot + 4) + 1023) & ~(uintptr_t)1023);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiWarps);
+    }
+    mbar_init(bres_full, 1);
+    mbar_init(bres_empty, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised before any cross-CTA traffic
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nunits = a.unit_offsets[a.G];
+  unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  const long long t_start = clock64();
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer (both CTAs): own slab half + own m-tile rows
+      int stage = 0;
+      uint32_t phase = 0, uph = 0;
+      for (int u = cid; u < nunits; u += ncl) {
+        const UnitInfo ui = decode_unit(a, u);
+        twait(bres_empty, uph ^ 1, tr, 4);
+        if (leader) mbar_arrive_expect_tx(bres_full, 2u * kbu * 16384u);
+        for (int kb = 0; kb < kbu; ++kb) {
+          int krow;
+          if (KIND == K_FWD2) krow = ui.b * a.bw + kb * 64;
+          else krow = kb * 64 < a.bw ? ui.b * a.bw + kb * 64 : a.D + ui.b * a.bw + (kb * 64 - a.bw);
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            tma_load_2d_pair(sBres + kb * 16384 + j * 8192, &a.tb, bres_full,
+                             ui.nt * 256 + (int)rank * 128 + j * 64, krow);
+        }
+        uph ^= 1;
+        for (int mt = ui.mt0; mt < ui.mt1; mt += 2) {
+          const int64_t prow0 = (int64_t)(a.r.tile_offsets[ui.b] + mt + (int)rank) * 128;
+          for (int kb = 0; kb < kbu; ++kb) {
+            twait(&empty[stage], phase ^ 1, tr, 4);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2u * kABytes);
+            tma_load_2d_pair(ring + stage * kABytes, &a.ta, &full[stage], kb * 64, (int)prow0);
+            if (++stage == n_stages) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {  // MMA issuer (leader only; whole warp, one elected lane issues)
+      const uint32_t idesc = idesc_bf16(256, 256, false, true);
+      const uint64_t adesc0 = sdesc_sw128(smem_u32(ring), 16, 1024);
+      const uint64_t bdesc0 = sdesc_sw128(smem_u32(sBres), 8192, 1024);
+      unsigned long long* trl = lane == 0 ? tr : nullptr;
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0, uph = 0;
+      for (int u = cid; u < nunits; u += ncl) {
+        const UnitInfo ui = decode_unit(a, u);
+        twait(bres_full, uph, trl, 5);
+        uph ^= 1;
+        for (int mt = ui.mt0; mt < ui.mt1; mt += 2) {
+          twait(&tempty[acc], aphase ^ 1, trl, 1);
+          tc_fence_after();
+          if (trl) trl[7] += 1;
+          const uint32_t dtm = tmem + acc * 256;
+          for (int kb = 0; kb < kbu; ++kb) {
+            twait(&full[stage], phase, trl, 0);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t ad = adesc0 + (uint64_t)((stage * kABytes) >> 4);
+              const uint64_t bd = bdesc0 + (uint64_t)((kb * 16384) >> 4);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_pair(dtm, ad + k * 2, bd + k * 128, idesc, (kb != 0 || k != 0) ? 1u : 0u);
+              mma_commit_pair(&empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == n_stages) { stage = 0; phase ^= 1; }
+          }
+          if (elect_one()) mma_commit_pair(&tfull[acc]);
+          __syncwarp();
+          if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
+        if (elect_one()) mma_commit_pair(bres_empty);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + kEpiWarps) {  // epilogue (both CTAs): own m-tile
+    const int e = warp - 4;
+    const int q = warp & 3;
+    const int half = e >> 2;
+    int acc = 0, stg_i = 0;
+    uint32_t aphase = 0;
+    for (int u = cid; u < nunits; u += ncl) {
+      const UnitInfo ui = decode_unit(a, u);
+      for (int mt = ui.mt0; mt < ui.mt1; mt += 2) {
+        const int my_mt = mt + (int)rank;
+        twait(&tfull[acc], aphase, (tr && threadIdx.x == 4 * 32) ? tr : nullptr, 2);
+        tc_fence_after();
+        const long long te0 = clock64();
+        if (my_mt < ui.mt1) {  // the pair's second m-tile may not exist
+          const TileInfo ti = decode_mtile<KIND>(a, ui, my_mt);
+          epilogue_tma_store(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, q, lane, half,
+                             stg_base + e * a.n_stg * 4096, stg_i);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (tr && threadIdx.x == 4 * 32) tr[3] += (unsigned long long)(clock64() - te0);
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[acc]);
+          else mbar_arrive_remote(&tempty[acc], 0);
+        }
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[6] = (unsigned long long)(clock64() - t_start);
+  cluster_sync();  // the leader's MMAs into this CTA's TMEM / smem are done
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem);
+  }
+}
+
 // ====================================================================== host
 static bool debug_sync() {  // SPT_FFN_DEBUG_SYNC=1: synchronise + report after each GEMM launch
   static int v = -1;
@@ -972,6 +1159,38 @@ static int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+// SPT_FFN_TRACE=1: per-CTA role cycle counters (slots: kTraceSlots above),
+// summed over the grid and printed after a synchronising readback
+static unsigned long long* g_trace_buf = nullptr;
+static bool trace_begin(TcArgs& a, cudaStream_t s) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SPT_FFN_TRACE");
+    on = (e && e[0] == '1') ? 1 : 0;
+    if (on) cudaMalloc(&g_trace_buf, 1024 * kTraceSlots * sizeof(unsigned long long));
+  }
+  if (!on) return false;
+  cudaMemsetAsync(g_trace_buf, 0, 1024 * kTraceSlots * sizeof(unsigned long long), s);
+  a.trace = g_trace_buf;
+  return true;
+}
+static void trace_report(TcArgs& a, const char* name, int grid, cudaStream_t s) {
+  unsigned long long h[1024 * kTraceSlots];
+  cudaMemcpyAsync(h, g_trace_buf, sizeof(unsigned long long) * grid * kTraceSlots,
+                  cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  double sum[kTraceSlots] = {0};
+  for (int b = 0; b < grid; ++b)
+    for (int i = 0; i < kTraceSlots; ++i) sum[i] += (double)h[b * kTraceSlots + i];
+  const double tot = sum[6] > 0 ? sum[6] : 1;
+  fprintf(stderr,
+          "[spt-trace] %-16s tiles/cta %.1f | MMA wait full %.0f%% wait tempty %.0f%% slab/fences "
+          "%.0f%% | epi wait %.0f%% busy %.0f%% | tma prod wait empty %.0f%% | cta cycles %.0f\n",
+          name, sum[7] / grid, 100 * sum[0] / tot, 100 * sum[1] / tot, 100 * sum[5] / tot,
+          100 * sum[2] / tot, 100 * sum[3] / tot, 100 * sum[4] / tot, tot / grid);
+  a.trace = nullptr;
 }
 
 template <int KIND>
@@ -1000,36 +1219,11 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   static const char* kNames[] = {"tc_router", "tc_fwd1_gate_up", "tc_fwd2_down", "tc_bwd_dA",
                                  "tc_bwd_dX", "tc_bwd_dW1", "tc_bwd_dW2", "tc_bwd_dWR",
                                  "tc_bwd_dAT"};
-  static unsigned long long* trace_buf = nullptr;
-  static int trace_on = -1;
-  if (trace_on < 0) {
-    const char* e = getenv("SPT_FFN_TRACE");
-    trace_on = (e && e[0] == '1') ? 1 : 0;
-    if (trace_on) cudaMalloc(&trace_buf, 1024 * kTraceSlots * sizeof(unsigned long long));
-  }
-  if (trace_on) {
-    cudaMemsetAsync(trace_buf, 0, 1024 * kTraceSlots * sizeof(unsigned long long), s);
-    a.trace = trace_buf;
-  }
+  const bool trace_on = trace_begin(a, s);
   prof_begin(kNames[KIND], s);
   tc_gemm_kernel<KIND><<<grid, kThreads, smem, s>>>(a, stages);
   prof_end(s);
-  if (trace_on) {
-    unsigned long long h[1024 * kTraceSlots];
-    cudaMemcpyAsync(h, trace_buf, sizeof(unsigned long long) * grid * kTraceSlots,
-                    cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    double sum[kTraceSlots] = {0};
-    for (int b = 0; b < grid; ++b)
-      for (int i = 0; i < kTraceSlots; ++i) sum[i] += (double)h[b * kTraceSlots + i];
-    const double tot = sum[6] > 0 ? sum[6] : 1;
-    fprintf(stderr,
-            "[spt-trace] %-16s tiles/cta %.1f | MMA wait full %.0f%% wait tempty %.0f%% fences "
-            "%.0f%% | epi wait %.0f%% busy %.0f%% | tma prod wait empty %.0f%% | cta cycles %.0f\n",
-            kNames[KIND], sum[7] / grid, 100 * sum[0] / tot, 100 * sum[1] / tot, 100 * sum[5] / tot,
-            100 * sum[2] / tot, 100 * sum[3] / tot, 100 * sum[4] / tot, tot / grid);
-    a.trace = nullptr;
-  }
+  if (trace_on) trace_report(a, kNames[KIND], grid, s);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (debug_sync()) {
@@ -1038,6 +1232,77 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
             stages, smem, a.BN, a.MH, cudaGetErrorString(e));
   }
   return e;
+}
+
+// SPT_FFN_PAIR=1 selects the CTA-pair weight-resident kernel for FWD2 / DX
+// (correct, measured slower on B200 in r01: these GEMMs are bound by the
+// partial-output writes, and the pair couples two CTAs' epilogues)
+static bool use_pair() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_PAIR");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <int KIND>
+static cudaError_t launch_pair(TcArgs& a, int units_upper, cudaStream_t s) {
+  const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
+  const int slab = kbu * 16384;  // this CTA's 128-column half of the slab
+  const int extra = 1024 + 256;
+  a.n_stg = slab > 32768 ? 1 : 2;
+  const int stg = kEpiWarps * a.n_stg * 4096 + 1024;
+  const int stages = std::min(8, (227 * 1024 - extra - slab - stg) / kABytes);
+  const int smem = slab + stages * kABytes + extra + stg;
+  static bool attr_set = false;
+  static int max_clusters = 0;  // co-resident 2-CTA clusters (GPCs may hold odd SM counts)
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_pair_kernel<KIND>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(num_sms());
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 2;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, tc_pair_kernel<KIND>, &cfg) != cudaSuccess ||
+        max_clusters <= 0) {
+      cudaGetLastError();
+      max_clusters = num_sms() / 2;
+    }
+    if (debug_sync()) fprintf(stderr, "[spt] pair kind %d: max active clusters %d\n", KIND, max_clusters);
+    attr_set = true;
+  }
+  const int clusters = std::max(1, std::min(units_upper, max_clusters));
+  const bool trace_on = trace_begin(a, s);
+  const char* name = KIND == K_FWD2 ? "tc_fwd2_down" : "tc_bwd_dX";
+  prof_begin(name, s);
+  tc_pair_kernel<KIND><<<2 * clusters, kThreads, smem, s>>>(a, stages);
+  prof_end(s);
+  if (trace_on) trace_report(a, name, 2 * clusters, s);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (debug_sync()) {
+    e = cudaStreamSynchronize(s);
+    fprintf(stderr, "[spt] tc pair kind %d clusters %d stages %d smem %d: %s\n", KIND, clusters,
+            stages, smem, cudaGetErrorString(e));
+  }
+  return e;
+}
+
+template <int KIND>
+static cudaError_t launch_bres(TcArgs& a, int units_upper, cudaStream_t s) {
+  const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
+  const bool fits = 227 * 1024 - 1280 - kbu * 16384 - (kEpiWarps * 4096 + 1024) >= 3 * kABytes;
+  if (fits && use_pair()) return launch_pair<KIND>(a, units_upper, s);
+  return launch<KIND>(a, units_upper, s);
 }
 
 static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
@@ -1215,7 +1480,7 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
     a.BN = 256;
     a.out = b.part;
     a.unit_offsets = b.unit_offsets;
-    TRY(launch<K_FWD2>(a, units_upper(g), s));
+    TRY(launch_bres<K_FWD2>(a, units_upper(g), s));
   }
   return launch_combine_fwd(g, r, b.part, y, s);
 }
@@ -1437,7 +1702,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.BN = 256;
     a.out = b.part;
     a.unit_offsets = b.unit_offsets;
-    TRY(launch<K_DX>(a, units_upper(g), s));
+    TRY(launch_bres<K_DX>(a, units_upper(g), s));
   }
   e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
   if (e != cudaSuccess) return e;

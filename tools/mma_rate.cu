@@ -127,11 +127,112 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// Ring variant: the library's stage protocol without data.  `stages` stage
+// barriers; producers (nprod threads of warps 2.., one arrival each, plus the
+// optional cp.async-style noinc arrival) wait empty[s] then arrive on full[s];
+// the MMA thread waits full[s], issues 4 x MH MMAs (N=256), commits empty[s].
+// Every `tile_k` stages it commits to tfull and waits for it (accumulator drain).
+__global__ void __launch_bounds__(512, 1) ring_kernel(int iters, int stages, int nprod, int MH,
+                                                      int tile_k, int noinc, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[8], empty[8], tfull;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], nprod);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const int pt = threadIdx.x - 64;
+  if (threadIdx.x == 32) {
+    const uint32_t idesc = idesc_bf16(128, 256, false, false);
+    const uint32_t sa0 = smem_u32(smem);
+    const long long t0 = clock64();
+    int stage = 0;
+    uint32_t ph = 0, tph = 0;
+    for (int it = 0; it < iters; ++it) {
+      mbar_wait(&full[stage], ph);
+      const uint32_t sa = sa0 + stage * 65536u, sb = sa + 32768;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t bd = sdesc_sw128(sb + k * 32, 16, 1024);
+        for (int h = 0; h < MH; ++h)
+          mma_bf16(tmem + h * 256, sdesc_sw128(sa + h * 16384 + k * 32, 16, 1024), bd, idesc,
+                   (it | k) != 0);
+      }
+      mma_commit(&empty[stage]);
+      if (++stage == stages) { stage = 0; ph ^= 1; }
+      if (tile_k > 0 && (it % tile_k) == tile_k - 1) {
+        mma_commit(&tfull);
+        mbar_wait(&tfull, tph);
+        tph ^= 1;
+      }
+    }
+    mma_commit(&tfull);
+    mbar_wait(&tfull, tph);
+    cycles[blockIdx.x] = clock64() - t0;
+  } else if (pt >= 0 && pt < nprod) {
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int it = 0; it < iters; ++it) {
+      mbar_wait(&empty[stage], ph ^ 1);
+      if (noinc) {
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[stage]))
+                     : "memory");
+      } else {
+        mbar_arrive(&full[stage]);
+      }
+      if (++stage == stages) { stage = 0; ph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
 int main() {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   long long* d;
   cudaMalloc(&d, nsm * sizeof(long long));
+  {
+    const int rsmem = 1024 + 3 * 65536;
+    cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
+    struct R { int stages, nprod, MH, tile_k, noinc; } rs[] = {
+        {3, 1, 2, 0, 0},   {3, 1, 2, 64, 0},  {3, 131, 2, 64, 0}, {3, 131, 2, 64, 1},
+        {2, 1, 2, 64, 0},  {3, 1, 1, 64, 0},  {3, 131, 1, 64, 1}};
+    for (auto c : rs) {
+      const int iters = 4096;
+      ring_kernel<<<nsm, 512, rsmem>>>(64, c.stages, c.nprod, c.MH, c.tile_k, c.noinc, d);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      ring_kernel<<<nsm, 512, rsmem>>>(iters, c.stages, c.nprod, c.MH, c.tile_k, c.noinc, d);
+      cudaEventRecord(e1);
+      cudaError_t err = cudaEventSynchronize(e1);
+      if (err != cudaSuccess) { printf("ring error %s\n", cudaGetErrorString(err)); return 1; }
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      long long h[1024];
+      cudaMemcpy(h, d, nsm * sizeof(long long), cudaMemcpyDeviceToHost);
+      double cyc = 0;
+      for (int i = 0; i < nsm; ++i) cyc += h[i];
+      cyc /= nsm;
+      const double flop_sm = 2.0 * 128 * 256 * 64 * c.MH * iters;
+      printf("RING stages=%d nprod=%3d MH=%d tile_k=%2d noinc=%d: %.0f%% of 8192 FLOP/clk/SM (%.3f ms)\n",
+             c.stages, c.nprod, c.MH, c.tile_k, c.noinc, 100 * flop_sm / cyc / 8192, ms);
+    }
+  }
   const int smem = 1024 + 32768 + 32768;
   cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   struct C { int N, MH, bmn; } cs[] = {{64, 1, 0}, {128, 1, 0}, {256, 1, 0}, {128, 2, 0},
