@@ -158,6 +158,16 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
       "r"(rank)
       : "memory");
 }
+// relaxed remote arrive (no release fence): for signals whose data was made
+// visible by other means (a preceding proxy fence + completed async copies)
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
 // 2-SM TMA tile load: data lands in THIS CTA's smem, the transaction bytes are
 // signalled on the pair leader's barrier (same offset; peer bit cleared)
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint64_t* bar,

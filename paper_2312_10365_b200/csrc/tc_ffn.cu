@@ -980,6 +980,226 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
 }
 
+// =========================================== CTA-pair gather GEMMs (FWD1 / DA)
+// A pair tile (256 bucket rows of one block, the tile list of the 1-CTA
+// kernel) runs on a 2-CTA cluster with M = 256 cta_group::2 MMAs: CTA r
+// gathers rows [128r, 128r+128) and holds the N-half r of B (FWD1 SwiGLU: the
+// gate rows in CTA 0, the up rows in CTA 1), and its TMEM receives its 128
+// rows x N.  Two accumulators fit (N <= 256), so the epilogue of tile i
+// overlaps the MMAs of tile i+1 -- the 1-CTA kernel needs all 512 columns for
+// its 256-row tile and cannot overlap.  A stage is 32 KB per CTA (6 stages).
+// Producers fill their own CTA's stage and arrive on their own `full`
+// barrier; the peer's warp 1 relays its completed stage to the leader
+// (proxy fence + remote arrive), whose `full` counts that relay.  `empty` /
+// `tfull` are multicast by tcgen05.commit; `tempty` (leader) counts both
+// CTAs' epilogue warps.
+constexpr int kPairRows = 64;  // rows per CTA-stage gathered by TMA gather4 (rest: cp.async)
+constexpr int kPairStage = 32768;
+
+template <int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_pair_gather_kernel(const __grid_constant__ TcArgs a, int n_stages) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + n_stages * kPairStage);
+  uint64_t* empty = full + n_stages;
+  uint64_t* tfull = empty + n_stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  float* dg_xchg = (float*)(tmem_slot + 4);  // [128] DA half-row exchange
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nh = a.BN / 2;  // B rows (N columns) held by this CTA
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(&full[s], kTmaGatherWarps + kCpThreadsA + (leader ? 1 : 0));
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&a.ta);
+    tma_prefetch_desc(&a.tb);
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ntiles = a.unit_offsets[a.G + 1];
+  unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  const long long t_start = clock64();
+
+  // this CTA's 128-row half of pair tile `tile`
+  auto my_half = [&](int tile) {
+    TileInfo ti = decode<KIND>(a, tile);
+    ti.n_valid -= (int)rank * 128;
+    ti.prow0 += rank * 128;
+    ti.pos0 += rank * 128;
+    ti.rows_pad -= (int)rank * 128;
+    return ti;
+  };
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    // --------- TMA gather4 of rows [0, kPairRows); warp 0 lane 0 also loads B
+    const int p = warp == 0 ? 0 : warp - 1;
+    const int c = lane * kTmaGatherWarps + p;
+    constexpr int n_calls = kPairRows / 4;
+    const bool has_call = c < n_calls;
+    const int my_calls = n_calls > p ? (n_calls - p + kTmaGatherWarps - 1) / kTmaGatherWarps : 0;
+    const uint32_t tx = (uint32_t)my_calls * 512u + (p == 0 ? (uint32_t)nh * 128u : 0u);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = cid; tile < ntiles; tile += ncl) {
+      const TileInfo ti = my_half(tile);
+      int rr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * c + i;
+        rr[i] = (has_call && r < ti.n_valid) ? a.r.bucket_token[ti.pos0 + r] : (int)a.T;
+      }
+      if (KIND == K_DA) {  // warm L2 with this half's Z stash rows (read by the epilogue)
+        const int zrow = a.mp * a.bw * 2;
+        for (int r = lane * kTmaGatherWarps + p; r < 128 && r < ti.rows_pad; r += 32 * kTmaGatherWarps)
+          prefetch_l2_bulk((const uint8_t*)a.aux + (ti.prow0 + r) * zrow, zrow);
+      }
+      const int brow = (KIND == K_FWD1 && a.mp == 2) ? (int)rank * a.D + ti.b * a.bw
+                                                     : ti.b * a.bw + (int)rank * nh;
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        if (lane == 0) {
+          twait(&empty[stage], phase ^ 1, (tr && warp == 0) ? tr : nullptr, 4);
+          mbar_arrive_expect_tx(&full[stage], tx);
+        }
+        __syncwarp();
+        uint8_t* sA = smem + stage * kPairStage;
+        if (p == 0 && lane == 0) tma_load_2d(sA + kABytes, &a.tb, &full[stage], kb * 64, brow);
+        if (has_call) tma_gather4(sA + c * 512, &a.ta, &full[stage], kb * 64, rr[0], rr[1], rr[2], rr[3]);
+        if (++stage == n_stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= 12) {
+    // ------------------------------- cp.async of rows [kPairRows, 128)
+    const int t = threadIdx.x - 12 * 32;  // 0..127
+    const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
+    const int ch = t & 7;
+    constexpr int kRowsPer = (128 - kPairRows) * 8 / kCpThreadsA;  // 4
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = cid; tile < ntiles; tile += ncl) {
+      const TileInfo ti = my_half(tile);
+      int tok[kRowsPer];
+#pragma unroll
+      for (int i = 0; i < kRowsPer; ++i) {
+        const int r = kPairRows + (t >> 3) + 16 * i;
+        tok[i] = r < ti.n_valid ? a.r.bucket_token[ti.pos0 + r] : -1;
+      }
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
+        __syncwarp();
+        const uint32_t sA = smem_u32(smem + stage * kPairStage);
+#pragma unroll
+        for (int i = 0; i < kRowsPer; ++i) {
+          const int r = kPairRows + (t >> 3) + 16 * i;
+          const uint32_t dst = sA + r * 128 + ((ch ^ (r & 7)) << 4);
+          const __nv_bfloat16* g = src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kb * 64 + ch * 8;
+          cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
+        }
+        cp_async_arrive_noinc(&full[stage]);
+        if (++stage == n_stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ------------------------------------------- MMA issuer (leader)
+      const uint32_t idesc = idesc_bf16(256, a.BN, false, false);
+      const uint64_t adesc0 = sdesc_sw128(smem_u32(smem), 16, 1024);
+      const uint64_t bdesc0 = sdesc_sw128(smem_u32(smem) + kABytes, 16, 1024);
+      unsigned long long* trl = lane == 0 ? tr : nullptr;
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int tile = cid; tile < ntiles; tile += ncl) {
+        const TileInfo ti = decode<KIND>(a, tile);
+        twait(&tempty[acc], aphase ^ 1, trl, 1);
+        tc_fence_after();
+        if (trl) trl[7] += 1;
+        const uint32_t dtm = tmem + acc * 256;
+        for (int kb = 0; kb < ti.nkb; ++kb) {
+          twait(&full[stage], phase, trl, 0);
+          fence_proxy_async_smem();  // this CTA's cp.async rows -> async proxy
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t soff = (uint64_t)((stage * kPairStage) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_pair(dtm, adesc0 + soff + k * 2, bdesc0 + soff + k * 2, idesc,
+                            (kb != 0 || k != 0) ? 1u : 0u);
+            mma_commit_pair(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == n_stages) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) mma_commit_pair(&tfull[acc]);
+        __syncwarp();
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    } else if (lane == 0) {
+      // ------------- relay (peer): this CTA's stage complete -> leader
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < ntiles; tile += ncl) {
+        const TileInfo ti = decode<KIND>(a, tile);
+        for (int kb = 0; kb < ti.nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_proxy_async_smem();  // cp.async rows -> async proxy before the leader's MMAs
+          if (a.ablate == 9) mbar_arrive_remote(&full[stage], 0);
+          else mbar_arrive_remote_relaxed(&full[stage], 0);
+          if (++stage == n_stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 4 + kEpiWarps) {
+    // ------------------------------------------- epilogue (both CTAs)
+    const int e = warp - 4;
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int half = e >> 2;  // column (unit) half of the tile
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = cid; tile < ntiles; tile += ncl) {
+      const TileInfo ti = my_half(tile);
+      twait(&tfull[acc], aphase, (tr && threadIdx.x == 4 * 32) ? tr : nullptr, 2);
+      tc_fence_after();
+      const long long te0 = clock64();
+      if (ti.rows_pad > 0)  // the pair's second m-tile may not exist: write nothing
+        epilogue<KIND>(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, row, half, dg_xchg);
+      tc_fence_before();
+      __syncwarp();
+      if (tr && threadIdx.x == 4 * 32) tr[3] += (unsigned long long)(clock64() - te0);
+      if (lane == 0) {
+        if (leader) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_remote(&tempty[acc], 0);
+      }
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[6] = (unsigned long long)(clock64() - t_start);
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem);
+  }
+}
+
 // ============================================= CTA-pair weight-resident GEMMs
 // FWD2 / DX on CTA pairs (cta_group::2): a unit (block b, 256 output columns,
 // its m-tiles) runs on a 2-CTA cluster; CTA r computes m-tiles 2p + r, keeps
@@ -1297,6 +1517,64 @@ static cudaError_t launch_pair(TcArgs& a, int units_upper, cudaStream_t s) {
   return e;
 }
 
+// SPT_FFN_PAIR_GATHER=0 selects the 1-CTA kernel for FWD1 / DA
+static bool use_pair_gather() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_PAIR_GATHER");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+// pair gather kernel shapes: N = BN split in halves of BN/2 B rows per CTA
+static bool pair_gather_ok(int BN) { return BN <= 256 && BN % 32 == 0; }
+
+template <int KIND>
+static cudaError_t launch_pair_gather(TcArgs& a, int tiles_upper, cudaStream_t s) {
+  const int stages = std::min(7, (227 * 1024 - 2048) / kPairStage);
+  const int smem = stages * kPairStage + 2048;
+  static bool attr_set = false;
+  static int max_clusters = 0;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(tc_pair_gather_kernel<KIND>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(num_sms());
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 2;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, tc_pair_gather_kernel<KIND>, &cfg) !=
+            cudaSuccess ||
+        max_clusters <= 0) {
+      cudaGetLastError();
+      max_clusters = num_sms() / 2;
+    }
+    attr_set = true;
+  }
+  const int clusters = std::max(1, std::min(tiles_upper, max_clusters));
+  const bool trace_on = trace_begin(a, s);
+  const char* name = KIND == K_FWD1 ? "tc_fwd1_gate_up" : "tc_bwd_dA";
+  prof_begin(name, s);
+  tc_pair_gather_kernel<KIND><<<2 * clusters, kThreads, smem, s>>>(a, stages);
+  prof_end(s);
+  if (trace_on) trace_report(a, name, 2 * clusters, s);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (debug_sync()) {
+    e = cudaStreamSynchronize(s);
+    fprintf(stderr, "[spt] tc pair-gather kind %d clusters %d stages %d smem %d BN %d: %s\n", KIND,
+            clusters, stages, smem, a.BN, cudaGetErrorString(e));
+  }
+  return e;
+}
+
 template <int KIND>
 static cudaError_t launch_bres(TcArgs& a, int units_upper, cudaStream_t s) {
   const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
@@ -1469,7 +1747,14 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
     a.out = b.z;
     a.out2 = b.h;
     a.unit_offsets = b.unit_offsets;
-    TRY(launch<K_FWD1>(a, up / 2 + g.G, s));
+    if (use_pair_gather() && pair_gather_ok(a.BN)) {
+      // CTA r holds B rows of its N half: the gate (r = 0) / up (r = 1) rows
+      // for SwiGLU (a box of bw rows), else rows [r BN/2, (r+1) BN/2) of the block
+      if (g.mp != 2) ok = ok && make_tmap_bf16_2d(&a.tb, w1, g.D, g.d, g.d, 64, a.BN / 2);
+      TRY(launch_pair_gather<K_FWD1>(a, up / 2 + g.G, s));
+    } else {
+      TRY(launch<K_FWD1>(a, up / 2 + g.G, s));
+    }
   }
   {
     TcArgs a{};
@@ -1640,7 +1925,12 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.MH = 2;
     a.aux2 = dy;
     a.unit_offsets = b.unit_offsets;
-    TRY(launch<K_DA>(a, up / 2 + g.G, s));
+    if (use_pair_gather() && pair_gather_ok(a.BN)) {
+      ok = ok && make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, a.BN / 2);
+      TRY(launch_pair_gather<K_DA>(a, up / 2 + g.G, s));
+    } else {
+      TRY(launch<K_DA>(a, up / 2 + g.G, s));
+    }
   }
   {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features in <= 2 halves)
     TcArgs a{};
