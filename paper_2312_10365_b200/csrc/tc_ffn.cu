@@ -1185,7 +1185,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (tr && threadIdx.x == 4 * 32) tr[3] += (unsigned long long)(clock64() - te0);
       if (lane == 0) {
         if (leader) mbar_arrive(&tempty[acc]);
-        else mbar_arrive_remote(&tempty[acc], 0);
+        else mbar_arrive_remote_relaxed(&tempty[acc], 0);  // its TMEM loads completed (wait::ld)
       }
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
@@ -1343,7 +1343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (tr && threadIdx.x == 4 * 32) tr[3] += (unsigned long long)(clock64() - te0);
         if (lane == 0) {
           if (leader) mbar_arrive(&tempty[acc]);
-          else mbar_arrive_remote(&tempty[acc], 0);
+          else mbar_arrive_remote_relaxed(&tempty[acc], 0);  // its TMEM loads completed (wait::ld)
         }
         if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
@@ -1454,18 +1454,18 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   return e;
 }
 
-// SPT_FFN_PAIR=1 selects the CTA-pair weight-resident kernel for FWD2 / DX
-// (correct, measured slower on B200 in r01: these GEMMs are bound by the
-// partial-output writes, and the pair couples two CTAs' epilogues)
-static bool use_pair() {
-  static int v = -1;
-  if (v < 0) {
+// CTA-pair weight-resident kernel: default for DX (K = m'bw = 256: the
+// 1-CTA slab leaves a 4-stage A ring, measured 1.45 vs 1.79 ms), not for FWD2
+// (K = bw = 128: bound by the partial-output writes, where the pair's coupled
+// epilogues lose, 1.54 vs 1.31 ms).  SPT_FFN_PAIR=0: neither, =1: both.
+static bool use_pair(int kind) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("SPT_FFN_PAIR");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = e ? (e[0] == '1' ? 1 : 0) : -1;
   }
-  return v == 1;
+  return v == 1 || (v == -1 && kind == K_DX);
 }
-
 template <int KIND>
 static cudaError_t launch_pair(TcArgs& a, int units_upper, cudaStream_t s) {
   const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
@@ -1579,7 +1579,7 @@ template <int KIND>
 static cudaError_t launch_bres(TcArgs& a, int units_upper, cudaStream_t s) {
   const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
   const bool fits = 227 * 1024 - 1280 - kbu * 16384 - (kEpiWarps * 4096 + 1024) >= 3 * kABytes;
-  if (fits && use_pair()) return launch_pair<KIND>(a, units_upper, s);
+  if (fits && use_pair(KIND)) return launch_pair<KIND>(a, units_upper, s);
   return launch<KIND>(a, units_upper, s);
 }
 
@@ -1673,7 +1673,7 @@ cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logi
 //  tile_list[P(mt) + rank_b(mt)] = mt << 8 | b, i.e. bucket tiles in (m-tile,
 //  block) order with P(mt) = sum_b min(nt_b, mt) and rank_b(mt) = #{b' < b :
 //  nt_b' > mt};  unit_offsets = prefix over blocks of ceil(nt_b/16) * NT.
-__global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, int unit_mt,
+__global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, int unit_mt, int raster,
                                                          const int32_t* __restrict__ tile_offsets,
                                                          int32_t* __restrict__ tile_list,
                                                          int32_t* __restrict__ unit_offsets,
@@ -1690,7 +1690,7 @@ __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, int unit
   // the in-flight m-levels gather both stay in L2.
   const int b = blockIdx.x;
   for (int t = tile_offsets[b] + threadIdx.x; t < tile_offsets[b + 1]; t += blockDim.x) tile_block[t] = b;
-  const int g0 = (b / kRasterBlocks) * kRasterBlocks, g1 = min(G, g0 + kRasterBlocks);
+  const int g0 = (b / raster) * raster, g1 = min(G, g0 + raster);
   int base = 0;
   for (int bb = 0; bb < g0; ++bb) base += ntb[bb];
   for (int mt = threadIdx.x; mt < ntb[b]; mt += blockDim.x) {
@@ -1714,9 +1714,21 @@ __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, int unit
   }
 }
 
+// blocks per L2 raster group of the gathered-A GEMMs (SPT_FFN_RASTER, default kRasterBlocks)
+static int raster_blocks() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("SPT_FFN_RASTER");
+    v = e ? atoi(e) : kRasterBlocks;
+    if (v < 1) v = kRasterBlocks;
+  }
+  return v;
+}
+
 static cudaError_t build_schedules(const Geom& g, const RouteView& r, const Bufs& b, cudaStream_t s) {
   prof_begin("tile_sched", s);
-  tile_sched_kernel<<<g.G, 256, 0, s>>>(g.G, (int)ceil_div(g.d, 256), unit_mtiles(), r.tile_offsets,
+  tile_sched_kernel<<<g.G, 256, 0, s>>>(g.G, (int)ceil_div(g.d, 256), unit_mtiles(),
+                                        raster_blocks(), r.tile_offsets,
                                         b.tile_list,
                                         b.unit_offsets, b.tile_block);
   prof_end(s);

@@ -2,7 +2,7 @@
 knobs read once per process, so each case runs in its own interpreter):
   SPT_FFN_DAT=1       a7 with tokens on N + da_post_kernel
   SPT_FFN_PREFETCH=1  L2 prefetch of gathered rows
-  SPT_FFN_PAIR=1      CTA-pair (cta_group::2) weight-resident FWD2 / dX kernel
+  SPT_FFN_PAIR=1|0    CTA-pair (cta_group::2) weight-resident kernel for FWD2 + dX / neither (default: dX only)
   SPT_FFN_PAIR_GATHER=0  1-CTA FWD1 / dA kernel (default: CTA-pair gather kernel)
 """
 import os
@@ -32,7 +32,7 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"},
+@pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"}, {"SPT_FFN_PAIR": "0"},
                                  {"SPT_FFN_PAIR_GATHER": "0"}])
 def test_variant_parity(env):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
