@@ -190,6 +190,49 @@ def workload_config(cfg, world, T):
                 (cfg.mprime + 1) * cfg.D * cfg.d * (2 if cfg.dtype == 'bf16' else 4) / 1e6)}
 
 
+# ------------------------------------------------------- dense context
+def dense_context(cfg, x, w1, w2, dy, ms_routed, iters=5, warmup=2):
+    """the dense FFN fwd+bwd at the same shape through cuBLAS
+    (torch.matmul, bf16 in / fp32 accumulate) + torch elementwise activation --
+    the B200 analogue of the paper's dense-vs-SPT comparison (ideal speedup
+    G/k).  Context only: not this library's path."""
+    import torch
+    import torch.nn.functional as F
+    D = cfg.D
+    w1 = w1.reshape(-1, cfg.d)  # [m'D, d] (SwiGLU: gate rows then up rows)
+
+    def act(z):
+        if cfg.act == S.ACT_SWIGLU:
+            return F.silu(z[:, :D]) * z[:, D:]
+        return F.relu(z) if cfg.act == S.ACT_RELU else F.gelu(z)
+
+    def step():
+        z = x @ w1.t()                      # [T, m'D]
+        zr = z.detach().requires_grad_(True)
+        h = act(zr)
+        _ = h @ w2                          # Y [T, d]
+        dh = dy @ w2.t()                    # [T, D]
+        _ = h.t() @ dy                      # dW2 [D, d]
+        (dz,) = torch.autograd.grad(h, zr, dh)
+        _ = dz @ w1                         # dX [T, d]
+        _ = dz.t() @ x                      # dW1 [m'D, d]
+
+    for _ in range(warmup):
+        step()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    flops = 6.0 * x.shape[0] * cfg.d * D * (cfg.mprime + 1)
+    return {"ms_per_step": ms, "gemm_tflops": flops / (ms / 1e3) / 1e12,
+            "routed_speedup": ms / ms_routed, "ideal_speedup": cfg.G / cfg.k,
+            "what": "dense FFN fwd+bwd (torch.matmul / cuBLAS bf16 + torch activation), same T, d, D"}
+
+
 # ------------------------------------------------------------------- ours
 def main():
     ap = argparse.ArgumentParser()
@@ -202,6 +245,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense cuBLAS context")
     args = ap.parse_args()
     cfg = S.CONFIGS[args.config]
     if args.tokens:
@@ -372,6 +416,11 @@ def main():
                                           "peak_src": pk["src"] + " bf16 sustained"},
         "roofline": roofline, "kernels": kernels, "gpu_launches": launches, "clocks": clocks, "e2e": e2e,
     }
+    if world == 1 and not args.no_dense and cfg.dtype == "bf16":
+        try:
+            out["dense_context"] = dense_context(cfg, x, w1, w2, dy, ms_max)
+        except Exception as ex:  # e.g. out of memory: context only
+            out["dense_context"] = {"error": str(ex)[:200]}
     if world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline(cfg)

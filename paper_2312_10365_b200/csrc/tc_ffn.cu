@@ -1526,8 +1526,12 @@ static bool use_pair_gather() {
   }
   return v == 1;
 }
-// pair gather kernel shapes: N = BN split in halves of BN/2 B rows per CTA
-static bool pair_gather_ok(int BN) { return BN <= 256 && BN % 32 == 0; }
+// pair gather kernel: N = BN split in halves of BN/2 B rows per CTA.  Used
+// for N > 128 only: at N = 128 one M = 256 x N = 128 accumulator chain per CTA
+// runs the tensor pipe at ~43 % and the 1-CTA kernel (two M halves in flight)
+// wins (same-box A/B, LLaMA-scale dA: 1.18 vs 1.33 ms; OPT FWD1 114 vs 132 us),
+// while at N = 256 the pair wins (LLaMA FWD1 1.31 vs 1.50 ms).
+static bool pair_gather_ok(int BN) { return BN > 128 && BN <= 256 && BN % 32 == 0; }
 
 template <int KIND>
 static cudaError_t launch_pair_gather(TcArgs& a, int tiles_upper, cudaStream_t s) {

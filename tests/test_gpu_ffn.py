@@ -81,6 +81,14 @@ def test_k_equals_G_is_dense(orc):
     _parity(orc, cfg, 300)
 
 
+@pytest.mark.parametrize("name,d,D,G,k,act", [("bw256", 512, 2048, 8, 2, S.ACT_GELU),
+                                               ("bw192", 256, 1536, 8, 3, S.ACT_RELU)])
+def test_wide_blocks(orc, name, d, D, G, k, act):
+    """128 < m'*bw <= 256 with m' = 1: FWD1 and dA both take the CTA-pair gather
+    kernel (N > 128), B split into halves of bw/2 rows per CTA."""
+    _parity(orc, S.FfnConfig(name, d, D, G, k, 700, "bf16", act), 700)
+
+
 def test_k1_bf16(orc):
     cfg = S.FfnConfig("k1", 256, 2048, 16, 1, 400, "bf16", S.ACT_GELU)
     _parity(orc, cfg, 400)
