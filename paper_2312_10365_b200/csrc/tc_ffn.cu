@@ -104,8 +104,13 @@ __host__ __device__ constexpr bool kind_b_mn(int k) {
 // FWD2 / DX keep one (block, 256-column) weight slab resident in smem and
 // stream up to unit_mtiles() A tiles of that block through it
 __host__ __device__ constexpr bool kind_bres(int k) { return k == K_FWD2 || k == K_DX; }
+// K rows per smem stage (64 for every kind).  32-row stages for the dW kinds
+// (twice the ring depth for their latency-bound gathers) are supported and
+// parity-clean but measured slower on B200 (dW1 1.83 vs 1.45 ms, dW2 1.71 vs
+// 1.05 ms): the per-stage protocol (193 arrivals, commit, wake) doubles.
+__host__ __device__ constexpr int kind_bk(int) { return 64; }
 __host__ __device__ constexpr int b_bytes(int kind, int BN) {
-  return kind_bres(kind) ? 0 : (kind_b_mn(kind) ? 32768 : BN * 128);
+  return kind_bres(kind) ? 0 : (kind_b_mn(kind) ? 512 * kind_bk(kind) : BN * 128);
 }
 
 __device__ __forceinline__ int find_block(const int32_t* tile_offsets, int G, int t128) {
@@ -172,7 +177,8 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
     ti.pos0 = a.r.block_offsets[ti.b];
     ti.n_valid = a.r.block_offsets[ti.b + 1] - a.r.block_offsets[ti.b];  // bucket size n_b
     ti.kbase = (int64_t)a.r.tile_offsets[ti.b] * 128;
-    ti.nkb = 2 * (a.r.tile_offsets[ti.b + 1] - a.r.tile_offsets[ti.b]);
+    // rows past n_b up to the stage boundary are the block's zero padding
+    ti.nkb = (ti.n_valid + kind_bk(KIND) - 1) / kind_bk(KIND);
   } else {  // DWR: tile = (split, nt)
     ti.nt = tile % a.NT;
     const int s = tile / a.NT;
@@ -220,7 +226,7 @@ __device__ __forceinline__ uint32_t tile_tx_bytes(const TcArgs& a) {
   if (KIND == K_DA) return a.bw * 128;
   if (KIND == K_DAT) return 128 * 128;  // the W2 box is always 128 unit rows (rows >= bw unused)
   if (KIND == K_ROUTER) return kABytes + a.gpad * 128;
-  if (KIND == K_DW1 || KIND == K_DW2) return kABytes * a.MH;
+  if (KIND == K_DW1 || KIND == K_DW2) return 128 * kind_bk(KIND) * 2 * a.MH;
   return kABytes + 32768;  // FWD2, DX, DWR
 }
 
@@ -245,8 +251,9 @@ __device__ __forceinline__ void produce_tiles(const TcArgs& a, const TileInfo& t
 #pragma unroll
     for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, krow);
   } else if (KIND == K_DW1 || KIND == K_DW2) {
-    for (int j = 0; j < 2 * a.MH; ++j)  // MN-major A: 64-feature chunks x 64 bucket rows
-      tma_load_2d(sA + j * 8192, &a.ta, bar, j * 64, (int)(ti.kbase + kb * 64));
+    constexpr int BK = kind_bk(KIND);  // MN-major A: 64-feature chunks x BK bucket rows
+    for (int j = 0; j < 2 * a.MH; ++j)
+      tma_load_2d(sA + j * (BK * 128), &a.ta, bar, j * 64, (int)(ti.kbase + kb * BK));
   } else {  // DWR
     const int nk = ti.nkb / 2;
     const int part = kb >= nk;
@@ -559,15 +566,16 @@ __device__ __forceinline__ void epilogue_dat(const TcArgs& a, const TileInfo& ti
 // One K stage (4 x K=16) of MMAs into MH accumulator halves: descriptors are
 // advanced by constant adds (start address field, 16-byte units; no carry:
 // smem offsets < 256 KB), the A half h lives 16 KB after half 0.
-template <int MH>
+template <int MH, int NK = 4>
 __device__ __forceinline__ void issue_kstage(uint32_t dtm, uint32_t hstride, uint64_t ad,
                                              uint64_t bd, uint32_t a_kstep, uint32_t b_kstep,
-                                             uint32_t idesc, bool accumulate) {
+                                             uint32_t idesc, bool accumulate,
+                                             uint32_t a_hoff = 16384 >> 4) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < NK; ++k)
 #pragma unroll
     for (int h = 0; h < MH; ++h)
-      mma_bf16(dtm + h * hstride, ad + h * (16384 >> 4) + k * a_kstep, bd + k * b_kstep, idesc,
+      mma_bf16(dtm + h * hstride, ad + h * a_hoff + k * a_kstep, bd + k * b_kstep, idesc,
                (accumulate || k != 0) ? 1u : 0u);
 }
 
@@ -593,7 +601,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr bool kAmn = kind_a_mn(KIND);
   constexpr bool kBmn = kind_b_mn(KIND);
-  const int astride = kABytes * a.MH;
+  constexpr int BK = kind_bk(KIND);  // K rows per stage
+  const int astride = kABytes * BK / 64 * a.MH;
   const int bstride = (b_bytes(KIND, a.BN) + 1023) & ~1023;
   const int sstride = astride + bstride;
   // barrier area after the stage ring (weight-resident kinds: after slab + ring)
@@ -836,10 +845,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     }
   } else if (kind_gather_b(KIND) && (warp == 2 || warp == 3 || warp >= 12)) {
     // -------------------------- DW*: cp.async row gathers of B (6 warps)
-    // B: 64 bucket rows (K) x 256 columns (N) per stage, MN-major: 64-column
-    // chunk j at +8 KB*j, K row r at +128 B*r, 16-byte piece p swizzled by r.
-    // This thread: piece (gt & 31) of rows r_i = (gt >> 5) + 6 i.  Its
+    // B: BK bucket rows (K) x 256 columns (N) per stage, MN-major: 64-column
+    // chunk j at +BK*128 B*j, K row r at +128 B*r, 16-byte piece p swizzled
+    // by r.  This thread: piece (gt & 31) of rows r_i = (gt >> 5) + 6 i.  Its
     // arrival on the stage barrier fires when its copies have landed.
+    constexpr int kRowsG = (BK + 5) / 6;  // rows per thread (upper bound)
     const int gt = (warp < 4 ? warp - 2 : warp - 10) * 32 + lane;  // 0..191
     const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
     const int j = (gt & 31) >> 3, pc = gt & 7;
@@ -847,13 +857,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo ti = decode<KIND>(a, tile);
-      int tok[11];
+      int tok[kRowsG];
       auto load_idx = [&](int kb) {
 #pragma unroll
-        for (int i = 0; i < 11; ++i) {
+        for (int i = 0; i < kRowsG; ++i) {
           const int r = (gt >> 5) + 6 * i;
-          const int e = kb * 64 + r;
-          tok[i] = (r < 64 && e < ti.n_valid) ? a.r.bucket_token[ti.pos0 + e] : -1;
+          const int e = kb * BK + r;
+          tok[i] = (r < BK && e < ti.n_valid) ? a.r.bucket_token[ti.pos0 + e] : -1;
         }
       };
       if (ti.nkb > 0) load_idx(0);
@@ -861,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       auto prefetch_rows = [&]() {
         if (a.prefetch && (gt & 31) == 0) {
 #pragma unroll
-          for (int i = 0; i < 11; ++i)
+          for (int i = 0; i < kRowsG; ++i)
             if (tok[i] >= 0) prefetch_l2_bulk(src + (int64_t)tok[i] * a.d + ti.nt * 256, 512);
         }
       };
@@ -871,10 +881,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         __syncwarp();
         const uint32_t sB = smem_u32(smem + stage * sstride + astride);
 #pragma unroll
-        for (int i = 0; i < 11; ++i) {
+        for (int i = 0; i < kRowsG; ++i) {
           const int r = (gt >> 5) + 6 * i;
-          if (r < 64) {
-            const uint32_t dst = sB + j * 8192 + r * 128 + ((pc ^ (r & 7)) << 4);
+          if (r < BK) {
+            const uint32_t dst = sB + j * (BK * 128) + r * 128 + ((pc ^ (r & 7)) << 4);
             const __nv_bfloat16* g =
                 src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + ti.nt * 256 + j * 64 + pc * 8;
             cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
@@ -898,9 +908,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     const uint32_t a_kstep = kAmn ? 2048 >> 4 : 32 >> 4;  // descriptor units (16 B)
     const uint32_t b_kstep = kBmn ? 2048 >> 4 : 32 >> 4;
     const uint32_t hstride = (uint32_t)tm_half_stride(a.BN);
-    const uint64_t adesc0 = sdesc_sw128(smem_u32(smem), kAmn ? 8192 : 16, 1024);
-    const uint64_t bdesc0 = kBmn ? sdesc_sw128(smem_u32(smem) + astride, 8192, 1024)
+    // MN-major LBO = stride of the 64-element MN chunks = BK rows x 128 B
+    const uint64_t adesc0 = sdesc_sw128(smem_u32(smem), kAmn ? BK * 128 : 16, 1024);
+    const uint64_t bdesc0 = kBmn ? sdesc_sw128(smem_u32(smem) + astride, BK * 128, 1024)
                                  : sdesc_sw128(smem_u32(smem) + astride, 16, 1024);
+    const uint32_t a_hoff = (uint32_t)((astride / a.MH) >> 4);  // A half h at +astride/MH
     unsigned long long* trl = lane == 0 ? tr : nullptr;
     int stage = 0;
     uint32_t phase = 0;
@@ -922,9 +934,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const uint64_t soff = (uint64_t)((stage * sstride) >> 4);
         if (elect_one()) {
           if (a.MH == 2)
-            issue_kstage<2>(dtm, hstride, adesc0 + soff, bdesc0 + soff, a_kstep, b_kstep, idesc, kb != 0);
+            issue_kstage<2, BK / 16>(dtm, hstride, adesc0 + soff, bdesc0 + soff, a_kstep, b_kstep,
+                                     idesc, kb != 0, a_hoff);
           else
-            issue_kstage<1>(dtm, hstride, adesc0 + soff, bdesc0 + soff, a_kstep, b_kstep, idesc, kb != 0);
+            issue_kstage<1, BK / 16>(dtm, hstride, adesc0 + soff, bdesc0 + soff, a_kstep, b_kstep,
+                                     idesc, kb != 0, a_hoff);
           mma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -1416,7 +1430,7 @@ static void trace_report(TcArgs& a, const char* name, int grid, cudaStream_t s) 
 template <int KIND>
 static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   const int bst = (b_bytes(KIND, a.BN) + 1023) & ~1023;
-  const int sst = kABytes * a.MH + bst;
+  const int sst = kABytes * kind_bk(KIND) / 64 * a.MH + bst;
   const int extra = 1024 + 256 + 512;  // alignment slack + barriers + DA exchange
   // weight-resident kinds: the slab (K stages x 32 KB) is carved before the A ring
   const int slab = kind_bres(KIND)
@@ -1426,7 +1440,8 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   if (kind_bres(KIND)) a.n_stg = slab > 65536 ? 1 : 2;
   const int stg = kind_bres(KIND) ? kEpiWarps * a.n_stg * 4096 + 1024
                                   : (KIND == K_DAT ? kEpiWarps * 4096 + 1024 : 0);
-  int stages = std::min(kind_bres(KIND) ? 8 : 6, (227 * 1024 - extra - slab - stg) / sst);
+  int stages = std::min(kind_bres(KIND) || kind_bk(KIND) < 64 ? 8 : 6,
+                        (227 * 1024 - extra - slab - stg) / sst);
   const int smem = slab + stages * sst + extra + stg;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1952,7 +1967,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
-                                (uint64_t)g.mp * g.bw, 64, 64) &&
+                                (uint64_t)g.mp * g.bw, 64, kind_bk(K_DW1)) &&
               make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 1);
     a.BN = 256;
     a.MH = (int)ceil_div(g.mp * g.bw, 128);
@@ -1964,7 +1979,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   {  // a9: dW2_b = H~_b^T dY[bucket_b]
     TcArgs a{};
     base_args(a, g, r);
-    bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, 64) &&
+    bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, kind_bk(K_DW2)) &&
               make_tmap_bf16_2d(&a.tb, dy, g.T, g.d, g.d, 64, 1);
     a.BN = 256;
     a.MH = (int)ceil_div(g.bw, 128);
