@@ -240,14 +240,14 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="llama_scale", choices=sorted(S.CONFIGS))
+    ap.add_argument("--config", default="llama_scale", choices=sorted(S.ALL_CONFIGS))
     ap.add_argument("--tokens", type=int, default=0, help="override tokens per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense cuBLAS context")
     args = ap.parse_args()
-    cfg = S.CONFIGS[args.config]
+    cfg = S.ALL_CONFIGS[args.config]
     if args.tokens:
         cfg = cfg.with_(T=args.tokens)
     if args.impl == "reference":

@@ -69,6 +69,14 @@ struct TcArgs {
   int unit_mt;                  // FWD2/DX: m-tiles per weight-resident unit
   int prefetch;                 // gathering kinds: L2 prefetch of gathered rows (SPT_FFN_PREFETCH)
   unsigned long long* trace;    // SPT_FFN_TRACE: per-CTA role cycle counters (diagnostics)
+  // wide blocks (m' bw > 256, the paper's G = 4 / 8 blocks): FWD1 / DA tile
+  // the block's units (bn_u per tile, nu tiles), DW1 / DW2 tile the features
+  // (256 per tile, nu tiles), FWD2 / DX stream K instead of keeping the
+  // weight slab resident (kstream).  nu = 1, kstream = 0 otherwise.
+  int bn_u;                     // FWD1 / DA: units per tile (= bw when nu == 1)
+  int nu;                       // FWD1 / DA: unit tiles; DW1 / DW2: feature tiles
+  int kstream;                  // FWD2 / DX: K-streaming tiles (K > 256)
+  float* dgp;                   // DA, nu > 1: per-unit-tile dgate partials [rows_cap][nu]
   int ablate;                   // SPT_FFN_ABLATE (timing experiments only; results wrong):
                                 //  1 = skip gathered-row copies, 2 = skip FWD1 epilogue stores,
                                 //  3 = no operand loads at all, 4 = 3 + no epilogue work,
@@ -109,8 +117,8 @@ __host__ __device__ constexpr bool kind_bres(int k) { return k == K_FWD2 || k ==
 // parity-clean but measured slower on B200 (dW1 1.83 vs 1.45 ms, dW2 1.71 vs
 // 1.05 ms): the per-stage protocol (193 arrivals, commit, wake) doubles.
 __host__ __device__ constexpr int kind_bk(int) { return 64; }
-__host__ __device__ constexpr int b_bytes(int kind, int BN) {
-  return kind_bres(kind) ? 0 : (kind_b_mn(kind) ? 512 * kind_bk(kind) : BN * 128);
+__host__ __device__ constexpr int b_bytes(int kind, int BN, int kstream = 0) {
+  return kind_bres(kind) && !kstream ? 0 : (kind_b_mn(kind) ? 512 * kind_bk(kind) : BN * 128);
 }
 
 __device__ __forceinline__ int find_block(const int32_t* tile_offsets, int G, int t128) {
@@ -130,6 +138,7 @@ struct TileInfo {
   int nkb;          // K stages
   int64_t kbase;    // DW*: first padded row of the block; DWR: first token of the split
   int rows_pad;     // bucket-row kinds: padded rows of the block from prow0 on (write limit)
+  int ut;           // FWD1 / DA: unit tile; DW1 / DW2: feature tile (wide blocks)
 };
 
 // TMEM columns: accumulator buffer `acc`, M half `h` (each half holds BN <= 256
@@ -146,9 +155,10 @@ __host__ __device__ __forceinline__ uint32_t tm_col(int BN, int MH, int acc, int
 template <int KIND>
 __device__ __forceinline__ int num_tiles(const TcArgs& a) {
   if (KIND == K_ROUTER) return (int)ceil_div(a.T, 128);
-  if (kind_gather_a(KIND)) return a.unit_offsets[a.G + 1];  // 256-row pair tiles
-  if (KIND == K_FWD2 || KIND == K_DX) return a.unit_offsets[a.G];  // units
-  if (KIND == K_DW1 || KIND == K_DW2) return a.G * a.NT;
+  if (kind_gather_a(KIND)) return a.unit_offsets[a.G + 1] * a.nu;  // 256-row pair tiles x unit tiles
+  if (KIND == K_FWD2 || KIND == K_DX)  // weight-resident units, or (m-tile, N tile) when streaming K
+    return a.kstream ? a.r.tile_offsets[a.G] * a.NT : a.unit_offsets[a.G];
+  if (KIND == K_DW1 || KIND == K_DW2) return a.G * a.nu * a.NT;
   return a.NT * a.n_split;  // DWR (G <= 128 rows: one M tile)
 }
 
@@ -161,8 +171,9 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
     ti.nkb = a.d / 64;
   } else if (kind_gather_a(KIND)) {
     // pair tiles (two 128-row m-tiles sharing each B stage) in the raster order
-    // of tile_sched_kernel
-    const int e = a.tile_list[tile];
+    // of tile_sched_kernel; unit tiles fastest (their A rows are shared in L2)
+    ti.ut = tile % a.nu;
+    const int e = a.tile_list[tile / a.nu];
     ti.b = e & 255;
     const int mt = 2 * (e >> 8);
     const int nb = a.r.block_offsets[ti.b + 1] - a.r.block_offsets[ti.b];
@@ -171,9 +182,20 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
     ti.pos0 = a.r.block_offsets[ti.b] + mt * 128;
     ti.rows_pad = (a.r.tile_offsets[ti.b + 1] - a.r.tile_offsets[ti.b] - mt) * 128;
     ti.nkb = a.d / 64;
+  } else if (KIND == K_FWD2 || KIND == K_DX) {  // K-streaming: (global m-tile, N tile)
+    ti.nt = tile % a.NT;
+    const int mg = tile / a.NT;
+    ti.b = find_block(a.r.tile_offsets, a.G, mg);
+    const int mt = mg - a.r.tile_offsets[ti.b];
+    const int nb = a.r.block_offsets[ti.b + 1] - a.r.block_offsets[ti.b];
+    ti.n_valid = nb - mt * 128;
+    ti.prow0 = (int64_t)mg * 128;
+    ti.pos0 = a.r.block_offsets[ti.b] + mt * 128;
+    ti.nkb = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
   } else if (KIND == K_DW1 || KIND == K_DW2) {
     ti.nt = tile % a.NT;
-    ti.b = tile / a.NT;
+    ti.ut = (tile / a.NT) % a.nu;
+    ti.b = tile / a.NT / a.nu;
     ti.pos0 = a.r.block_offsets[ti.b];
     ti.n_valid = a.r.block_offsets[ti.b + 1] - a.r.block_offsets[ti.b];  // bucket size n_b
     ti.kbase = (int64_t)a.r.tile_offsets[ti.b] * 128;
@@ -222,8 +244,8 @@ __device__ __forceinline__ TileInfo decode_mtile(const TcArgs& a, const UnitInfo
 // bytes of the tile (non-gather) loads of one stage, issued by warp 0 lane 0
 template <int KIND>
 __device__ __forceinline__ uint32_t tile_tx_bytes(const TcArgs& a) {
-  if (KIND == K_FWD1) return a.mp * a.bw * 128;
-  if (KIND == K_DA) return a.bw * 128;
+  if (KIND == K_FWD1) return a.mp * a.bn_u * 128;
+  if (KIND == K_DA) return a.bn_u * 128;
   if (KIND == K_DAT) return 128 * 128;  // the W2 box is always 128 unit rows (rows >= bw unused)
   if (KIND == K_ROUTER) return kABytes + a.gpad * 128;
   if (KIND == K_DW1 || KIND == K_DW2) return 128 * kind_bk(KIND) * 2 * a.MH;
@@ -240,9 +262,10 @@ __device__ __forceinline__ void produce_tiles(const TcArgs& a, const TileInfo& t
     tma_load_2d(sB, &a.tb, bar, kb * 64, 0);
   } else if (KIND == K_DAT) {  // A = the block's W2 rows (units) x 64 columns
     tma_load_2d(sA, &a.tb, bar, kb * 64, ti.b * a.bw);
-  } else if (KIND == K_FWD1 || KIND == K_DA) {
-    tma_load_2d(sB, &a.tb, bar, kb * 64, ti.b * a.bw);
-    if (KIND == K_FWD1 && a.mp == 2) tma_load_2d(sB + a.bw * 128, &a.tb, bar, kb * 64, a.D + ti.b * a.bw);
+  } else if (KIND == K_FWD1 || KIND == K_DA) {  // B: the tile's bn_u units (+ up rows)
+    const int u0 = ti.b * a.bw + ti.ut * a.bn_u;
+    tma_load_2d(sB, &a.tb, bar, kb * 64, u0);
+    if (KIND == K_FWD1 && a.mp == 2) tma_load_2d(sB + a.bn_u * 128, &a.tb, bar, kb * 64, a.D + u0);
   } else if (KIND == K_FWD2 || KIND == K_DX) {
     tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
     int krow;
@@ -252,8 +275,8 @@ __device__ __forceinline__ void produce_tiles(const TcArgs& a, const TileInfo& t
     for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, krow);
   } else if (KIND == K_DW1 || KIND == K_DW2) {
     constexpr int BK = kind_bk(KIND);  // MN-major A: 64-feature chunks x BK bucket rows
-    for (int j = 0; j < 2 * a.MH; ++j)
-      tma_load_2d(sA + j * (BK * 128), &a.ta, bar, j * 64, (int)(ti.kbase + kb * BK));
+    for (int j = 0; j < 2 * a.MH; ++j)  // features [256 ut + 64 j, +64)
+      tma_load_2d(sA + j * (BK * 128), &a.ta, bar, ti.ut * 256 + j * 64, (int)(ti.kbase + kb * BK));
   } else {  // DWR
     const int nk = ti.nkb / 2;
     const int part = kb >= nk;
@@ -312,14 +335,17 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     // 16 units per step (register budget: the kernel runs 512 threads)
     const float g = valid ? a.r.bucket_gate[ti.pos0 + row] : 0.f;
     const int64_t prow = ti.prow0 + row;
-    __nv_bfloat16* zr = (__nv_bfloat16*)a.out + prow * (int64_t)(a.mp * a.bw);
-    __nv_bfloat16* hr = (__nv_bfloat16*)a.out2 + prow * (int64_t)a.bw;
-    const int hw = ((a.bw / 2) + 15) & ~15;
-    const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? a.bw : min(a.bw, u_lo + hw);
+    // this tile's units [ub, ub + nut) of the block: TMEM columns u (gate) and
+    // bn_u + u (up); Z stash row = [gate bw | up bw], H row = [bw]
+    const int ub = ti.ut * a.bn_u, nut = min(a.bn_u, a.bw - ub);
+    __nv_bfloat16* zr = (__nv_bfloat16*)a.out + prow * (int64_t)(a.mp * a.bw) + ub;
+    __nv_bfloat16* hr = (__nv_bfloat16*)a.out2 + prow * (int64_t)a.bw + ub;
+    const int hw = ((a.bn_u / 2) + 15) & ~15;
+    const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? nut : min(nut, u_lo + hw);
     for (int u0 = u_lo; u0 < u_hi; u0 += 16) {
       uint32_t vg[16], vu[16];
       tmem_ld16(tacc + u0, vg);
-      if (a.mp == 2) tmem_ld16(tacc + a.bw + u0, vu);
+      if (a.mp == 2) tmem_ld16(tacc + a.bn_u + u0, vu);
       tmem_ld_wait();
       uint32_t pz[8], pu[8], ph[8];
 #pragma unroll
@@ -363,10 +389,11 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
   } else if (KIND == K_DA) {
     const int64_t prow = ti.prow0 + row;
     const float g = valid ? a.r.bucket_gate[ti.pos0 + row] : 0.f;
-    const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + prow * (int64_t)(a.mp * a.bw);
-    __nv_bfloat16* dzr = (__nv_bfloat16*)a.out2 + prow * (int64_t)(a.mp * a.bw);
-    const int hw = ((a.bw / 2) + 15) & ~15;
-    const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? a.bw : min(a.bw, u_lo + hw);
+    const int ub = ti.ut * a.bn_u, nut = min(a.bn_u, a.bw - ub);  // this tile's units
+    const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + prow * (int64_t)(a.mp * a.bw) + ub;
+    __nv_bfloat16* dzr = (__nv_bfloat16*)a.out2 + prow * (int64_t)(a.mp * a.bw) + ub;
+    const int hw = ((a.bn_u / 2) + 15) & ~15;
+    const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? nut : min(nut, u_lo + hw);
     float dgate = 0.f;
     for (int u0 = u_lo; u0 < u_hi; u0 += 16) {  // 16 units per step (register budget)
       uint32_t v[16];
@@ -428,7 +455,11 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
       asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
       if (half == 0) dgate = dgate + dg_xchg[row];
     }
-    if (half <= 0) {
+    if (half <= 0 && a.nu > 1) {
+      // unit-tiled block: this tile's partial dgate; dgate_reduce_kernel sums
+      // the tiles and derives dlogit / the dense dlogits
+      a.dgp[prow * a.nu + ti.ut] = valid ? dgate : 0.f;
+    } else if (half <= 0) {
       // dlogit = dgate * g (1 - g) = dgate * sigma(z) sigma(-z): no cancellation in 1 - g
       float dlogit = 0.f;
       int64_t t = 0;
@@ -462,7 +493,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     } else {
       // MH == 2: this warp's half owns accumulator `half` (features half*128 + row);
       // MH == 1: one accumulator, columns split between the halves
-      const int f = (a.MH == 2 ? half * 128 : 0) + row;
+      const int f = ti.ut * 256 + (a.MH == 2 ? half * 128 : 0) + row;
       const int M = KIND == K_DW1 ? a.mp * a.bw : a.bw;
       live = f < M;
       if (KIND == K_DW1 && a.mp == 2)
@@ -603,10 +634,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   constexpr bool kBmn = kind_b_mn(KIND);
   constexpr int BK = kind_bk(KIND);  // K rows per stage
   const int astride = kABytes * BK / 64 * a.MH;
-  const int bstride = (b_bytes(KIND, a.BN) + 1023) & ~1023;
+  const int bstride = (b_bytes(KIND, a.BN, a.kstream) + 1023) & ~1023;
   const int sstride = astride + bstride;
+  const bool resident = kind_bres(KIND) && !a.kstream;  // weight-resident units
   // barrier area after the stage ring (weight-resident kinds: after slab + ring)
-  const int ring_bytes = kind_bres(KIND)
+  const int ring_bytes = resident
                              ? (KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64) * 32768 +
                                    n_stages * kABytes
                              : n_stages * sstride;
@@ -654,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   const long long t_start = clock64();
 
-  if (kind_bres(KIND)) {
+  if (resident) {
     // ============ weight-resident units (FWD2 / DX): B slab once per unit
     const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;  // K stages
     uint8_t* sBres = smem;                                   // kbu x 32 KB
@@ -1047,7 +1079,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int ntiles = a.unit_offsets[a.G + 1];
+  const int ntiles = a.unit_offsets[a.G + 1] * a.nu;  // pair tiles x unit tiles
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   const long long t_start = clock64();
 
@@ -1084,8 +1116,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int r = lane * kTmaGatherWarps + p; r < 128 && r < ti.rows_pad; r += 32 * kTmaGatherWarps)
           prefetch_l2_bulk((const uint8_t*)a.aux + (ti.prow0 + r) * zrow, zrow);
       }
-      const int brow = (KIND == K_FWD1 && a.mp == 2) ? (int)rank * a.D + ti.b * a.bw
-                                                     : ti.b * a.bw + (int)rank * nh;
+      const int u0 = ti.b * a.bw + ti.ut * a.bn_u;  // first unit of the tile
+      const int brow = (KIND == K_FWD1 && a.mp == 2) ? (int)rank * a.D + u0 : u0 + (int)rank * nh;
       for (int kb = 0; kb < ti.nkb; ++kb) {
         if (lane == 0) {
           twait(&empty[stage], phase ^ 1, (tr && warp == 0) ? tr : nullptr, 4);
@@ -1429,17 +1461,18 @@ static void trace_report(TcArgs& a, const char* name, int grid, cudaStream_t s) 
 
 template <int KIND>
 static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
-  const int bst = (b_bytes(KIND, a.BN) + 1023) & ~1023;
+  const int bst = (b_bytes(KIND, a.BN, a.kstream) + 1023) & ~1023;
   const int sst = kABytes * kind_bk(KIND) / 64 * a.MH + bst;
   const int extra = 1024 + 256 + 512;  // alignment slack + barriers + DA exchange
+  const bool resident = kind_bres(KIND) && !a.kstream;
   // weight-resident kinds: the slab (K stages x 32 KB) is carved before the A ring
-  const int slab = kind_bres(KIND)
+  const int slab = resident
                        ? (KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64) * 32768
                        : 0;
   // FWD2 keeps 2 staging buffers per epilogue warp, DX (128 KB slab) keeps 1
-  if (kind_bres(KIND)) a.n_stg = slab > 65536 ? 1 : 2;
-  const int stg = kind_bres(KIND) ? kEpiWarps * a.n_stg * 4096 + 1024
-                                  : (KIND == K_DAT ? kEpiWarps * 4096 + 1024 : 0);
+  if (resident) a.n_stg = slab > 65536 ? 1 : 2;
+  const int stg = resident ? kEpiWarps * a.n_stg * 4096 + 1024
+                           : (KIND == K_DAT ? kEpiWarps * 4096 + 1024 : 0);
   int stages = std::min(kind_bres(KIND) || kind_bk(KIND) < 64 ? 8 : 6,
                         (227 * 1024 - extra - slab - stg) / sst);
   const int smem = slab + stages * sst + extra + stg;
@@ -1615,6 +1648,9 @@ static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
   a.gpad = g.gpad;
   a.NT = (int)ceil_div(g.d, 256);
   a.MH = 1;
+  a.nu = 1;
+  a.bn_u = g.bw;
+  a.kstream = 0;
   a.unit_mt = unit_mtiles();
   static int pf = -1;  // SPT_FFN_PREFETCH=1 enables the L2 prefetch of gathered rows
   if (pf < 0) {
@@ -1658,7 +1694,8 @@ static bool use_fused_da() {
 
 bool tc_supported(const Geom& g) {
   if (g.d % 64) return false;
-  if (g.mp * g.bw > 256) return false;          // FWD1 N = m' * bw in one MMA; DW1 M <= 256
+  // m' bw > 256 (wide blocks): FWD1 / DA tile the units, DW* the features,
+  // FWD2 / DX stream K (no limit on bw beyond the ABI's bw % 16 == 0)
   if (g.mp == 2 && g.bw % 64) return false;     // DX K stages must not straddle gate/up
   if (g.gpad > 128) return false;               // DWR: one 128-row M tile of blocks
   return true;
@@ -1768,23 +1805,27 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
     TcArgs a{};
     base_args(a, g, r);
     a.tile_list = b.tile_list;
+    // wide blocks (m' bw > 256): tiles of 256 / m' units (N = 256)
+    a.bn_u = g.mp * g.bw > 256 ? 256 / g.mp : g.bw;
+    a.nu = (int)ceil_div(g.bw, a.bn_u);
     bool ok = make_tmap_bf16_2d(&a.ta, x, g.T, g.d, g.d, 64, 1) &&
-              make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, g.bw) &&
+              make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, a.bn_u) &&
               make_tmap_bf16_2d(&a.tc, x, g.T, g.d, g.d, 256, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                 CU_TENSOR_MAP_SWIZZLE_NONE);  // L2 prefetch rows
-    a.BN = g.mp * g.bw;
+    a.BN = g.mp * a.bn_u;
     a.MH = 2;
     a.aux2 = x;
     a.out = b.z;
     a.out2 = b.h;
     a.unit_offsets = b.unit_offsets;
+    const int tiles = (up / 2 + g.G) * a.nu;
     if (use_pair_gather() && pair_gather_ok(a.BN)) {
       // CTA r holds B rows of its N half: the gate (r = 0) / up (r = 1) rows
-      // for SwiGLU (a box of bw rows), else rows [r BN/2, (r+1) BN/2) of the block
+      // for SwiGLU (a box of bn_u rows), else rows [r BN/2, (r+1) BN/2) of the tile
       if (g.mp != 2) ok = ok && make_tmap_bf16_2d(&a.tb, w1, g.D, g.d, g.d, 64, a.BN / 2);
-      TRY(launch_pair_gather<K_FWD1>(a, up / 2 + g.G, s));
+      TRY(launch_pair_gather<K_FWD1>(a, tiles, s));
     } else {
-      TRY(launch<K_FWD1>(a, up / 2 + g.G, s));
+      TRY(launch<K_FWD1>(a, tiles, s));
     }
   }
   {
@@ -1796,7 +1837,12 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
     a.BN = 256;
     a.out = b.part;
     a.unit_offsets = b.unit_offsets;
-    TRY(launch_bres<K_FWD2>(a, units_upper(g), s));
+    a.kstream = g.bw > 256;  // the K = bw slab no longer fits smem: stream K
+    if (a.kstream) {
+      TRY(launch<K_FWD2>(a, up * a.NT, s));
+    } else {
+      TRY(launch_bres<K_FWD2>(a, units_upper(g), s));
+    }
   }
   return launch_combine_fwd(g, r, b.part, y, s);
 }
@@ -1911,6 +1957,37 @@ __global__ void dwr_reduce_kernel(int n_split, int64_t n, const float* __restric
   out[i] = s;
 }
 
+// Wide blocks (bw > 256): dA is unit-tiled, so each pair's dgate arrives as
+// nu partial sums (one per unit tile, dgp[prow][ut]).  One thread per (token,
+// selected block): dgate = sum of the partials, dlogit = dgate sigma(z)
+// sigma(-z) (SIGMOID), and the dense hi/lo bf16 dlogits of the dW_R GEMM --
+// what the fused dA epilogue writes inline when nu == 1.
+__global__ void __launch_bounds__(256) dgate_reduce_kernel(int64_t T, int G, int k, int nu, int gate,
+                                                           int gpad, RouteView r,
+                                                           const float* __restrict__ dgp,
+                                                           float* __restrict__ rows_f,
+                                                           float* __restrict__ rows_g,
+                                                           __nv_bfloat16* __restrict__ dlg) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= T * k) return;
+  const int64_t t = i / k;
+  const int b = r.topk_idx[i];
+  const int64_t pos = r.pair_slot[i];
+  const int64_t prow = (int64_t)r.tile_offsets[b] * 128 + (pos - r.block_offsets[b]);
+  float dgate = 0.f;
+  for (int u = 0; u < nu; ++u) dgate += dgp[prow * nu + u];
+  float dlogit = 0.f;
+  if (gate == SPT_GATE_SIGMOID) {
+    dlogit = dgate * sigmoid_pair(r.logits[t * G + b]);
+    const __nv_bfloat16 hi = __float2bfloat16(dlogit);
+    const __nv_bfloat16 lo = __float2bfloat16(dlogit - __bfloat162float(hi));
+    dlg[t * gpad + b] = hi;
+    dlg[(T + t) * gpad + b] = lo;
+  }
+  rows_f[prow] = dgate;
+  rows_g[prow] = dlogit;
+}
+
 cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void* w2,
                         const void* w_r, const RouteView& r, const void* dy, void* dx, float* dw1,
                         float* dw2, float* dw_r, float* dgate_out, bool accumulate, const Bufs& b,
@@ -1921,7 +1998,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   if (e0 != cudaSuccess) return e0;
   if (sig && cudaMemsetAsync(b.dlg, 0, (size_t)2 * g.T * g.gpad * 2, s) != cudaSuccess)
     return cudaErrorUnknown;
-  if (!use_fused_da()) {  // a7: dA^T = W2_b dY[bucket]^T (tokens on N), then the dgate/dZ pass
+  if (!use_fused_da() && g.bw <= 128) {  // a7: dA^T = W2_b dY[bucket]^T (tokens on N), then dgate/dZ
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, dy, g.T, g.d, g.d, 64, 1) &&
@@ -1942,11 +2019,16 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   } else {  // a7 fused variant: dA = dY[bucket] W2_b^T with the dgate / dZ / dlogit epilogue
     TcArgs a{};
     base_args(a, g, r);
+    // wide blocks (bw > 256): tiles of 256 units (N = 256: the CTA-pair
+    // kernel); dgate partials per tile
+    a.bn_u = g.bw > 256 ? 256 : g.bw;
+    a.nu = (int)ceil_div(g.bw, a.bn_u);
+    a.dgp = b.da;  // [rows_cap][nu] fits the [rows_cap][bw] f32 scratch
     bool ok = make_tmap_bf16_2d(&a.ta, dy, g.T, g.d, g.d, 64, 1) &&
-              make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, g.bw) &&
+              make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, a.bn_u) &&
               make_tmap_bf16_2d(&a.tc, dy, g.T, g.d, g.d, 256, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                 CU_TENSOR_MAP_SWIZZLE_NONE);  // L2 prefetch rows
-    a.BN = g.bw;
+    a.BN = a.bn_u;
     a.aux = b.z;
     a.out2 = b.dz;
     a.rows_f = b.dgate;
@@ -1956,25 +2038,37 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.MH = 2;
     a.aux2 = dy;
     a.unit_offsets = b.unit_offsets;
+    const int tiles = (up / 2 + g.G) * a.nu;
     if (use_pair_gather() && pair_gather_ok(a.BN)) {
       ok = ok && make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, a.BN / 2);
-      TRY(launch_pair_gather<K_DA>(a, up / 2 + g.G, s));
+      TRY(launch_pair_gather<K_DA>(a, tiles, s));
     } else {
-      TRY(launch<K_DA>(a, up / 2 + g.G, s));
+      TRY(launch<K_DA>(a, tiles, s));
+    }
+    if (a.nu > 1) {  // sum the unit tiles' dgate partials; dlogit, dense dlogits
+      const int64_t n = g.T * g.k;
+      prof_begin("dgate_reduce", s);
+      dgate_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(
+          g.T, g.G, g.k, a.nu, g.gate, g.gpad, r, b.da, b.dgate, b.dlogit, (__nv_bfloat16*)b.dlg);
+      prof_end(s);
+      count_launch();
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
     }
   }
-  {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features in <= 2 halves)
+  {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features: <= 2 halves, or 256-feature tiles)
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
                                 (uint64_t)g.mp * g.bw, 64, kind_bk(K_DW1)) &&
               make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 1);
     a.BN = 256;
-    a.MH = (int)ceil_div(g.mp * g.bw, 128);
+    a.MH = (int)std::min<int64_t>(2, ceil_div(g.mp * g.bw, 128));
+    a.nu = (int)ceil_div(g.mp * g.bw, 256);
     a.aux2 = x;
     a.out = dw1;
     a.acc_mode = accumulate;
-    TRY(launch<K_DW1>(a, g.G * a.NT, s));
+    TRY(launch<K_DW1>(a, g.G * a.nu * a.NT, s));
   }
   {  // a9: dW2_b = H~_b^T dY[bucket_b]
     TcArgs a{};
@@ -1982,11 +2076,12 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, kind_bk(K_DW2)) &&
               make_tmap_bf16_2d(&a.tb, dy, g.T, g.d, g.d, 64, 1);
     a.BN = 256;
-    a.MH = (int)ceil_div(g.bw, 128);
+    a.MH = (int)std::min<int64_t>(2, ceil_div(g.bw, 128));
+    a.nu = (int)ceil_div(g.bw, 256);
     a.aux2 = dy;
     a.out = dw2;
     a.acc_mode = accumulate;
-    TRY(launch<K_DW2>(a, g.G * a.NT, s));
+    TRY(launch<K_DW2>(a, g.G * a.nu * a.NT, s));
   }
   // a10: dW_R = dLogits^T X  (split-K, hi + lo bf16 halves of dlogit)
   if (sig) {
@@ -2023,7 +2118,12 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.BN = 256;
     a.out = b.part;
     a.unit_offsets = b.unit_offsets;
-    TRY(launch_bres<K_DX>(a, units_upper(g), s));
+    a.kstream = g.mp * g.bw > 256;  // the K = m' bw slab no longer fits smem: stream K
+    if (a.kstream) {
+      TRY(launch<K_DX>(a, up * a.NT, s));
+    } else {
+      TRY(launch_bres<K_DX>(a, units_upper(g), s));
+    }
   }
   e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
   if (e != cudaSuccess) return e;

@@ -77,6 +77,17 @@ CONFIGS = {
                              cfg_index=4),
 }
 
+# the paper's own FFN workload (Table 5, PAPER.md:1011-1048;
+# Table 3 shapes): OPT-2048 / LLaMA-4096 2-matrix FFNs, batch
+# 16 x 512 tokens, G = 8 blocks, beta = k/G = 1/2.  The
+# paper's LLaMA-family block uses GELU in its 2-matrix form.
+PAPER_CONFIGS = {
+    "opt2048_g8": FfnConfig("opt2048_g8", 2048, 8192, 8, 4, 16 * 512, "bf16", ACT_RELU, cfg_index=5),
+    "llama4096_g8": FfnConfig("llama4096_g8", 4096, 11008, 8, 4, 16 * 512, "bf16", ACT_GELU,
+                              cfg_index=6),
+}
+ALL_CONFIGS = {**CONFIGS, **PAPER_CONFIGS}
+
 _TENSOR_IDS = {"x": 1, "w1": 2, "w2": 3, "w_r": 4, "dy": 5, "logits": 6}
 
 

@@ -89,6 +89,19 @@ def test_wide_blocks(orc, name, d, D, G, k, act):
     _parity(orc, S.FfnConfig(name, d, D, G, k, 700, "bf16", act), 700)
 
 
+@pytest.mark.parametrize("name,d,D,G,k,act", [
+    ("wide1024", 256, 2048, 2, 1, S.ACT_GELU),      # bw 1024: 4 FWD1 / 8 dA unit tiles
+    ("wide512sw", 256, 1024, 2, 1, S.ACT_SWIGLU),   # bw 512 SwiGLU: m' bw = 1024
+    ("wide1376", 256, 2752, 2, 1, S.ACT_GELU),      # bw 1376: partial unit / feature tiles
+    ("g8k4", 512, 4096, 8, 4, S.ACT_RELU),          # the paper's G = 8, beta = 1/2 shape
+])
+def test_wide_blocks_tiled(orc, name, d, D, G, k, act):
+    """m' bw > 256 (the paper's G = 4 / 8 blocks): FWD1 / dA tile
+    the block's units (dA's dgate summed over the unit tiles by dgate_reduce),
+    FWD2 / dX stream K, dW1 / dW2 tile the features."""
+    _parity(orc, S.FfnConfig(name, d, D, G, k, 600, "bf16", act), 600)
+
+
 def test_k1_bf16(orc):
     cfg = S.FfnConfig("k1", 256, 2048, 16, 1, 400, "bf16", S.ACT_GELU)
     _parity(orc, cfg, 400)

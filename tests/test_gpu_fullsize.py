@@ -19,12 +19,14 @@ pytestmark = pytest.mark.gpu
 
 # (config, sampled blocks): LLaMA-size blocks are sampled once (each takes the
 # oracle ~10 s single-threaded: it sums over all ~8k tokens of the block)
-CASES = [("tiny", 2), ("bert", 2), ("opt", 2), ("llama", 1), ("llama_scale", 1)]
+CASES = [("tiny", 2), ("bert", 2), ("opt", 2), ("llama", 1), ("llama_scale", 1),
+         # the paper's own G = 8, beta = 1/2 workloads (wide blocks)
+         ("opt2048_g8", 1), ("llama4096_g8", 1)]
 
 
 @pytest.mark.parametrize("name,n_blocks", CASES)
 def test_fullsize_sampled_parity(orc, name, n_blocks):
-    cfg = S.CONFIGS[name]
+    cfg = S.ALL_CONFIGS[name]
     T = cfg.T
     inp = S.make_inputs(cfg, T)
     got = gpu_run(cfg, T, inp)

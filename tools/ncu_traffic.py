@@ -40,7 +40,8 @@ def profile_name(kernel):
     for key, name in (("topk_hist", "topk_hist"), ("bucket_scan", "bucket_scan"),
                       ("bucket_scatter", "bucket_scatter"), ("tile_sched", "tile_sched"),
                       ("gather_dgate", "gather_dgate"), ("dwr_reduce", "dwr_reduce"),
-                      ("da_post", "da_post"), ("router_simt", "router_simt")):
+                      ("da_post", "da_post"), ("router_simt", "router_simt"),
+                      ("dgate_reduce", "dgate_reduce")):
         if key in kernel:
             return name
     return kernel[:40]
