@@ -65,7 +65,7 @@ struct TcArgs {
   void* dlg;       // DA: dense dlogits [2][T][gpad] bf16
   const int32_t* tile_list;     // FWD1/DA: (mt << 8 | b) in m-tile-major order
   const int32_t* unit_offsets;  // FWD2/DX: weight-resident unit prefix per block
-  int n_stg;                    // FWD2/DX: 4 KB staging buffers per epilogue warp (1 or 2)
+  int n_stg;                    // FWD2/DX: 4 KB staging buffers per epilogue warp (1-3)
   int unit_mt;                  // FWD2/DX: m-tiles per weight-resident unit
   int prefetch;                 // gathering kinds: L2 prefetch of gathered rows (SPT_FFN_PREFETCH)
   unsigned long long* trace;    // SPT_FFN_TRACE: per-CTA role cycle counters (diagnostics)
@@ -547,7 +547,9 @@ __device__ __forceinline__ void epilogue_tma_store(const TcArgs& a, const TileIn
     tmem_ld64(tacc + c0, v, true);
     uint8_t* buf = stg + stg_i * 4096;
     if (lane == 0) {
-      if (a.n_stg == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
+      if (a.n_stg == 3) bulk_wait_read<2>();
+      else if (a.n_stg == 2) bulk_wait_read<1>();
+      else bulk_wait_read<0>();
     }
     __syncwarp();
 #pragma unroll
@@ -1459,6 +1461,16 @@ static void trace_report(TcArgs& a, const char* name, int grid, cudaStream_t s) 
   a.trace = nullptr;
 }
 
+static int nstg_fwd2() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("SPT_FFN_NSTG");
+    v = e ? atoi(e) : 3;  // measured: FWD2 1.21 ms at 3 vs 1.31 ms at 2 (LLaMA-scale)
+    if (v < 1 || v > 3) v = 3;
+  }
+  return v;
+}
+
 template <int KIND>
 static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   const int bst = (b_bytes(KIND, a.BN, a.kstream) + 1023) & ~1023;
@@ -1470,7 +1482,9 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
                        ? (KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64) * 32768
                        : 0;
   // FWD2 keeps 2 staging buffers per epilogue warp, DX (128 KB slab) keeps 1
-  if (resident) a.n_stg = slab > 65536 ? 1 : 2;
+  // (FWD2, K = bw <= 128: a 4-stage A ring covers two m-tiles, the rest of smem
+  // keeps more partial-output stores in flight; SPT_FFN_NSTG overrides)
+  if (resident) a.n_stg = slab > 65536 ? 1 : nstg_fwd2();
   const int stg = resident ? kEpiWarps * a.n_stg * 4096 + 1024
                            : (KIND == K_DAT ? kEpiWarps * 4096 + 1024 : 0);
   int stages = std::min(kind_bres(KIND) || kind_bk(KIND) < 64 ? 8 : 6,
@@ -1519,7 +1533,14 @@ static cudaError_t launch_pair(TcArgs& a, int units_upper, cudaStream_t s) {
   const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
   const int slab = kbu * 16384;  // this CTA's 128-column half of the slab
   const int extra = 1024 + 256;
-  a.n_stg = slab > 32768 ? 1 : 2;
+  {  // SPT_FFN_PAIR_NSTG overrides the staging depth of the pair kernel
+    static int v = -1;
+    if (v < 0) {
+      const char* e = getenv("SPT_FFN_PAIR_NSTG");
+      v = e ? atoi(e) : 0;
+    }
+    a.n_stg = (v >= 1 && v <= 3) ? v : (slab > 32768 ? 1 : 2);
+  }
   const int stg = kEpiWarps * a.n_stg * 4096 + 1024;
   const int stages = std::min(8, (227 * 1024 - extra - slab - stg) / kABytes);
   const int smem = slab + stages * kABytes + extra + stg;
