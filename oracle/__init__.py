@@ -55,6 +55,8 @@ def lib():
         _lib.spt_oracle_backward_blocks.argtypes = [i64, i32, i32, i32, i32, i32, i32,
                                                     P, P, P, P, P, P, P, i32, P, P, P]
         _lib.spt_oracle_forward_gemm_flops.argtypes = [i64, i32, i32, i32, i32, i32]
+        _lib.spt_oracle_balance.argtypes = [i64, i32, i32, P, P, P]
+        _lib.spt_oracle_balance.restype = ctypes.c_double
         _lib.spt_oracle_forward_gemm_flops.restype = ctypes.c_double
         _lib.spt_oracle_max_threads.restype = ctypes.c_int
     return _lib
@@ -125,9 +127,24 @@ def forward(x, w1, w2, logits, topk_idx, act, gate, tokens=None) -> np.ndarray:
     return y
 
 
+def balance(logits, topk_idx, want_grad=True):
+    """Load-balancing loss L = G sum_g f_g pbar_g and dL/dx_R [T, G]
+    (reading c18: f_g = n_g / (T k)).  spt_oracle.c."""
+    lg, ti = _f64(logits), np.ascontiguousarray(topk_idx, dtype=np.int32)
+    T, G = lg.shape
+    k = ti.shape[1] if ti.ndim == 2 else 1
+    dl = np.zeros((T, G)) if want_grad else None
+    L = float(lib().spt_oracle_balance(T, G, k, _ptr(lg), _ptr(ti), _ptr(dl)))
+    return L, dl
+
+
 def backward(x, w1, w2, w_r, logits, topk_idx, dy, act, gate, tokens=None, blocks=None,
-             want_tokens=True, want_blocks=True) -> dict:
-    """O2 backward: dx, dgate (per token subset) and dw1, dw2, dw_r (per block subset)."""
+             want_tokens=True, want_blocks=True, lb_weight=0.0) -> dict:
+    """O2 backward: dx, dgate (per token subset) and dw1, dw2, dw_r (per block subset).
+
+    lb_weight = lambda > 0 adds the gradient of lambda * L_balance (balance()):
+    x_R = x W_R gives dW_R += lambda * dL/dx_R^T X and dX += lambda * dL/dx_R W_R^T
+    (every block, selected or not); dgate is the task loss's only."""
     x, w1, w2, w_r, dy = _f64(x), _f64(w1), _f64(w2), _f64(w_r), _f64(dy)
     lg, ti = _f64(logits), np.ascontiguousarray(topk_idx, dtype=np.int32)
     T, d = x.shape
@@ -154,6 +171,14 @@ def backward(x, w1, w2, w_r, logits, topk_idx, dy, act, gate, tokens=None, block
                                          0 if bl is None else len(bl), _ptr(dw1), _ptr(dw2),
                                          _ptr(dwr))
         out["dw1"], out["dw2"], out["dw_r"] = dw1, dw2, dwr
+    if lb_weight:
+        _, dl = balance(lg, ti)
+        if want_tokens:
+            rows = slice(None) if tokens is None else np.asarray(tokens)
+            out["dx"][rows] += lb_weight * (dl[rows] @ w_r)
+        if want_blocks:
+            bl = slice(None) if blocks is None else np.asarray(blocks)
+            out["dw_r"][bl] += lb_weight * (dl[:, bl].T @ x)
     return out
 
 

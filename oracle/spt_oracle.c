@@ -370,3 +370,43 @@ double spt_oracle_forward_gemm_flops(int64_t T, int d, int D, int G, int k, int 
   const int mp = act == ACT_SWIGLU ? 2 : 1;
   return 2.0 * (double)T * k * (double)(mp + 1) * d * (double)(D / G);
 }
+
+/* ------------------------------ load-balancing loss */
+/* SPEC S:342-349 load_balance_loss (the paper names "similar activation
+ * rates" in §4.2, but gives no formula):
+ *   L = G * sum_g f_g * pbar_g
+ *   f_g    = n_g / (T k): the share of the T*k (token, block) activations on
+ *            block g (reading c18: the normalisation under which perfectly
+ *            uniform routing gives exactly 1);
+ *   pbar_g = (1/T) sum_t p_tg,  p_t = softmax(x_R[t])  ("pre").
+ * f is piecewise constant in the logits (no gradient through the selection,
+ * reading c11), so the gradient flows through p only:
+ *   dL/dx_R[t,j] = (G/T) sum_g f_g dp_tg/dx_R[t,j] = (G/T) p_tj (f_j - sum_g f_g p_tg).
+ * Returns L; writes dL/dx_R [T,G] when dlogit != NULL.  T = 0 returns 0. */
+double spt_oracle_balance(int64_t T, int G, int k, const double* logits,
+                          const int32_t* topk_idx, double* dlogit) {
+  if (T <= 0) return 0.0;
+  double* f = (double*)calloc((size_t)G, sizeof(double));
+  double* pbar = (double*)calloc((size_t)G, sizeof(double));
+  double* p = (double*)malloc((size_t)G * sizeof(double));
+  for (int64_t t = 0; t < T; ++t)
+    for (int j = 0; j < k; ++j) f[topk_idx[t * k + j]] += 1.0;
+  for (int g = 0; g < G; ++g) f[g] /= (double)T * (double)k;
+  for (int64_t t = 0; t < T; ++t) {  /* softmax row t, max-subtracted */
+    const double* l = logits + t * G;
+    double m = l[0], s = 0.0;
+    for (int g = 1; g < G; ++g) m = l[g] > m ? l[g] : m;
+    for (int g = 0; g < G; ++g) { p[g] = exp(l[g] - m); s += p[g]; }
+    double fp = 0.0;
+    for (int g = 0; g < G; ++g) { p[g] /= s; pbar[g] += p[g] / (double)T; fp += f[g] * p[g]; }
+    if (dlogit)
+      for (int j = 0; j < G; ++j) dlogit[t * G + j] = (double)G / (double)T * p[j] * (f[j] - fp);
+  }
+  double L = 0.0;
+  for (int g = 0; g < G; ++g) L += f[g] * pbar[g];
+  L *= (double)G;
+  free(f);
+  free(pbar);
+  free(p);
+  return L;
+}
