@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SPT_FFN_ABI_VERSION 1
+#define SPT_FFN_ABI_VERSION 2
 /* Height of a bucket tile: tile_offsets counts ceil(n_b / SPT_TILE_M) per block. */
 #define SPT_TILE_M 128
 
@@ -81,6 +81,9 @@ typedef struct {
   int32_t dtype;    /* spt_dtype: storage dtype of x, y, dy, dx, w1, w2, w_r */
   int32_t act;      /* spt_act */
   int32_t gate;     /* spt_gate */
+  /* lambda >= 0 (finite): spt_ffn_backward adds the gradient of lambda * L_balance
+   * (spt_ffn_balance_loss) to dw_r and dx.  0 disables it.  (ABI 2) */
+  float balance_weight;
 } spt_ffn_desc;
 
 /* Routing decision and bucket layout (all DEVICE buffers, caller-allocated).
@@ -129,6 +132,8 @@ spt_status spt_ffn_forward(const spt_ffn_desc* desc, const void* x, const void* 
  *   dx   [T,d]   = sum_b dZ_b W1_b + sum_b dlogit_b w_r[b]       (act dtype)
  *   dw1, dw2     = per-block weight gradients (fp32, rows of inactive blocks 0)
  *   dw_r [G,d]   = sum over pairs of dlogit * x_t  (fp32; 0 for GATE_NONE)
+ *                  + lambda * sum_t dL_balance/dx_R[t,:]^T x_t  (lambda = balance_weight;
+ *                  dx likewise gets + lambda * dL_balance/dx_R[t,:] w_r)
  *   dgate [T,k]  = dL/dg per pair (fp32, optional: may be NULL)
  * with dlogit = dgate * g (1 - g) for GATE_SIGMOID.  stash must be the one the
  * matching spt_ffn_forward wrote.  flags: SPT_BWD_ACCUMULATE_DW.
@@ -142,6 +147,18 @@ spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void*
                             const void* stash, const void* dy, void* dx, float* dw1, float* dw2,
                             float* dw_r, float* dgate, unsigned flags, void* ws, size_t ws_bytes,
                             void* dw_event, void* stream);
+
+/* Load-balancing loss of a routing decision (the paper
+ * names "similar activation rates", without a formula; SPEC
+ * S:342-349 defines it, reading c18):
+ *   L = G * sum_g f_g * pbar_g,  f_g = n_g / (T k),  pbar_g = (1/T) sum_t softmax(x_R[t])_g
+ * (L = 1 for perfectly uniform routing).  Reads r->logits and r->block_offsets
+ * (written by spt_ffn_route); writes the fp32 scalar *loss (DEVICE pointer) on
+ * `stream`.  Deterministic.  T = 0 writes 0.  Its gradient enters
+ * spt_ffn_backward through desc->balance_weight (every block's logit, not
+ * just the selected ones; f carries no gradient). */
+spt_status spt_ffn_balance_loss(const spt_ffn_desc* desc, const spt_route_buf* r, float* loss,
+                                void* ws, size_t ws_bytes, void* stream);
 
 /* Static string for a status code (never NULL). */
 const char* spt_status_string(spt_status s);

@@ -21,14 +21,15 @@ SPT_TILE_M = 128
 
 # every symbol include/spt_ffn.h declares
 EXPORTED = ("spt_ffn_sizes", "spt_ffn_route", "spt_ffn_forward", "spt_ffn_backward",
-            "spt_status_string", "spt_ffn_abi_version", "spt_ffn_launch_count",
+            "spt_ffn_balance_loss", "spt_status_string", "spt_ffn_abi_version", "spt_ffn_launch_count",
             "spt_ffn_profile_enable", "spt_ffn_profile_read")
 
 
 class spt_ffn_desc(ctypes.Structure):
     _fields_ = [("n_tokens", ctypes.c_int64), ("d_model", ctypes.c_int32), ("d_ff", ctypes.c_int32),
                 ("n_blocks", ctypes.c_int32), ("top_k", ctypes.c_int32), ("dtype", ctypes.c_int32),
-                ("act", ctypes.c_int32), ("gate", ctypes.c_int32)]
+                ("act", ctypes.c_int32), ("gate", ctypes.c_int32),
+                ("balance_weight", ctypes.c_float)]  # ABI 2
 
 
 class spt_route_buf(ctypes.Structure):
@@ -60,7 +61,9 @@ def lib() -> ctypes.CDLL:
         L.spt_ffn_forward.argtypes = [D, P, P, P, R, P, P, P, ctypes.c_size_t, P]
         L.spt_ffn_backward.argtypes = [D, P, P, P, P, R, P, P, P, P, P, P, P, ctypes.c_uint, P,
                                        ctypes.c_size_t, P, P]
-        for f in ("spt_ffn_sizes", "spt_ffn_route", "spt_ffn_forward", "spt_ffn_backward"):
+        L.spt_ffn_balance_loss.argtypes = [D, R, P, P, ctypes.c_size_t, P]
+        for f in ("spt_ffn_sizes", "spt_ffn_route", "spt_ffn_forward", "spt_ffn_backward",
+                  "spt_ffn_balance_loss"):
             getattr(L, f).restype = ctypes.c_int
         L.spt_status_string.argtypes = [ctypes.c_int]
         L.spt_status_string.restype = ctypes.c_char_p

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(128) combine_kernel(int64_t T, int d, int k, R
                                                       const TIn* __restrict__ part,
                                                       const float* __restrict__ dlogit,
                                                       const TIn* __restrict__ w_r,
+                                                      const TIn* __restrict__ dense,
                                                       TIn* __restrict__ out) {
   constexpr int V = Vec<TIn>::N;
   __shared__ int64_t rows[kMaxBlocks];
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(128) combine_kernel(int64_t T, int d, int k, R
   const int64_t t = blockIdx.x;
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     rows[j] = pair_row(r, t, k, j);
-    if (kBwd) {
+    if (kBwd && dlogit) {  // sparse router term (dense mode passes no dlogit)
       blk[j] = r.topk_idx[t * k + j];
       dl[j] = dlogit[rows[j]];
     }
@@ -93,7 +94,12 @@ __global__ void __launch_bounds__(128) combine_kernel(int64_t T, int d, int k, R
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[i] += v0[i];
     }
-    if (kBwd && w_r) {  // router term: sum_j dlogit_j * w_r[b_j]   (ascending j)
+    if (kBwd && dense) {  // router term precomputed densely (load-balancing loss on)
+      float v[V];
+      Vec<TIn>::load(dense + t * d + c, v);
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] += v[i];
+    } else if (kBwd && w_r) {  // router term: sum_j dlogit_j * w_r[b_j]   (ascending j)
       for (int jj = 0; jj < k; ++jj) {
         float w[V];
         Vec<TIn>::load(w_r + (int64_t)blk[jj] * d + c, w);
@@ -110,10 +116,11 @@ cudaError_t launch_combine_fwd(const Geom& g, const RouteView& r, const void* pa
   prof_begin("combine_fwd", s);
   if (g.dtype == SPT_BF16)
     combine_kernel<__nv_bfloat16, false><<<(unsigned)g.T, 128, 0, s>>>(
-        g.T, g.d, g.k, r, (const __nv_bfloat16*)part, nullptr, nullptr, (__nv_bfloat16*)y);
+        g.T, g.d, g.k, r, (const __nv_bfloat16*)part, nullptr, nullptr, nullptr,
+        (__nv_bfloat16*)y);
   else
     combine_kernel<float, false><<<(unsigned)g.T, 128, 0, s>>>(g.T, g.d, g.k, r, (const float*)part,
-                                                               nullptr, nullptr, (float*)y);
+                                                               nullptr, nullptr, nullptr, (float*)y);
   prof_end(s);
   count_launch();
   return cudaGetLastError();
@@ -126,11 +133,26 @@ cudaError_t launch_combine_bwd(const Geom& g, const RouteView& r, const void* pa
   prof_begin("combine_bwd", s);
   if (g.dtype == SPT_BF16)
     combine_kernel<__nv_bfloat16, true><<<(unsigned)g.T, 128, 0, s>>>(
-        g.T, g.d, g.k, r, (const __nv_bfloat16*)part, dlogit, (const __nv_bfloat16*)wr,
+        g.T, g.d, g.k, r, (const __nv_bfloat16*)part, dlogit, (const __nv_bfloat16*)wr, nullptr,
         (__nv_bfloat16*)dx);
   else
     combine_kernel<float, true><<<(unsigned)g.T, 128, 0, s>>>(
-        g.T, g.d, g.k, r, (const float*)part, dlogit, (const float*)wr, (float*)dx);
+        g.T, g.d, g.k, r, (const float*)part, dlogit, (const float*)wr, nullptr, (float*)dx);
+  prof_end(s);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_bwd_dense(const Geom& g, const RouteView& r, const void* part,
+                                     const void* dxr, void* dx, cudaStream_t s) {
+  prof_begin("combine_bwd", s);
+  if (g.dtype == SPT_BF16)
+    combine_kernel<__nv_bfloat16, true><<<(unsigned)g.T, 128, 0, s>>>(
+        g.T, g.d, g.k, r, (const __nv_bfloat16*)part, nullptr, nullptr,
+        (const __nv_bfloat16*)dxr, (__nv_bfloat16*)dx);
+  else
+    combine_kernel<float, true><<<(unsigned)g.T, 128, 0, s>>>(
+        g.T, g.d, g.k, r, (const float*)part, nullptr, nullptr, (const float*)dxr, (float*)dx);
   prof_end(s);
   count_launch();
   return cudaGetLastError();

@@ -22,6 +22,7 @@ struct Geom {
   int64_t n_chunks;  // ceil(T / kRouteChunk)
   int gpad;          // G rounded up to 16 (router GEMM N, dense dlogit width)
   int esize;         // bytes per act element
+  float lbw;         // load-balancing loss weight lambda (desc->balance_weight; 0 = off)
 };
 
 // Device-resident views of the routing decision (= spt_route_buf).
@@ -56,6 +57,9 @@ struct Bufs {
   int32_t* tile_list;     // [ceil(T*k/128) + G]: bucket tiles in (m-tile, block) order
   int32_t* unit_offsets;  // [G+2]: prefix of weight-resident work units per block; [G+1] = pair tiles
   int32_t* tile_block;    // [ceil(T*k/128) + G]: block of each 128-row bucket tile
+  float* lb_part;         // [n_chunks, G] f32: per-chunk softmax sums (balance loss)
+  void* lb_x;             // lambda != 0: bf16 [T, d] dense router term of dx (tcgen05 path)
+                          //              f32 [T, G] lambda dL_balance/dx_R (SIMT path)
 };
 
 int unit_mtiles();  // m-tiles per weight-resident unit (FWD2 / DX); SPT_FFN_UNIT_MT, default 128
@@ -86,6 +90,23 @@ cudaError_t launch_combine_bwd(const Geom& g, const RouteView& r, const void* pa
                                const float* dlogit, const void* w_r, void* dx, cudaStream_t s);
 cudaError_t launch_gather_dgate(const Geom& g, const RouteView& r, const float* dgate_rows,
                                 float* dgate_out, cudaStream_t s);
+// the combine of dx with the dense router term dxr [T,d] (act dtype) replacing
+// the sparse sum_j dlogit_j w_r[b_j] (load-balancing loss active)
+cudaError_t launch_combine_bwd_dense(const Geom& g, const RouteView& r, const void* part,
+                                     const void* dxr, void* dx, cudaStream_t s);
+
+// load-balancing loss (balance.cu, reading c18)
+cudaError_t launch_balance_loss(const Geom& g, const RouteView& r, const Bufs& b, float* loss,
+                                cudaStream_t s);
+// adds lambda dL/dx_R to the dense hi/lo bf16 dlogits (dlg != NULL) or writes it
+// to a dense f32 [T,G] buffer (lbg != NULL)
+cudaError_t launch_balance_grad(const Geom& g, const RouteView& r, void* dlg, float* lbg,
+                                cudaStream_t s);
+// SIMT path: dw_r += lbg^T x ; dx += lbg w_r (f32)
+cudaError_t launch_balance_simt_dwr(const Geom& g, const float* lbg, const void* x, float* dw_r,
+                                    cudaStream_t s);
+cudaError_t launch_balance_simt_dx(const Geom& g, const float* lbg, const void* w_r, void* dx,
+                                   cudaStream_t s);
 
 // tcgen05 path (tc_ffn.cu), bf16 only
 bool tc_supported(const Geom& g);

@@ -358,6 +358,11 @@ cudaError_t bwd_impl(const Geom& g, const T* x, const T* w1, const T* w2, const 
   count_launch(5);  // b1, b1b, dw x2, dwr
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  float* lbg = (float*)b.lb_x;  // f2: lambda dL_balance/dx_R [T, G] (every block)
+  if (g.lbw != 0.f) {
+    if ((e = launch_balance_grad(g, r, nullptr, lbg, s)) != cudaSuccess) return e;
+    if ((e = launch_balance_simt_dwr(g, lbg, x, dw_r, s)) != cudaSuccess) return e;
+  }
   if (dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
   OpDX<T> odx{(const T*)b.dz, w1, (T*)b.part, g.d, g.D, g.bw, g.mp};
   prof_begin("simt_b2", s);
@@ -366,6 +371,7 @@ cudaError_t bwd_impl(const Geom& g, const T* x, const T* w1, const T* w2, const 
   count_launch(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s)) != cudaSuccess) return e;
+  if (g.lbw != 0.f && (e = launch_balance_simt_dx(g, lbg, w_r, dx, s)) != cudaSuccess) return e;
   if (dgate_out) return launch_gather_dgate(g, r, b.dgate, dgate_out, s);
   return cudaSuccess;
 }

@@ -60,6 +60,8 @@ static spt_status make_geom(const spt_ffn_desc* d, Geom* g) {
   if (d->dtype != SPT_F32 && d->dtype != SPT_BF16) return SPT_ERR_INVALID_ARGUMENT;
   if (d->act < SPT_ACT_RELU || d->act > SPT_ACT_SWIGLU) return SPT_ERR_INVALID_ARGUMENT;
   if (d->gate != SPT_GATE_SIGMOID && d->gate != SPT_GATE_NONE) return SPT_ERR_INVALID_ARGUMENT;
+  if (!(d->balance_weight >= 0.f) || d->balance_weight > 3.0e38f)  // NaN, < 0, Inf
+    return SPT_ERR_INVALID_ARGUMENT;
   g->T = d->n_tokens;
   g->d = d->d_model;
   g->D = d->d_ff;
@@ -75,6 +77,7 @@ static spt_status make_geom(const spt_ffn_desc* d, Geom* g) {
   g->n_chunks = ceil_div(g->T, kRouteChunk);
   g->gpad = (int)ceil_div(g->G, 16) * 16;
   g->esize = d->dtype == SPT_BF16 ? 2 : 4;
+  g->lbw = d->balance_weight;
   if (g->G > kMaxBlocks) return SPT_ERR_UNSUPPORTED;
   if (g->d % 64) return SPT_ERR_UNSUPPORTED;
   if (g->bw % 16) return SPT_ERR_UNSUPPORTED;
@@ -93,7 +96,7 @@ static int dwr_splits(const Geom& g) {
 
 struct Sizes {
   size_t z, h, stash;
-  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, tb, ws;
+  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, tb, lbp, lbx, ws;
 };
 
 static Sizes compute_sizes(const Geom& g) {
@@ -115,8 +118,11 @@ static Sizes compute_sizes(const Geom& g) {
   s.tl = align256((size_t)(ceil_div(g.pairs, kTileM) + g.G) * 4);
   s.uo = align256((size_t)(g.G + 2) * 4);
   s.tb = s.tl;
+  s.lbp = align256((size_t)g.n_chunks * g.G * 4);  // balance loss: per-chunk softmax sums
+  s.lbx = g.lbw == 0.f ? 0                         // balance gradient: dense router term
+          : align256(g.dtype == SPT_BF16 ? (size_t)g.T * g.d * 2 : (size_t)g.T * g.G * 4);
   s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb +
-         s.tl + s.uo + s.tb;
+         s.tl + s.uo + s.tb + s.lbp + s.lbx;
   return s;
 }
 
@@ -143,6 +149,8 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
   b.tile_list = (int32_t*)w; w += s.tl;
   b.unit_offsets = (int32_t*)w; w += s.uo;
   b.tile_block = (int32_t*)w; w += s.tb;
+  b.lb_part = (float*)w; w += s.lbp;
+  b.lb_x = s.lbx ? (void*)w : nullptr; w += s.lbx;
   return b;
 }
 
@@ -279,6 +287,18 @@ spt_status spt_ffn_route(const spt_ffn_desc* desc, const void* x, const void* w_
     if (e != cudaSuccess) return SPT_ERR_CUDA;
   }
   return to_status(launch_topk_bucket(g, rv, b, s));
+}
+
+spt_status spt_ffn_balance_loss(const spt_ffn_desc* desc, const spt_route_buf* r, float* loss,
+                                void* ws, size_t ws_bytes, void* stream) {
+  Geom g;
+  spt_status st = make_geom(desc, &g);
+  if (st != SPT_OK) return st;
+  if (!route_complete(r, g.T) || !loss || !ws) return SPT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < compute_sizes(g).ws) return SPT_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = device_ok()) != SPT_OK) return st;
+  Bufs b = carve(g, nullptr, ws);
+  return to_status(launch_balance_loss(g, view(r), b, loss, (cudaStream_t)stream));
 }
 
 spt_status spt_ffn_forward(const spt_ffn_desc* desc, const void* x, const void* w1, const void* w2,

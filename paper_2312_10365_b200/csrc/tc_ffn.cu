@@ -41,7 +41,7 @@ namespace spt {
 
 using namespace tc;
 
-enum Kind : int { K_ROUTER = 0, K_FWD1, K_FWD2, K_DA, K_DX, K_DW1, K_DW2, K_DWR, K_DAT };
+enum Kind : int { K_ROUTER = 0, K_FWD1, K_FWD2, K_DA, K_DX, K_DW1, K_DW2, K_DWR, K_DAT, K_DXR };
 
 struct TcArgs {
   CUtensorMap ta;  // A operand
@@ -159,6 +159,7 @@ __device__ __forceinline__ int num_tiles(const TcArgs& a) {
   if (KIND == K_FWD2 || KIND == K_DX)  // weight-resident units, or (m-tile, N tile) when streaming K
     return a.kstream ? a.r.tile_offsets[a.G] * a.NT : a.unit_offsets[a.G];
   if (KIND == K_DW1 || KIND == K_DW2) return a.G * a.nu * a.NT;
+  if (KIND == K_DXR) return (int)ceil_div(a.T, 128) * a.NT;
   return a.NT * a.n_split;  // DWR (G <= 128 rows: one M tile)
 }
 
@@ -192,6 +193,11 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
     ti.prow0 = (int64_t)mg * 128;
     ti.pos0 = a.r.block_offsets[ti.b] + mt * 128;
     ti.nkb = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
+  } else if (KIND == K_DXR) {  // (token tile, N tile); K = hi then lo dlogits
+    ti.nt = tile % a.NT;
+    ti.prow0 = (int64_t)(tile / a.NT) * 128;
+    ti.n_valid = (int)(a.T - ti.prow0 < 128 ? a.T - ti.prow0 : 128);
+    ti.nkb = 2 * (a.gpad / 64 + (a.gpad % 64 ? 1 : 0));
   } else if (KIND == K_DW1 || KIND == K_DW2) {
     ti.nt = tile % a.NT;
     ti.ut = (tile / a.NT) % a.nu;
@@ -273,6 +279,11 @@ __device__ __forceinline__ void produce_tiles(const TcArgs& a, const TileInfo& t
     else krow = kb * 64 < a.bw ? ti.b * a.bw + kb * 64 : a.D + ti.b * a.bw + (kb * 64 - a.bw);
 #pragma unroll
     for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, krow);
+  } else if (KIND == K_DXR) {  // A = dense dlogits (hi rows, then lo rows), B = w_r (MN-major)
+    const int nkh = ti.nkb / 2, kk = kb % nkh;
+    tma_load_2d(sA, &a.ta, bar, kk * 64, (int)((kb < nkh ? 0 : a.T) + ti.prow0));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, kk * 64);
   } else if (KIND == K_DW1 || KIND == K_DW2) {
     constexpr int BK = kind_bk(KIND);  // MN-major A: 64-feature chunks x BK bucket rows
     for (int j = 0; j < 2 * a.MH; ++j)  // features [256 ut + 64 j, +64)
@@ -375,7 +386,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         for (int q = 0; q < 2; ++q) ud[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
       }
     }
-  } else if (KIND == K_FWD2 || KIND == K_DX) {
+  } else if (KIND == K_FWD2 || KIND == K_DX || KIND == K_DXR) {
     const int64_t prow = ti.prow0 + row;
     __nv_bfloat16* dst = (__nv_bfloat16*)a.out + prow * (int64_t)a.d + ti.nt * 256;
     const int ncols = min(256, a.d - ti.nt * 256);
@@ -1500,7 +1511,7 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   const int grid = std::max(1, std::min(tiles_upper, num_sms()));
   static const char* kNames[] = {"tc_router", "tc_fwd1_gate_up", "tc_fwd2_down", "tc_bwd_dA",
                                  "tc_bwd_dX", "tc_bwd_dW1", "tc_bwd_dW2", "tc_bwd_dWR",
-                                 "tc_bwd_dAT"};
+                                 "tc_bwd_dAT", "tc_bwd_dXR"};
   const bool trace_on = trace_begin(a, s);
   prof_begin(kNames[KIND], s);
   tc_gemm_kernel<KIND><<<grid, kThreads, smem, s>>>(a, stages);
@@ -2015,9 +2026,10 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
                         cudaEvent_t dw_ev, cudaStream_t s) {
   const int up = bucket_tiles_upper(g);
   const bool sig = g.gate == SPT_GATE_SIGMOID;
+  const bool lb = g.lbw != 0.f;  // load-balancing loss: dense router gradient (every block)
   cudaError_t e0 = build_schedules(g, r, b, s);
   if (e0 != cudaSuccess) return e0;
-  if (sig && cudaMemsetAsync(b.dlg, 0, (size_t)2 * g.T * g.gpad * 2, s) != cudaSuccess)
+  if ((sig || lb) && cudaMemsetAsync(b.dlg, 0, (size_t)2 * g.T * g.gpad * 2, s) != cudaSuccess)
     return cudaErrorUnknown;
   if (!use_fused_da() && g.bw <= 128) {  // a7: dA^T = W2_b dY[bucket]^T (tokens on N), then dgate/dZ
     TcArgs a{};
@@ -2104,8 +2116,13 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.acc_mode = accumulate;
     TRY(launch<K_DW2>(a, g.G * a.nu * a.NT, s));
   }
+  // f2: + lambda dL_balance/dx_R for every (token, block), into the dense dlogits
+  if (lb) {
+    cudaError_t e = launch_balance_grad(g, r, b.dlg, nullptr, s);
+    if (e != cudaSuccess) return e;
+  }
   // a10: dW_R = dLogits^T X  (split-K, hi + lo bf16 halves of dlogit)
-  if (sig) {
+  if (sig || lb) {
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.dlg, (uint64_t)2 * g.T, g.gpad, g.gpad, 64, 64) &&
@@ -2146,7 +2163,19 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       TRY(launch_bres<K_DX>(a, units_upper(g), s));
     }
   }
-  e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
+  if (lb) {
+    // router term of dx from the dense dlogits (task + balance): dXR = dLogits W_R
+    TcArgs a{};
+    base_args(a, g, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, b.dlg, (uint64_t)2 * g.T, g.gpad, g.gpad, 64, 128) &&
+              make_tmap_bf16_2d(&a.tb, w_r, g.G, g.d, g.d, 64, 64);
+    a.BN = 256;
+    a.out = b.lb_x;
+    TRY(launch<K_DXR>(a, (int)ceil_div(g.T, 128) * a.NT, s));
+    e = launch_combine_bwd_dense(g, r, b.part, b.lb_x, dx, s);
+  } else {
+    e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
+  }
   if (e != cudaSuccess) return e;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (dgate_out) return launch_gather_dgate(g, r, b.dgate, dgate_out, s);

@@ -17,10 +17,12 @@ _DT = {torch.float32: L.SPT_F32, torch.bfloat16: L.SPT_BF16}
 
 
 def make_desc(T: int, d: int, D: int, G: int, k: int, dtype: torch.dtype, act: int,
-              gate: int = L.SPT_GATE_SIGMOID) -> L.spt_ffn_desc:
+              gate: int = L.SPT_GATE_SIGMOID, balance_weight: float = 0.0) -> L.spt_ffn_desc:
+    """balance_weight = lambda of the load-balancing loss (0 = off; spt_ffn_balance_loss)."""
     if dtype not in _DT:
         raise ValueError(f"unsupported dtype {dtype}")
-    return L.spt_ffn_desc(int(T), int(d), int(D), int(G), int(k), _DT[dtype], int(act), int(gate))
+    return L.spt_ffn_desc(int(T), int(d), int(D), int(G), int(k), _DT[dtype], int(act), int(gate),
+                          float(balance_weight))
 
 
 def spt_ffn_sizes(desc: L.spt_ffn_desc) -> tuple[int, int]:
@@ -83,6 +85,15 @@ def spt_ffn_forward(desc, x, w1, w2, route: RouteBuffers, y, stash, ws, stream=N
         ws.numel() * ws.element_size(), _stream(stream)))
 
 
+def spt_ffn_balance_loss(desc, route: RouteBuffers, loss: torch.Tensor, ws, stream=None):
+    """L = G sum_g f_g pbar_g of the routing in ``route`` into the 1-element
+    float32 device tensor ``loss`` (reading c18)."""
+    rb = route.as_c()
+    L.check("spt_ffn_balance_loss", L.lib().spt_ffn_balance_loss(
+        ctypes.byref(desc), ctypes.byref(rb), _p(loss), _p(ws), ws.numel() * ws.element_size(),
+        _stream(stream)))
+
+
 def spt_ffn_backward(desc, x, w1, w2, w_r, route: RouteBuffers, stash, dy, dx, dw1, dw2, dw_r,
                      ws, dgate=None, flags: int = 0, stream=None, dw_event=None):
     """dw_event: optional torch.cuda.Event recorded once dw1/dw2/dw_r are final
@@ -124,8 +135,9 @@ class RoutedFFN:
     """Buffers for one routed-FFN layer shape (a convenience owner of memory;
     the three methods are the ABI calls)."""
 
-    def __init__(self, T, d, D, G, k, dtype, act, gate=L.SPT_GATE_SIGMOID, device="cuda"):
-        self.desc = make_desc(T, d, D, G, k, dtype, act, gate)
+    def __init__(self, T, d, D, G, k, dtype, act, gate=L.SPT_GATE_SIGMOID, device="cuda",
+                 balance_weight=0.0):
+        self.desc = make_desc(T, d, D, G, k, dtype, act, gate, balance_weight)
         self.T, self.d, self.D, self.G, self.k = T, d, D, G, k
         self.dtype, self.act, self.gate = dtype, act, gate
         self.mp = 2 if act == L.SPT_ACT_SWIGLU else 1
@@ -140,10 +152,16 @@ class RoutedFFN:
         self.dw2 = torch.empty(D, d, dtype=torch.float32, device=device)
         self.dw_r = torch.empty(G, d, dtype=torch.float32, device=device)
         self.dgate = torch.empty(T, k, dtype=torch.float32, device=device)
+        self.loss_lb = torch.zeros(1, dtype=torch.float32, device=device)
 
     def route(self, x, w_r, flags=0, stream=None):
         spt_ffn_route(self.desc, x, w_r, self.route_buf, self.ws, flags, stream)
         return self.route_buf
+
+    def balance_loss(self, stream=None):
+        """Load-balancing loss of the current routing (device scalar)."""
+        spt_ffn_balance_loss(self.desc, self.route_buf, self.loss_lb, self.ws, stream)
+        return self.loss_lb
 
     def forward(self, x, w1, w2, stream=None):
         spt_ffn_forward(self.desc, x, w1, w2, self.route_buf, self.y, self.stash, self.ws, stream)

@@ -30,11 +30,13 @@ def to_dev(a, cfg):
 
 
 def gpu_run(cfg: S.FfnConfig, T: int, inputs: dict, logits_in=None, backward=True,
-            accumulate_from=None, want_dgate=True):
-    """Route -> forward -> backward through the ABI; returns numpy outputs."""
+            accumulate_from=None, want_dgate=True, balance_weight=0.0):
+    """Route -> forward -> backward through the ABI; returns numpy outputs
+    (balance_weight: lambda of the load-balancing loss; adds "loss_lb")."""
     import torch
     import paper_2312_10365_b200 as P
-    f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, torch_dtype(cfg), cfg.act, cfg.gate)
+    f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, torch_dtype(cfg), cfg.act, cfg.gate,
+                    balance_weight=balance_weight)
     x, w1, w2, w_r, dy = (to_dev(inputs[n], cfg) for n in ("x", "w1", "w2", "w_r", "dy"))
     flags = 0
     if logits_in is not None:
@@ -46,6 +48,7 @@ def gpu_run(cfg: S.FfnConfig, T: int, inputs: dict, logits_in=None, backward=Tru
            ("logits", "topk_idx", "topk_gate", "block_offsets", "bucket_token", "bucket_gate",
             "pair_slot", "tile_offsets")}
     out["y"] = y.float().cpu().numpy()
+    out["loss_lb"] = float(f.balance_loss().cpu()[0])
     if backward:
         bflags = 0
         if accumulate_from is not None:
@@ -63,12 +66,13 @@ def gpu_run(cfg: S.FfnConfig, T: int, inputs: dict, logits_in=None, backward=Tru
 
 
 def oracle_run(orc, cfg: S.FfnConfig, inputs: dict, logits, topk_idx, tokens=None, blocks=None,
-               backward=True):
+               backward=True, lb_weight=0.0):
     """fp64 oracle on the same input bits.  logits: fp64 (or fp32) [T,G]."""
     y = orc.forward(inputs["x"], inputs["w1"], inputs["w2"], logits, topk_idx, cfg.act, cfg.gate,
                     tokens=tokens)
     out = {"y": y}
     if backward:
         out.update(orc.backward(inputs["x"], inputs["w1"], inputs["w2"], inputs["w_r"], logits,
-                                topk_idx, inputs["dy"], cfg.act, cfg.gate, tokens=tokens, blocks=blocks))
+                                topk_idx, inputs["dy"], cfg.act, cfg.gate, tokens=tokens, blocks=blocks,
+                                lb_weight=lb_weight))
     return out

@@ -22,7 +22,7 @@ def test_library_exports_every_declared_symbol():
     assert set(decl) == set(_lib.EXPORTED), decl
     for name in decl:
         assert hasattr(L, name), name
-    assert L.spt_ffn_abi_version() == 1
+    assert L.spt_ffn_abi_version() == 2
 
 
 def test_status_strings():
@@ -90,3 +90,20 @@ def test_workspace_too_small_rejected():
     fake = ctypes.c_void_p(16)  # never dereferenced: size check precedes any launch
     rb = _lib.spt_route_buf(*([16] * 8))
     assert L.spt_ffn_route(ctypes.byref(d), fake, fake, 0, ctypes.byref(rb), fake, 1, None) == 3
+
+
+def test_desc_layout_and_balance_weight_validation():
+    """ABI 2: spt_ffn_desc carries balance_weight (lambda >= 0, finite); the
+    workspace grows by the dense router-term buffer only when lambda != 0."""
+    import ctypes
+    import torch
+    from paper_2312_10365_b200 import _lib, spt_ffn_sizes
+    assert ctypes.sizeof(_lib.spt_ffn_desc) == 40
+    for bad in (-1.0, float("nan"), float("inf")):
+        d = _desc(balance_weight=bad)
+        s, w = ctypes.c_size_t(), ctypes.c_size_t()
+        assert _lib.lib().spt_ffn_sizes(ctypes.byref(d), ctypes.byref(s), ctypes.byref(w)) == 1
+    for dt, extra in ((torch.float32, 256 * 8 * 4), (torch.bfloat16, 256 * 128 * 2)):
+        _, w0 = spt_ffn_sizes(_desc(dtype=dt))
+        _, w1 = spt_ffn_sizes(_desc(dtype=dt, balance_weight=0.01))
+        assert w1 - w0 == extra, (dt, w1 - w0)
