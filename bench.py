@@ -180,10 +180,11 @@ def run_reference(args, cfg):
     }), flush=True)
 
 
-def workload_config(cfg, world, T):
+def workload_config(cfg, world, T, balance_weight=0.0):
+    lb = f", load-balancing loss lambda={balance_weight}" if balance_weight else ""
     return {"workload": f"{cfg.name}: routed FFN d={cfg.d} D={cfg.D} G={cfg.G} k={cfg.k} bw={cfg.bw} "
                         f"act={['relu', 'gelu', 'swiglu'][cfg.act]} "
-                        f"gate={['sigmoid', 'none'][cfg.gate]}, {T} tokens per GPU",
+                        f"gate={['sigmoid', 'none'][cfg.gate]}, {T} tokens per GPU{lb}",
             "tokens_per_gpu": T, "global_tokens": T * world, "parallelism": f"dp{world}",
             "l2": "inputs larger than L2 (x, dy %.0f MB each; weights %.0f MB)" % (
                 T * cfg.d * (2 if cfg.dtype == 'bf16' else 4) / 1e6,
@@ -246,6 +247,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense cuBLAS context")
+    ap.add_argument("--balance-weight", type=float, default=0.0,
+                    help="lambda of the load-balancing loss (SURVEY f2; 0 = the north_star step)")
     args = ap.parse_args()
     cfg = S.ALL_CONFIGS[args.config]
     if args.tokens:
@@ -274,7 +277,8 @@ def main():
     dev = {n: torch.from_numpy(inp[n]).to(dt).cuda() for n in ("x", "w1", "w2", "w_r", "dy")}
     del inp
     x, w1, w2, w_r, dy = (dev[n] for n in ("x", "w1", "w2", "w_r", "dy"))
-    f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, dt, cfg.act, cfg.gate)
+    f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, dt, cfg.act, cfg.gate,
+                    balance_weight=args.balance_weight)
     fg = dp.attach_flat_grads(f)
 
     # N > 1: the dW all-reduce starts (side stream) at the event the backward
@@ -284,6 +288,8 @@ def main():
 
     def step():
         f.route(x, w_r)
+        if args.balance_weight:
+            f.balance_loss()  # the router's load-balancing loss of this routing
         f.forward(x, w1, w2)
         ar.wait()
         f.backward(x, w1, w2, w_r, dy, dw_event=ar.event)
@@ -410,7 +416,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded random tokens and weights)",
-        "config": workload_config(cfg, world, T),
+        "config": workload_config(cfg, world, T, args.balance_weight),
         "tensor_pipe_frac_of_bf16_peak": {"step_gemm_tflops": step_tf, "peak": pk["bf16_sustained"],
                                           "frac": step_tf / pk["bf16_sustained"],
                                           "peak_src": pk["src"] + " bf16 sustained"},
