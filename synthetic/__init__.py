@@ -88,7 +88,8 @@ PAPER_CONFIGS = {
 }
 ALL_CONFIGS = {**CONFIGS, **PAPER_CONFIGS}
 
-_TENSOR_IDS = {"x": 1, "w1": 2, "w2": 3, "w_r": 4, "dy": 5, "logits": 6}
+_TENSOR_IDS = {"x": 1, "w1": 2, "w2": 3, "w_r": 4, "dy": 5, "logits": 6,
+               "b1": 7, "c1": 8, "b2": 9, "c2": 10}
 
 
 def _stream(seed: int, name: str, extra: int = 0) -> np.random.Generator:
@@ -140,6 +141,30 @@ def make_inputs(cfg: FfnConfig, T: int | None = None, need=("x", "w1", "w2", "w_
     if "w_r" in need:
         out["w_r"] = round_to_dtype(_stream(s, "w_r").standard_normal((G, d)) / np.sqrt(d), dt)
     return out
+
+
+LORA_RANK = 16  # d_lora default
+
+
+def make_lora(cfg: FfnConfig, r: int = LORA_RANK) -> dict:
+    """Seeded LoRA factors of both FFN projections (PAPER.md:159
+    Y = XW + XBC, B in R^{d x r}, C in R^{r x h}), in the library's storage:
+      b1 = B_I^T [m', r, d], c1 = C_I^T [m', D, r], b2 = B_O [D, r], c2 = C_O [r, d]
+    (m' = 2 for SwiGLU: gate, up; the leading axis is dropped for m' = 1).
+    Scales: b1 ~ N(0, 1/d) (u = x B_I ~ N(0,1)); c1 ~ N(0, 0.25/r) (the LoRA term of
+    z ~ N(0, 1/4), next to x W_I ~ N(0,1)); b2 ~ N(0, 1/(k bw)); c2 ~ N(0, 0.25/r).
+    Both factors are non-zero (LoRA's usual zero init of one factor would make
+    the other's gradient vanish and the parity check vacuous)."""
+    s, d, D, k, bw, dt = cfg.seed, cfg.d, cfg.D, cfg.k, cfg.bw, cfg.dtype
+    mp = cfg.mprime
+    lead = (mp,) if mp == 2 else ()
+    c = np.sqrt(0.25 / r)
+    return {
+        "b1": round_to_dtype(_stream(s, "b1", r).standard_normal(lead + (r, d)) / np.sqrt(d), dt),
+        "c1": round_to_dtype(_stream(s, "c1", r).standard_normal(lead + (D, r)) * c, dt),
+        "b2": round_to_dtype(_stream(s, "b2", r).standard_normal((D, r)) / np.sqrt(k * bw), dt),
+        "c2": round_to_dtype(_stream(s, "c2", r).standard_normal((r, d)) * c, dt),
+    }
 
 
 _ROW_CHUNK = 1024
