@@ -72,10 +72,18 @@ def kernel_work(cfg, T):
     }
 
 
-def step_gemm_flops(cfg, T):
-    """fwd 2(m'+1) d bw k + bwd 2x that, per token, + router 6 d G."""
-    per_tok = 2.0 * (cfg.mprime + 1) * cfg.d * cfg.bw * cfg.k * 3 + 6.0 * cfg.d * cfg.G
-    return per_tok * T
+def step_gemm_flops(cfg, T, lora=0):
+    """fwd 2(m'+1) d bw k + bwd 2x that, per token, + router 6 d G.
+    LoRA rank r: W frozen, so the bwd is dA + dX only (1x fwd), plus the
+    rank-r terms: per pair 2 bw r (2 m' + 1) fwd and 2 bw r (2 m' + 2) bwd, per
+    token 2 d r (m' + 1) fwd and 2 d r (2 m' + 2) bwd."""
+    mp, d, bw, k = cfg.mprime, cfg.d, cfg.bw, cfg.k
+    fwd = 2.0 * (mp + 1) * d * bw * k
+    if not lora:
+        return (fwd * 3 + 6.0 * d * cfg.G) * T
+    r = lora
+    extra = k * 2.0 * bw * r * (4 * mp + 3) + 2.0 * d * r * (3 * mp + 3)
+    return (fwd * 2 + 6.0 * d * cfg.G + extra) * T
 
 
 # ------------------------------------------------------------------ clocks
@@ -128,45 +136,55 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- oracle
-def oracle_sample(cfg, n_tok):
+def oracle_sample(cfg, n_tok, lora=0):
     """The CPU oracle (as it stands) over route + fwd + bwd of `n_tok` tokens of
-    the workload; returns (seconds, threads)."""
+    the workload (LoRA rank > 0: oracle/lora.py's fwd + bwd); returns (seconds, threads)."""
     import oracle
     inp = S.make_inputs(cfg, n_tok)
+    lo = S.make_lora(cfg, lora) if lora else None
     t = time.perf_counter()
     lg = oracle.router(inp["x"], inp["w_r"])
     ti = oracle.topk(lg.astype(np.float32), cfg.k)
     oracle.bucket(ti, cfg.G)
-    oracle.forward(inp["x"], inp["w1"], inp["w2"], lg, ti, cfg.act, cfg.gate)
-    oracle.backward(inp["x"], inp["w1"], inp["w2"], inp["w_r"], lg, ti, inp["dy"], cfg.act, cfg.gate)
+    if lora:
+        from oracle import lora as OL
+        OL.lora_forward(inp["x"], inp["w1"], inp["w2"], lo, lg, ti, cfg.act, cfg.gate)
+        OL.lora_backward(inp["x"], inp["w1"], inp["w2"], inp["w_r"], lo, lg, ti, inp["dy"], cfg.act,
+                         cfg.gate)
+    else:
+        oracle.forward(inp["x"], inp["w1"], inp["w2"], lg, ti, cfg.act, cfg.gate)
+        oracle.backward(inp["x"], inp["w1"], inp["w2"], inp["w_r"], lg, ti, inp["dy"], cfg.act,
+                        cfg.gate)
     return time.perf_counter() - t, oracle.max_threads()
 
 
-def cpu_baseline(cfg, target_s=15.0):
+def cpu_baseline(cfg, target_s=15.0, lora=0):
     """Oracle on a token sample sized (two calibration rounds) to ~target_s."""
-    n, (secs, cores) = 16, oracle_sample(cfg, 16)
+    n, (secs, cores) = 16, oracle_sample(cfg, 16, lora)
     for _ in range(2):
         if secs >= 0.6 * target_s or n >= 8192:
             break
         n = int(max(16, min(8192, n * target_s / max(secs, 1e-3))))
-        secs, cores = oracle_sample(cfg, n)
+        secs, cores = oracle_sample(cfg, n, lora)
+    what = (f"LoRA rank {lora}: fp64 numpy oracle (oracle/lora.py, BLAS threads)" if lora else
+            f"all {cfg.G} blocks' dW), {secs:.1f} s, fp64 C oracle, OpenMP")
     return {"value": n / secs, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n} tokens of {cfg.name} (route+fwd+bwd, all {cfg.G} blocks' dW), "
-                      f"{secs:.1f} s, fp64 C oracle, OpenMP"}
+            "sample": f"{n} tokens of {cfg.name} (route+fwd+bwd, " + what
+            + (f", {secs:.1f} s" if lora else "")}
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    t0, _ = oracle_sample(cfg, 8)
+    t0, _ = oracle_sample(cfg, 8, args.lora)
     budget = 150.0 / max(1, args.steps + args.warmup)          # seconds per step
     n = int(max(8, min(2048, 8 * budget / max(t0, 1e-3))))
     for _ in range(args.warmup):
-        oracle_sample(cfg, n)
+        oracle_sample(cfg, n, args.lora)
     tot, cores = 0.0, 1
     for _ in range(args.steps):
-        s, cores = oracle_sample(cfg, n)
+        s, cores = oracle_sample(cfg, n, args.lora)
         tot += s
     value = n * args.steps / tot
     sample = f"{n} tokens of {cfg.name} per step (route+fwd+bwd, fp64 C oracle, OpenMP)"
@@ -174,14 +192,16 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(cfg, args.gpus, cfg.T),
+        "data": "synthetic", "config": workload_config(cfg, args.gpus, cfg.T, args.balance_weight, args.lora),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-def workload_config(cfg, world, T, balance_weight=0.0):
+def workload_config(cfg, world, T, balance_weight=0.0, lora=0):
     lb = f", load-balancing loss lambda={balance_weight}" if balance_weight else ""
+    if lora:
+        lb += f", LoRA rank {lora} on fc1/fc2 (W frozen: no dW1/dW2; factor grads)"
     return {"workload": f"{cfg.name}: routed FFN d={cfg.d} D={cfg.D} G={cfg.G} k={cfg.k} bw={cfg.bw} "
                         f"act={['relu', 'gelu', 'swiglu'][cfg.act]} "
                         f"gate={['sigmoid', 'none'][cfg.gate]}, {T} tokens per GPU{lb}",
@@ -249,6 +269,9 @@ def main():
     ap.add_argument("--no-dense", action="store_true", help="skip the dense cuBLAS context")
     ap.add_argument("--balance-weight", type=float, default=0.0,
                     help="lambda of the load-balancing loss (SURVEY f2; 0 = the north_star step)")
+    ap.add_argument("--lora", type=int, default=0, metavar="R",
+                    help="LoRA-wrapped routed FFN of rank R (SURVEY f3; W frozen, factors trained); "
+                         "0 = the north_star step")
     args = ap.parse_args()
     cfg = S.ALL_CONFIGS[args.config]
     if args.tokens:
@@ -277,8 +300,14 @@ def main():
     dev = {n: torch.from_numpy(inp[n]).to(dt).cuda() for n in ("x", "w1", "w2", "w_r", "dy")}
     del inp
     x, w1, w2, w_r, dy = (dev[n] for n in ("x", "w1", "w2", "w_r", "dy"))
-    f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, dt, cfg.act, cfg.gate,
-                    balance_weight=args.balance_weight)
+    lora = None
+    if args.lora:
+        lora = {n: torch.from_numpy(v).to(dt).cuda() for n, v in S.make_lora(cfg, args.lora).items()}
+        f = P.RoutedLoRAFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, dt, cfg.act, args.lora, cfg.gate,
+                            balance_weight=args.balance_weight)
+    else:
+        f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, dt, cfg.act, cfg.gate,
+                        balance_weight=args.balance_weight)
     fg = dp.attach_flat_grads(f)
 
     # N > 1: the dW all-reduce starts (side stream) at the event the backward
@@ -290,9 +319,14 @@ def main():
         f.route(x, w_r)
         if args.balance_weight:
             f.balance_loss()  # the router's load-balancing loss of this routing
-        f.forward(x, w1, w2)
-        ar.wait()
-        f.backward(x, w1, w2, w_r, dy, dw_event=ar.event)
+        if lora is None:
+            f.forward(x, w1, w2)
+            ar.wait()
+            f.backward(x, w1, w2, w_r, dy, dw_event=ar.event)
+        else:
+            f.forward(x, w1, w2, lora)
+            ar.wait()
+            f.backward(x, w1, w2, w_r, lora, dy, grad_event=ar.event)
         ar.launch()
 
     def barrier():
@@ -348,7 +382,7 @@ def main():
         dyh.copy_(dy)
         yh = torch.empty_like(x, device="cpu").pin_memory()
         dxh = torch.empty_like(x, device="cpu").pin_memory()
-        pipe = HostStepPipeline(f, w1, w2, w_r, grad_hook=lambda: dp.allreduce_grads(fg))
+        pipe = HostStepPipeline(f, w1, w2, w_r, grad_hook=lambda: dp.allreduce_grads(fg), lora=lora)
         for i in range(3):
             pipe.step(i, xh, dyh, yh, dxh)
         pipe.synchronize()
@@ -411,12 +445,12 @@ def main():
                         "frac": ach / pk["hbm_gbs"], "traffic": traffic, "peak_src": pk["src"],
                         "algorithmic_per_launch": amt, "ms_per_launch": per,
                         "share_of_step": tot / args.steps / step_ms_prof}
-    step_tf = step_gemm_flops(cfg, T) / (ms_max / 1e3) / 1e12
+    step_tf = step_gemm_flops(cfg, T, args.lora) / (ms_max / 1e3) / 1e12
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded random tokens and weights)",
-        "config": workload_config(cfg, world, T, args.balance_weight),
+        "config": workload_config(cfg, world, T, args.balance_weight, args.lora),
         "tensor_pipe_frac_of_bf16_peak": {"step_gemm_tflops": step_tf, "peak": pk["bf16_sustained"],
                                           "frac": step_tf / pk["bf16_sustained"],
                                           "peak_src": pk["src"] + " bf16 sustained"},
@@ -429,7 +463,7 @@ def main():
             out["dense_context"] = {"error": str(ex)[:200]}
     if world == 1 and not args.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = cpu_baseline(cfg)
+            out["cpu_baseline"] = cpu_baseline(cfg, lora=args.lora)
         except Exception as ex:  # oracle build failure must not hide the GPU number
             out["cpu_baseline"] = {"error": str(ex)}
     print(json.dumps(out), flush=True)

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SPT_FFN_ABI_VERSION 2
+#define SPT_FFN_ABI_VERSION 3
 /* Height of a bucket tile: tile_offsets counts ceil(n_b / SPT_TILE_M) per block. */
 #define SPT_TILE_M 128
 
@@ -159,6 +159,66 @@ spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void*
  * just the selected ones; f carries no gradient). */
 spt_status spt_ffn_balance_loss(const spt_ffn_desc* desc, const spt_route_buf* r, float* loss,
                                 void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * LoRA-wrapped routed FFN (ABI 3) -- the paper's
+ * fine-tuning mode.  LoRA (Eq. 5) writes a projection
+ * Y = XW as Y = XW + XBC with W frozen and B in R^{d x r}, C in R^{r x h}
+ * trained; SPT wraps both FFN projections (Model Adapter log, PAPER.md:
+ * 1323-1328; rank "d_lora", default 16) and routes the FFN
+ * (§4.2): block b uses the hidden units [b bw, (b+1) bw) of W_I + B_I C_I and
+ * W_O + B_O C_O (reading c19).  Per token t, block b in S_t:
+ *   z = x_t W_I[:,b] + (x_t B_I) C_I[:,b],   h~ = g act(z)
+ *   y_t = sum_b h~ W_O[b,:] + (sum_b h~ B_O[b,:]) C_O
+ * Storage (all DEVICE, row-major, act dtype = bf16; m' = 2 for SwiGLU, whose
+ * gate and up projections each carry their own factors):
+ *   b1 : [m', r, d]  = B_I^T            c1 : [m', D, r] = C_I^T  (block b = rows)
+ *   b2 : [D, r]      = B_O (block b = rows)     c2 : [r, d]  = C_O
+ * Gradients (fp32, same shapes): db1, dc1, db2, dc2.
+ * Support: bf16 only (SPT_ERR_UNSUPPORTED for fp32); 1 <= r and m' r <= 64.
+ * Numerics: x B_I and dy C_O^T enter the tensor-core GEMMs rounded once to
+ * bf16 (an extra 64-wide K stage of FWD1 / dA); the reductions over a token's
+ * blocks (sum_b h~ B_O, sum_b dZ C_I^T) are fp32 in ascending block order. */
+typedef struct {
+  int32_t rank;   /* r */
+  const void* b1; /* [m', r, d] */
+  const void* c1; /* [m', D, r] */
+  const void* b2; /* [D, r]     */
+  const void* c2; /* [r, d]     */
+} spt_lora;
+
+typedef struct {
+  float* db1; /* [m', r, d] */
+  float* dc1; /* [m', D, r] */
+  float* db2; /* [D, r]     */
+  float* dc2; /* [r, d]     */
+} spt_lora_grads;
+
+/* Stash / workspace bytes of the LoRA-wrapped calls (>= spt_ffn_sizes').  Host only.
+ * SPT_ERR_INVALID_ARGUMENT: bad desc, rank < 1, NULL out-pointer;
+ * SPT_ERR_UNSUPPORTED: fp32 dtype or m' rank > 64. */
+spt_status spt_ffn_lora_sizes(const spt_ffn_desc* desc, int32_t rank, size_t* stash_bytes,
+                              size_t* workspace_bytes);
+
+/* Forward of the LoRA-wrapped routed FFN (formula above; routing from
+ * spt_ffn_route).  w1, w2 are the frozen W_I^T, W_O.  Writes y [T,d] and the
+ * stash (must survive unchanged until spt_ffn_lora_backward). */
+spt_status spt_ffn_lora_forward(const spt_ffn_desc* desc, const void* x, const void* w1,
+                                const void* w2, const spt_lora* lora, const spt_route_buf* r,
+                                void* y, void* stash, void* ws, size_t ws_bytes, void* stream);
+
+/* Backward of spt_ffn_lora_forward (W_I, W_O frozen: no dW1 / dW2; routing
+ * fixed).  Writes dx [T,d] (act dtype), the factor gradients *grads, dw_r
+ * (router, as spt_ffn_backward incl. desc->balance_weight) and optionally
+ * dgate [T,k].  flags: SPT_BWD_ACCUMULATE_DW adds into the factor gradients
+ * and dw_r.  grad_event (optional cudaEvent_t) is recorded once every gradient
+ * (factors and dw_r) is final -- for a data-parallel all-reduce. */
+spt_status spt_ffn_lora_backward(const spt_ffn_desc* desc, const void* x, const void* w1,
+                                 const void* w2, const void* w_r, const spt_lora* lora,
+                                 const spt_route_buf* r, const void* stash, const void* dy,
+                                 void* dx, const spt_lora_grads* grads, float* dw_r, float* dgate,
+                                 unsigned flags, void* ws, size_t ws_bytes, void* grad_event,
+                                 void* stream);
 
 /* Static string for a status code (never NULL). */
 const char* spt_status_string(spt_status s);

@@ -22,7 +22,8 @@ SPT_TILE_M = 128
 # every symbol include/spt_ffn.h declares
 EXPORTED = ("spt_ffn_sizes", "spt_ffn_route", "spt_ffn_forward", "spt_ffn_backward",
             "spt_ffn_balance_loss", "spt_status_string", "spt_ffn_abi_version", "spt_ffn_launch_count",
-            "spt_ffn_profile_enable", "spt_ffn_profile_read")
+            "spt_ffn_profile_enable", "spt_ffn_profile_read",
+            "spt_ffn_lora_sizes", "spt_ffn_lora_forward", "spt_ffn_lora_backward")  # ABI 3
 
 
 class spt_ffn_desc(ctypes.Structure):
@@ -36,6 +37,14 @@ class spt_route_buf(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("logits", "topk_idx", "topk_gate", "block_offsets",
                                                "bucket_token", "bucket_gate", "pair_slot",
                                                "tile_offsets")]
+
+
+class spt_lora(ctypes.Structure):  # ABI 3: LoRA factors (device pointers)
+    _fields_ = [("rank", ctypes.c_int32)] + [(n, ctypes.c_void_p) for n in ("b1", "c1", "b2", "c2")]
+
+
+class spt_lora_grads(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("db1", "dc1", "db2", "dc2")]
 
 
 class SptError(RuntimeError):
@@ -62,8 +71,14 @@ def lib() -> ctypes.CDLL:
         L.spt_ffn_backward.argtypes = [D, P, P, P, P, R, P, P, P, P, P, P, P, ctypes.c_uint, P,
                                        ctypes.c_size_t, P, P]
         L.spt_ffn_balance_loss.argtypes = [D, R, P, P, ctypes.c_size_t, P]
+        LO, LG = ctypes.POINTER(spt_lora), ctypes.POINTER(spt_lora_grads)
+        L.spt_ffn_lora_sizes.argtypes = [D, ctypes.c_int32, sz, sz]
+        L.spt_ffn_lora_forward.argtypes = [D, P, P, P, LO, R, P, P, P, ctypes.c_size_t, P]
+        L.spt_ffn_lora_backward.argtypes = [D, P, P, P, P, LO, R, P, P, P, LG, P, P, ctypes.c_uint,
+                                            P, ctypes.c_size_t, P, P]
         for f in ("spt_ffn_sizes", "spt_ffn_route", "spt_ffn_forward", "spt_ffn_backward",
-                  "spt_ffn_balance_loss"):
+                  "spt_ffn_balance_loss", "spt_ffn_lora_sizes", "spt_ffn_lora_forward",
+                  "spt_ffn_lora_backward"):
             getattr(L, f).restype = ctypes.c_int
         L.spt_status_string.argtypes = [ctypes.c_int]
         L.spt_status_string.restype = ctypes.c_char_p

@@ -49,11 +49,6 @@ struct Vec<__nv_bfloat16> {
   }
 };
 
-__device__ __forceinline__ int64_t pair_row(const RouteView& r, int64_t t, int k, int j) {
-  const int b = r.topk_idx[t * k + j];
-  return (int64_t)r.tile_offsets[b] * kTileM + (r.pair_slot[t * k + j] - r.block_offsets[b]);
-}
-
 template <typename TIn, bool kBwd>
 __global__ void __launch_bounds__(128) combine_kernel(int64_t T, int d, int k, RouteView r,
                                                       const TIn* __restrict__ part,

@@ -12,6 +12,8 @@ constexpr int kTileM = SPT_TILE_M;   // bucket tile height (rows of a grouped-GE
 constexpr int kRouteChunk = 256;     // tokens per bucketing chunk (one CTA)
 constexpr int kMaxBlocks = 256;      // G limit (routing keeps 8 logits per lane)
 
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
 // Problem geometry derived from spt_ffn_desc.
 struct Geom {
   int64_t T;
@@ -108,18 +110,76 @@ cudaError_t launch_balance_simt_dwr(const Geom& g, const float* lbg, const void*
 cudaError_t launch_balance_simt_dx(const Geom& g, const float* lbg, const void* w_r, void* dx,
                                    cudaStream_t s);
 
+// LoRA-wrapped routed FFN (lora.cu).  The LoRA terms of fc1
+// enter FWD1 as extra K columns: X_aug = [x | hi(u) | lo(u) | 0] against
+// W1_aug = [w1 | C_I^T | C_I^T | 0] with u = x B_I split into two bf16 halves
+// (z = x W_I + u C_I with u carried to ~16 bits, so a ReLU sign decision sees
+// the same z as the plain path); those of fc2 enter dA the same way
+// (dY_aug = [dy | hi(v) | lo(v) | 0], W2_aug = [w2 | B_O | B_O | 0], v = dy C_O^T).
+constexpr int kLoraK = 64;  // max m' r (width of the per-pair projection rows)
+// augmented K columns: one 64-wide stage when the hi|lo halves fit, else two
+inline int lora_ka(int mp, int r) { return 2 * mp * r <= 64 ? 64 : 128; }
+struct LoraArgs {
+  int r;                              // rank
+  int ka;                             // augmented K columns (lora_ka)
+  const void *b1, *c1, *b2, *c2;      // factors (bf16): [m',r,d], [m',D,r], [D,r], [r,d]
+  float *db1, *dc1, *db2, *dc2;       // factor gradients (fp32, same shapes)
+  bool accumulate;                    // gradients += instead of =
+  // workspace
+  void* xaug;    // [T, d+ka] bf16: fwd X_aug, bwd dY_aug
+  void* waug;    // [m'D, d+ka] bf16: fwd W1_aug, bwd W2_aug
+  float* uv;     // [T, m'r] f32: fwd U = x B_I, bwd V = dy C_O^T ([T, r])
+  float* rowp;   // [rows_cap, 64] f32 per pair: fwd q rows (h~ B_O[b]), bwd du rows (dZ C_I[b])
+  float* gpart;  // [tiles, m'+1, bw, r] f32 per-tile partials of dC_I (m' slabs) and dB_O
+  float* spart;  // split-K partials of dB_I / dC_O
+  int n_split_u, n_split_v;
+  void* dhl;     // [2, T, upad] bf16 (hi, lo) dU rows for the dB_I GEMM
+  // stash
+  float* ust;    // [T, m'r] f32: u = x B_I (for dC_I)
+  void* qhl;     // [2, T, qpad] bf16 (hi, lo) q = sum_b h~ B_O[b] for the dC_O GEMM
+};
+inline int lora_upad(const Geom& g, int r) { return (int)ceil_div(g.mp * r, 16) * 16; }
+inline int lora_qpad(int r) { return (int)ceil_div(r, 16) * 16; }
+
+cudaError_t lora_fwd_prep(const Geom& g, const void* x, const void* w1, const LoraArgs& lo,
+                          cudaStream_t s);
+cudaError_t lora_fwd_finish(const Geom& g, const RouteView& r, const Bufs& b, const LoraArgs& lo,
+                            void* y, cudaStream_t s);
+cudaError_t lora_bwd_prep(const Geom& g, const void* dy, const void* w2, const LoraArgs& lo,
+                          cudaStream_t s);
+cudaError_t lora_bwd_grads(const Geom& g, const RouteView& r, const Bufs& b, const LoraArgs& lo,
+                           cudaStream_t s);
+// dx = sum_j dXp rows + router term (dense [T,d] if `dense`, else sum_j dlogit w_r[b_j]
+// when w_r) + dU B_I^T; then dB_I = dU^T x and dC_O = q^T dy (tcgen05 split-K GEMMs)
+cudaError_t lora_bwd_finish(const Geom& g, const RouteView& r, const Bufs& b, const LoraArgs& lo,
+                            const void* x, const void* dy, const void* dense, const void* w_r,
+                            void* dx, cudaStream_t s);
+
 // tcgen05 path (tc_ffn.cu), bf16 only
 bool tc_supported(const Geom& g);
 cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logits,
                       cudaStream_t s);
+// dense split-K  out[G, d] (=|+=) A^T B  with A given as bf16 hi|lo halves [2, T, gpad]
+// and B [T, d] bf16 (the dW_R GEMM; also dB_I / dC_O of the LoRA path)
+cudaError_t tc_dense_tn(const Geom& g, const void* ahl, const void* bmat, float* part, int n_split,
+                        float* out, bool accumulate, cudaStream_t s);
+int dense_tn_splits(const Geom& g);
+// lo != NULL: the LoRA-wrapped FFN (FWD1 on X_aug / W1_aug; dA on dY_aug / W2_aug;
+// no dW1 / dW2 -- W is frozen -- and the LoRA factor gradients instead)
 cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void* w2,
-                       const RouteView& r, void* y, const Bufs& b, cudaStream_t s);
+                       const RouteView& r, void* y, const Bufs& b, cudaStream_t s,
+                       const LoraArgs* lo = nullptr);
 cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void* w2,
                         const void* w_r, const RouteView& r, const void* dy, void* dx, float* dw1,
                         float* dw2, float* dw_r, float* dgate_out, bool accumulate, const Bufs& b,
-                        cudaEvent_t dw_ev, cudaStream_t s);
+                        cudaEvent_t dw_ev, cudaStream_t s, const LoraArgs* lo = nullptr);
 
-// device helpers shared by kernels
-__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// padded bucket row of pair (t, b = topk_idx[t,j]):
+// tile_offsets[b]*128 + pair_slot[t*k+j] - block_offsets[b]
+__device__ __forceinline__ int64_t pair_row(const RouteView& r, int64_t t, int k, int j) {
+  const int b = r.topk_idx[t * k + j];
+  return (int64_t)r.tile_offsets[b] * kTileM + (r.pair_slot[t * k + j] - r.block_offsets[b]);
+}
 
 }  // namespace spt

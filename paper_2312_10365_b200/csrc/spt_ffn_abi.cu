@@ -1,5 +1,6 @@
 // spt_ffn_abi.cu -- the C ABI of include/spt_ffn.h: validation, workspace
 // carving and dispatch to the sm_100a kernels.  Host code only.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -86,13 +87,7 @@ static spt_status make_geom(const spt_ffn_desc* d, Geom* g) {
   return SPT_OK;
 }
 
-static int dwr_splits(const Geom& g) {
-  const int tiles = (int)(ceil_div(g.G, 128) * ceil_div(g.d, 256));
-  int s = (int)ceil_div(148, tiles);
-  const int max_s = (int)ceil_div(g.T, 64);
-  if (s > max_s) s = max_s;
-  return s < 1 ? 1 : s;
-}
+static int dwr_splits(const Geom& g) { return dense_tn_splits(g); }
 
 struct Sizes {
   size_t z, h, stash;
@@ -153,6 +148,78 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
   b.lb_x = s.lbx ? (void*)w : nullptr; w += s.lbx;
   return b;
 }
+
+// LoRA-wrapped calls (ABI 3): the plain stash / workspace followed by the LoRA
+// buffers (LoraArgs in internal.h).
+struct LoraSizes {
+  size_t ust, qhl, stash;                              // stash extras
+  size_t xaug, waug, uv, rowp, gpart, spart, dhl, ws;  // workspace extras
+  int n_split_u, n_split_v;
+};
+
+static spt_status lora_geom(const spt_ffn_desc* d, int32_t rank, Geom* g) {
+  spt_status st = make_geom(d, g);
+  if (st != SPT_OK) return st;
+  if (rank < 1) return SPT_ERR_INVALID_ARGUMENT;
+  if (g->dtype != SPT_BF16) return SPT_ERR_UNSUPPORTED;  // tcgen05 path only
+  if ((int64_t)g->mp * rank > kLoraK) return SPT_ERR_UNSUPPORTED;
+  return SPT_OK;
+}
+
+static Geom skinny_geom(const Geom& g, int n) {
+  Geom h = g;
+  h.G = n;
+  h.gpad = (int)ceil_div(n, 16) * 16;
+  return h;
+}
+
+static LoraSizes lora_sizes(const Geom& g, int r) {
+  LoraSizes s{};
+  const int64_t tiles = ceil_div(g.pairs, kTileM) + g.G;
+  s.ust = align256((size_t)g.T * g.mp * r * 4);
+  s.qhl = align256((size_t)2 * g.T * lora_qpad(r) * 2);
+  s.stash = s.ust + s.qhl;
+  const int ka = lora_ka(g.mp, r);
+  s.xaug = align256((size_t)g.T * (g.d + ka) * 2);
+  s.waug = align256((size_t)g.mp * g.D * (g.d + ka) * 2);
+  s.uv = align256((size_t)g.T * g.mp * r * 4);
+  s.rowp = align256((size_t)g.rows_cap * kLoraK * 4);
+  s.gpart = align256((size_t)tiles * (g.mp + 1) * g.bw * r * 4);
+  s.n_split_u = dense_tn_splits(skinny_geom(g, g.mp * r));
+  s.n_split_v = dense_tn_splits(skinny_geom(g, r));
+  s.spart = align256((size_t)std::max(s.n_split_u * g.mp * r, s.n_split_v * r) * g.d * 4);
+  s.dhl = align256((size_t)2 * g.T * lora_upad(g, r) * 2);
+  s.ws = s.xaug + s.waug + s.uv + s.rowp + s.gpart + s.spart + s.dhl;
+  return s;
+}
+
+static LoraArgs lora_carve(const Geom& g, const spt_lora* lr, void* stash, void* ws) {
+  const Sizes ps = compute_sizes(g);
+  const LoraSizes s = lora_sizes(g, lr->rank);
+  LoraArgs a{};
+  a.r = lr->rank;
+  a.ka = lora_ka(g.mp, lr->rank);
+  a.b1 = lr->b1;
+  a.c1 = lr->c1;
+  a.b2 = lr->b2;
+  a.c2 = lr->c2;
+  uint8_t* p = (uint8_t*)stash + ps.stash;
+  a.ust = (float*)p; p += s.ust;
+  a.qhl = p;
+  uint8_t* w = (uint8_t*)ws + ps.ws;
+  a.xaug = w; w += s.xaug;
+  a.waug = w; w += s.waug;
+  a.uv = (float*)w; w += s.uv;
+  a.rowp = (float*)w; w += s.rowp;
+  a.gpart = (float*)w; w += s.gpart;
+  a.spart = (float*)w; w += s.spart;
+  a.dhl = w;
+  a.n_split_u = s.n_split_u;
+  a.n_split_v = s.n_split_v;
+  return a;
+}
+
+static bool lora_complete(const spt_lora* l) { return l && l->b1 && l->c1 && l->b2 && l->c2; }
 
 static RouteView view(const spt_route_buf* r) {
   return RouteView{r->logits,       r->topk_idx,   r->topk_gate, r->block_offsets,
@@ -356,6 +423,86 @@ spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void*
                       : simt_backward(g, x, w1, w2, w_r, rv, dy, dx, dw1, dw2, dw_r, dgate, acc, b,
                                       ev, s);
   return to_status(e);
+}
+
+spt_status spt_ffn_lora_sizes(const spt_ffn_desc* desc, int32_t rank, size_t* stash_bytes,
+                              size_t* workspace_bytes) {
+  if (!stash_bytes || !workspace_bytes) return SPT_ERR_INVALID_ARGUMENT;
+  Geom g;
+  spt_status st = lora_geom(desc, rank, &g);
+  if (st != SPT_OK) return st;
+  const Sizes s = compute_sizes(g);
+  const LoraSizes l = lora_sizes(g, rank);
+  *stash_bytes = s.stash + l.stash;
+  *workspace_bytes = s.ws + l.ws;
+  return SPT_OK;
+}
+
+spt_status spt_ffn_lora_forward(const spt_ffn_desc* desc, const void* x, const void* w1,
+                                const void* w2, const spt_lora* lora, const spt_route_buf* r,
+                                void* y, void* stash, void* ws, size_t ws_bytes, void* stream) {
+  if (!lora) return SPT_ERR_INVALID_ARGUMENT;
+  Geom g;
+  spt_status st = lora_geom(desc, lora->rank, &g);
+  if (st != SPT_OK) return st;
+  if (!tok_ok(x, g.T) || !w1 || !w2 || !lora_complete(lora) || !route_complete(r, g.T) ||
+      !tok_ok(y, g.T) || !stash || !ws)
+    return SPT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < compute_sizes(g).ws + lora_sizes(g, lora->rank).ws)
+    return SPT_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = device_ok()) != SPT_OK) return st;
+  if (g.T == 0) return SPT_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  Bufs b = carve(g, stash, ws);
+  LoraArgs la = lora_carve(g, lora, stash, ws);
+  return to_status(tc_forward(g, x, w1, w2, view(r), y, b, s, &la));
+}
+
+spt_status spt_ffn_lora_backward(const spt_ffn_desc* desc, const void* x, const void* w1,
+                                 const void* w2, const void* w_r, const spt_lora* lora,
+                                 const spt_route_buf* r, const void* stash, const void* dy,
+                                 void* dx, const spt_lora_grads* grads, float* dw_r, float* dgate,
+                                 unsigned flags, void* ws, size_t ws_bytes, void* grad_event,
+                                 void* stream) {
+  if (!lora || !grads) return SPT_ERR_INVALID_ARGUMENT;
+  Geom g;
+  spt_status st = lora_geom(desc, lora->rank, &g);
+  if (st != SPT_OK) return st;
+  if (!tok_ok(x, g.T) || !w1 || !w2 || !w_r || !lora_complete(lora) || !route_complete(r, g.T) ||
+      !stash || !tok_ok(dy, g.T) || !tok_ok(dx, g.T) || !grads->db1 || !grads->dc1 ||
+      !grads->db2 || !grads->dc2 || !dw_r || !ws)
+    return SPT_ERR_INVALID_ARGUMENT;
+  if (ws_bytes < compute_sizes(g).ws + lora_sizes(g, lora->rank).ws)
+    return SPT_ERR_WORKSPACE_TOO_SMALL;
+  if ((st = device_ok()) != SPT_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool acc = flags & SPT_BWD_ACCUMULATE_DW;
+  const int rk = lora->rank;
+  if (g.T == 0) {  // no tokens: zero gradients (unless accumulating)
+    if (!acc) {
+      const size_t n1 = (size_t)g.mp * rk * g.d * 4, n2 = (size_t)g.mp * g.D * rk * 4,
+                   n3 = (size_t)g.D * rk * 4, n4 = (size_t)rk * g.d * 4,
+                   n5 = (size_t)g.G * g.d * 4;
+      if (cudaMemsetAsync(grads->db1, 0, n1, s) != cudaSuccess ||
+          cudaMemsetAsync(grads->dc1, 0, n2, s) != cudaSuccess ||
+          cudaMemsetAsync(grads->db2, 0, n3, s) != cudaSuccess ||
+          cudaMemsetAsync(grads->dc2, 0, n4, s) != cudaSuccess ||
+          cudaMemsetAsync(dw_r, 0, n5, s) != cudaSuccess)
+        return SPT_ERR_CUDA;
+    }
+    if (grad_event && cudaEventRecord((cudaEvent_t)grad_event, s) != cudaSuccess)
+      return SPT_ERR_CUDA;
+    return SPT_OK;
+  }
+  Bufs b = carve(g, const_cast<void*>(stash), ws);
+  LoraArgs la = lora_carve(g, lora, const_cast<void*>(stash), ws);
+  la.db1 = grads->db1;
+  la.dc1 = grads->dc1;
+  la.db2 = grads->db2;
+  la.dc2 = grads->dc2;
+  la.accumulate = acc;
+  return to_status(tc_backward(g, x, w1, w2, w_r, view(r), dy, dx, nullptr, nullptr, dw_r, dgate,
+                               acc, b, (cudaEvent_t)grad_event, s, &la));
 }
 
 #pragma GCC visibility pop

@@ -1829,11 +1829,21 @@ static int units_upper(const Geom& g) {
 }
 
 cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void* w2,
-                       const RouteView& r, void* y, const Bufs& b, cudaStream_t s) {
+                       const RouteView& r, void* y, const Bufs& b, cudaStream_t s,
+                       const LoraArgs* lo) {
   const int up = bucket_tiles_upper(g);
   cudaError_t e0 = build_schedules(g, r, b, s);
   if (e0 != cudaSuccess) return e0;
   {
+    // LoRA: FWD1 runs on X_aug / W1_aug (K = d + 64: the u C_I term is one more K stage)
+    Geom g1 = g;
+    if (lo) {
+      if ((e0 = lora_fwd_prep(g, x, w1, *lo, s)) != cudaSuccess) return e0;
+      g1.d = g.d + lo->ka;
+      x = lo->xaug;
+      w1 = lo->waug;
+    }
+    const Geom& g = g1;  // the FWD1 geometry
     TcArgs a{};
     base_args(a, g, r);
     a.tile_list = b.tile_list;
@@ -1876,6 +1886,7 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
       TRY(launch_bres<K_FWD2>(a, units_upper(g), s));
     }
   }
+  if (lo) return lora_fwd_finish(g, r, b, *lo, y, s);
   return launch_combine_fwd(g, r, b.part, y, s);
 }
 
@@ -2020,10 +2031,38 @@ __global__ void __launch_bounds__(256) dgate_reduce_kernel(int64_t T, int G, int
   rows_g[prow] = dlogit;
 }
 
+int dense_tn_splits(const Geom& g) {
+  const int tiles = (int)(ceil_div(g.G, 128) * ceil_div(g.d, 256));
+  int s = (int)ceil_div(148, tiles);
+  const int max_s = (int)ceil_div(g.T, 64);
+  if (s > max_s) s = max_s;
+  return s < 1 ? 1 : s;
+}
+
+cudaError_t tc_dense_tn(const Geom& g, const void* ahl, const void* bmat, float* part, int n_split,
+                        float* out, bool accumulate, cudaStream_t s) {
+  TcArgs a{};
+  base_args(a, g, RouteView{});
+  bool ok = make_tmap_bf16_2d(&a.ta, ahl, (uint64_t)2 * g.T, g.gpad, g.gpad, 64, 64) &&
+            make_tmap_bf16_2d(&a.tb, bmat, g.T, g.d, g.d, 64, 64);
+  a.BN = 256;
+  a.n_split = n_split;
+  a.ksplit = (int)(ceil_div(ceil_div(g.T, n_split), 64) * 64);
+  a.out = part;
+  TRY(launch<K_DWR>(a, a.NT * a.n_split, s));
+  const int64_t n = (int64_t)g.G * g.d;
+  prof_begin("dwr_reduce", s);
+  dwr_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n_split, n, part, out,
+                                                               accumulate ? 1 : 0);
+  prof_end(s);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void* w2,
                         const void* w_r, const RouteView& r, const void* dy, void* dx, float* dw1,
                         float* dw2, float* dw_r, float* dgate_out, bool accumulate, const Bufs& b,
-                        cudaEvent_t dw_ev, cudaStream_t s) {
+                        cudaEvent_t dw_ev, cudaStream_t s, const LoraArgs* lo) {
   const int up = bucket_tiles_upper(g);
   const bool sig = g.gate == SPT_GATE_SIGMOID;
   const bool lb = g.lbw != 0.f;  // load-balancing loss: dense router gradient (every block)
@@ -2031,15 +2070,25 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   if (e0 != cudaSuccess) return e0;
   if ((sig || lb) && cudaMemsetAsync(b.dlg, 0, (size_t)2 * g.T * g.gpad * 2, s) != cudaSuccess)
     return cudaErrorUnknown;
+  // LoRA: dA runs on dY_aug / W2_aug (K = d + 64: the (dy C_O^T) B_O^T term)
+  Geom gda = g;
+  const void* dy_da = dy;
+  const void* w2_da = w2;
+  if (lo) {
+    if ((e0 = lora_bwd_prep(g, dy, w2, *lo, s)) != cudaSuccess) return e0;
+    gda.d = g.d + lo->ka;
+    dy_da = lo->xaug;
+    w2_da = lo->waug;
+  }
   if (!use_fused_da() && g.bw <= 128) {  // a7: dA^T = W2_b dY[bucket]^T (tokens on N), then dgate/dZ
     TcArgs a{};
-    base_args(a, g, r);
-    bool ok = make_tmap_bf16_2d(&a.ta, dy, g.T, g.d, g.d, 64, 1) &&
-              make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, 128) &&
+    base_args(a, gda, r);
+    bool ok = make_tmap_bf16_2d(&a.ta, dy_da, g.T, gda.d, gda.d, 64, 1) &&
+              make_tmap_bf16_2d(&a.tb, w2_da, g.D, gda.d, gda.d, 64, 128) &&
               make_tmap_f32_2d(&a.tc, b.da, g.rows_cap, g.bw, g.bw, 32, 32);
     a.BN = 256;
     a.MH = 1;
-    a.aux2 = dy;
+    a.aux2 = dy_da;
     a.tile_list = b.tile_list;
     a.unit_offsets = b.unit_offsets;
     TRY(launch<K_DAT>(a, up / 2 + g.G, s));
@@ -2051,15 +2100,15 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     count_launch();
   } else {  // a7 fused variant: dA = dY[bucket] W2_b^T with the dgate / dZ / dlogit epilogue
     TcArgs a{};
-    base_args(a, g, r);
+    base_args(a, gda, r);
     // wide blocks (bw > 256): tiles of 256 units (N = 256: the CTA-pair
     // kernel); dgate partials per tile
     a.bn_u = g.bw > 256 ? 256 : g.bw;
     a.nu = (int)ceil_div(g.bw, a.bn_u);
     a.dgp = b.da;  // [rows_cap][nu] fits the [rows_cap][bw] f32 scratch
-    bool ok = make_tmap_bf16_2d(&a.ta, dy, g.T, g.d, g.d, 64, 1) &&
-              make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, a.bn_u) &&
-              make_tmap_bf16_2d(&a.tc, dy, g.T, g.d, g.d, 256, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    bool ok = make_tmap_bf16_2d(&a.ta, dy_da, g.T, gda.d, gda.d, 64, 1) &&
+              make_tmap_bf16_2d(&a.tb, w2_da, g.D, gda.d, gda.d, 64, a.bn_u) &&
+              make_tmap_bf16_2d(&a.tc, dy_da, g.T, gda.d, gda.d, 256, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                 CU_TENSOR_MAP_SWIZZLE_NONE);  // L2 prefetch rows
     a.BN = a.bn_u;
     a.aux = b.z;
@@ -2069,11 +2118,11 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.dlg = b.dlg;
     a.tile_list = b.tile_list;
     a.MH = 2;
-    a.aux2 = dy;
+    a.aux2 = dy_da;
     a.unit_offsets = b.unit_offsets;
     const int tiles = (up / 2 + g.G) * a.nu;
     if (use_pair_gather() && pair_gather_ok(a.BN)) {
-      ok = ok && make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, a.BN / 2);
+      ok = ok && make_tmap_bf16_2d(&a.tb, w2_da, g.D, gda.d, gda.d, 64, a.BN / 2);
       TRY(launch_pair_gather<K_DA>(a, tiles, s));
     } else {
       TRY(launch<K_DA>(a, tiles, s));
@@ -2089,7 +2138,10 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       if (e != cudaSuccess) return e;
     }
   }
-  {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features: <= 2 halves, or 256-feature tiles)
+  if (lo) {  // W frozen: the LoRA factor gradients dC_I, dB_O from dZ, h~ (no dW1 / dW2)
+    if ((e0 = lora_bwd_grads(g, r, b, *lo, s)) != cudaSuccess) return e0;
+  }
+  if (!lo) {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features: <= 2 halves, or 256-feature tiles)
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
@@ -2103,7 +2155,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.acc_mode = accumulate;
     TRY(launch<K_DW1>(a, g.G * a.nu * a.NT, s));
   }
-  {  // a9: dW2_b = H~_b^T dY[bucket_b]
+  if (!lo) {  // a9: dW2_b = H~_b^T dY[bucket_b]
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, kind_bk(K_DW2)) &&
@@ -2123,21 +2175,8 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   }
   // a10: dW_R = dLogits^T X  (split-K, hi + lo bf16 halves of dlogit)
   if (sig || lb) {
-    TcArgs a{};
-    base_args(a, g, r);
-    bool ok = make_tmap_bf16_2d(&a.ta, b.dlg, (uint64_t)2 * g.T, g.gpad, g.gpad, 64, 64) &&
-              make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 64);
-    a.BN = 256;
-    a.n_split = b.n_split;
-    a.ksplit = (int)(ceil_div(ceil_div(g.T, b.n_split), 64) * 64);
-    a.out = b.dwr_part;
-    TRY(launch<K_DWR>(a, a.NT * a.n_split, s));
-    const int64_t n = (int64_t)g.G * g.d;
-    prof_begin("dwr_reduce", s);
-    dwr_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(b.n_split, n, b.dwr_part, dw_r,
-                                                                 accumulate ? 1 : 0);
-    prof_end(s);
-    count_launch();
+    cudaError_t e = tc_dense_tn(g, b.dlg, x, b.dwr_part, b.n_split, dw_r, accumulate, s);
+    if (e != cudaSuccess) return e;
   } else if (!accumulate) {
     if (cudaMemsetAsync(dw_r, 0, (size_t)g.G * g.d * 4, s) != cudaSuccess) return cudaErrorUnknown;
   }
@@ -2145,7 +2184,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   // gradient all-reduce at this event while dX is computed below
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
+  if (!lo && dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
   {  // a8: dXp = dZ W1_b, then combine with the router term
     TcArgs a{};
     base_args(a, g, r);
@@ -2172,11 +2211,15 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.BN = 256;
     a.out = b.lb_x;
     TRY(launch<K_DXR>(a, (int)ceil_div(g.T, 128) * a.NT, s));
-    e = launch_combine_bwd_dense(g, r, b.part, b.lb_x, dx, s);
+    e = lo ? lora_bwd_finish(g, r, b, *lo, x, dy, b.lb_x, nullptr, dx, s)
+           : launch_combine_bwd_dense(g, r, b.part, b.lb_x, dx, s);
   } else {
-    e = launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
+    e = lo ? lora_bwd_finish(g, r, b, *lo, x, dy, nullptr, w_r, dx, s)
+           : launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
   }
   if (e != cudaSuccess) return e;
+  // LoRA: every gradient (dw_r and the factors) is final only here
+  if (lo && dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (dgate_out) return launch_gather_dgate(g, r, b.dgate, dgate_out, s);
   return cudaSuccess;

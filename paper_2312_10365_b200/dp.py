@@ -42,7 +42,14 @@ class FlatGrads:
 
 
 def attach_flat_grads(ffn, device="cuda") -> FlatGrads:
-    """Re-point a RoutedFFN's dw1/dw2/dw_r at views of one flat buffer."""
+    """Re-point a RoutedFFN's dw1/dw2/dw_r (a RoutedLoRAFFN's LoRA factor
+    gradients db1/dc1/db2/dc2 and dw_r: W is frozen) at views of one flat buffer."""
+    if hasattr(ffn, "grads"):  # LoRA-wrapped: the trained tensors only
+        fg = FlatGrads({**{n: tuple(g.shape) for n, g in ffn.grads.items()},
+                        "dw_r": tuple(ffn.dw_r.shape)}, device)
+        ffn.grads = {n: fg[n] for n in ffn.grads}
+        ffn.dw_r = fg["dw_r"]
+        return fg
     fg = FlatGrads({"dw1": tuple(ffn.dw1.shape), "dw2": tuple(ffn.dw2.shape),
                     "dw_r": tuple(ffn.dw_r.shape)}, device)
     ffn.dw1, ffn.dw2, ffn.dw_r = fg["dw1"], fg["dw2"], fg["dw_r"]

@@ -106,6 +106,43 @@ def spt_ffn_backward(desc, x, w1, w2, w_r, route: RouteBuffers, stash, dy, dx, d
         _stream(stream)))
 
 
+def spt_ffn_lora_sizes(desc: L.spt_ffn_desc, rank: int) -> tuple[int, int]:
+    """(stash_bytes, workspace_bytes) of the LoRA-wrapped calls (ABI 3)."""
+    s, w = ctypes.c_size_t(), ctypes.c_size_t()
+    L.check("spt_ffn_lora_sizes", L.lib().spt_ffn_lora_sizes(ctypes.byref(desc), int(rank),
+                                                              ctypes.byref(s), ctypes.byref(w)))
+    return s.value, w.value
+
+
+def _lora_c(rank, b1, c1, b2, c2) -> L.spt_lora:
+    return L.spt_lora(int(rank), *[_p(t) for t in (b1, c1, b2, c2)])
+
+
+def spt_ffn_lora_forward(desc, x, w1, w2, lora: dict, route: RouteBuffers, y, stash, ws, stream=None):
+    """LoRA-wrapped routed forward (include/spt_ffn.h; PAPER.md:159 on fc1/fc2).
+    lora: {"b1", "c1", "b2", "c2"} device tensors; the rank is c2.shape[0]."""
+    rb = route.as_c()
+    lc = _lora_c(lora["c2"].shape[0], lora["b1"], lora["c1"], lora["b2"], lora["c2"])
+    L.check("spt_ffn_lora_forward", L.lib().spt_ffn_lora_forward(
+        ctypes.byref(desc), _p(x), _p(w1), _p(w2), ctypes.byref(lc), ctypes.byref(rb), _p(y),
+        _p(stash), _p(ws), ws.numel() * ws.element_size(), _stream(stream)))
+
+
+def spt_ffn_lora_backward(desc, x, w1, w2, w_r, lora: dict, route: RouteBuffers, stash, dy, dx,
+                          grads: dict, dw_r, ws, dgate=None, flags: int = 0, stream=None,
+                          grad_event=None):
+    """Backward of spt_ffn_lora_forward (W frozen): dx, grads {"db1", "dc1", "db2",
+    "dc2"} (fp32), dw_r; grad_event recorded once every gradient is final."""
+    rb = route.as_c()
+    lc = _lora_c(lora["c2"].shape[0], lora["b1"], lora["c1"], lora["b2"], lora["c2"])
+    gc = L.spt_lora_grads(*[_p(grads[n]) for n in ("db1", "dc1", "db2", "dc2")])
+    ev = None if grad_event is None else ctypes.c_void_p(grad_event.cuda_event)
+    L.check("spt_ffn_lora_backward", L.lib().spt_ffn_lora_backward(
+        ctypes.byref(desc), _p(x), _p(w1), _p(w2), _p(w_r), ctypes.byref(lc), ctypes.byref(rb),
+        _p(stash), _p(dy), _p(dx), ctypes.byref(gc), _p(dw_r), _p(dgate), flags, _p(ws),
+        ws.numel() * ws.element_size(), ev, _stream(stream)))
+
+
 def spt_status_string(code: int) -> str:
     return L.status_string(code)
 
@@ -172,3 +209,40 @@ class RoutedFFN:
                          self.dw2, self.dw_r, self.ws, self.dgate if want_dgate else None, flags, stream,
                          dw_event)
         return self.dx, self.dw1, self.dw2, self.dw_r
+
+
+class RoutedLoRAFFN(RoutedFFN):
+    """Buffers for the LoRA-wrapped routed FFN (ABI 3): W_I, W_O
+    frozen, rank-``rank`` factors of both projections trained."""
+
+    def __init__(self, T, d, D, G, k, dtype, act, rank, gate=L.SPT_GATE_SIGMOID, device="cuda",
+                 balance_weight=0.0):
+        self.desc = make_desc(T, d, D, G, k, dtype, act, gate, balance_weight)
+        self.T, self.d, self.D, self.G, self.k, self.rank = T, d, D, G, k, rank
+        self.dtype, self.act, self.gate = dtype, act, gate
+        self.mp = 2 if act == L.SPT_ACT_SWIGLU else 1
+        stash_b, ws_b = spt_ffn_lora_sizes(self.desc, rank)
+        self.stash = torch.empty(max(stash_b, 16), dtype=torch.uint8, device=device)
+        self.ws = torch.empty(max(ws_b, 16), dtype=torch.uint8, device=device)
+        self.route_buf = RouteBuffers.empty(T, G, k, device)
+        self.y = torch.empty(T, d, dtype=dtype, device=device)
+        self.dx = torch.empty(T, d, dtype=dtype, device=device)
+        lead = (2,) if self.mp == 2 else ()
+        f = dict(dtype=torch.float32, device=device)
+        self.grads = {"db1": torch.empty(lead + (rank, d), **f), "dc1": torch.empty(lead + (D, rank), **f),
+                      "db2": torch.empty(D, rank, **f), "dc2": torch.empty(rank, d, **f)}
+        self.dw_r = torch.empty(G, d, **f)
+        self.dgate = torch.empty(T, k, **f)
+        self.loss_lb = torch.zeros(1, **f)
+
+    def forward(self, x, w1, w2, lora, stream=None):
+        spt_ffn_lora_forward(self.desc, x, w1, w2, lora, self.route_buf, self.y, self.stash, self.ws,
+                             stream)
+        return self.y
+
+    def backward(self, x, w1, w2, w_r, lora, dy, flags=0, want_dgate=False, stream=None,
+                 grad_event=None):
+        spt_ffn_lora_backward(self.desc, x, w1, w2, w_r, lora, self.route_buf, self.stash, dy, self.dx,
+                              self.grads, self.dw_r, self.ws, self.dgate if want_dgate else None, flags,
+                              stream, grad_event)
+        return self.dx, self.grads, self.dw_r

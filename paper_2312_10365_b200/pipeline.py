@@ -16,8 +16,9 @@ from .ffn import RoutedFFN
 
 
 class HostStepPipeline:
-    def __init__(self, ffn: RoutedFFN, w1, w2, w_r, grad_hook=None):
+    def __init__(self, ffn: RoutedFFN, w1, w2, w_r, grad_hook=None, lora=None):
         self.ffn, self.w1, self.w2, self.w_r = ffn, w1, w2, w_r
+        self.lora = lora  # LoRA factors of a RoutedLoRAFFN, else None
         self.grad_hook = grad_hook  # called on the compute stream after backward (e.g. all-reduce)
         T, d, dt = ffn.T, ffn.d, ffn.dtype
         dev = w1.device
@@ -50,8 +51,13 @@ class HostStepPipeline:
                 self.s_comp.wait_event(self.d2h_done[b])      # step i-2's y[b], dx[b] copied out
             f.y, f.dx = self.y[b], self.dx[b]
             f.route(self.x[b], self.w_r, stream=self.s_comp)
-            f.forward(self.x[b], self.w1, self.w2, stream=self.s_comp)
-            f.backward(self.x[b], self.w1, self.w2, self.w_r, self.dy[b], stream=self.s_comp)
+            if self.lora is None:
+                f.forward(self.x[b], self.w1, self.w2, stream=self.s_comp)
+                f.backward(self.x[b], self.w1, self.w2, self.w_r, self.dy[b], stream=self.s_comp)
+            else:
+                f.forward(self.x[b], self.w1, self.w2, self.lora, stream=self.s_comp)
+                f.backward(self.x[b], self.w1, self.w2, self.w_r, self.lora, self.dy[b],
+                           stream=self.s_comp)
             if self.grad_hook is not None:
                 self.grad_hook()
             self.comp_done[b].record(self.s_comp)

@@ -22,7 +22,7 @@ def test_library_exports_every_declared_symbol():
     assert set(decl) == set(_lib.EXPORTED), decl
     for name in decl:
         assert hasattr(L, name), name
-    assert L.spt_ffn_abi_version() == 2
+    assert L.spt_ffn_abi_version() == 3
 
 
 def test_status_strings():
@@ -107,3 +107,49 @@ def test_desc_layout_and_balance_weight_validation():
         _, w0 = spt_ffn_sizes(_desc(dtype=dt))
         _, w1 = spt_ffn_sizes(_desc(dtype=dt, balance_weight=0.01))
         assert w1 - w0 == extra, (dt, w1 - w0)
+
+
+# ------------------------------------------------------------ LoRA (ABI 3)
+def test_lora_sizes_extend_plain_sizes():
+    import torch
+    from paper_2312_10365_b200 import spt_ffn_lora_sizes, spt_ffn_sizes
+    d = _desc(dtype=torch.bfloat16, d=256, D=1024, G=8, k=2)
+    s, w = spt_ffn_sizes(d)
+    ls, lw = spt_ffn_lora_sizes(d, 16)
+    assert ls > s and lw > w
+    ls2, lw2 = spt_ffn_lora_sizes(d, 32)
+    assert ls2 >= ls and lw2 > lw
+
+
+@pytest.mark.parametrize("kw,rank,code", [
+    (dict(), 16, 2),                                    # fp32: tcgen05 path only
+    (dict(dtype="bf16"), 0, 1),                         # rank < 1
+    (dict(dtype="bf16"), 65, 2),                        # m' r > 64
+    (dict(dtype="bf16", act=2, D=1024, G=8), 33, 2),    # SwiGLU: 2 r > 64
+    (dict(dtype="bf16", k=9), 16, 1),                   # bad descriptor
+])
+def test_lora_invalid_arguments(kw, rank, code):
+    import torch
+    from paper_2312_10365_b200 import _lib, spt_ffn_lora_sizes
+    if kw.get("dtype") == "bf16":
+        kw = dict(kw, dtype=torch.bfloat16)
+    with pytest.raises(_lib.SptError) as e:
+        spt_ffn_lora_sizes(_desc(**kw), rank)
+    assert e.value.code == code
+
+
+def test_lora_null_pointers_rejected_before_any_launch():
+    import torch
+    from paper_2312_10365_b200 import _lib
+    L = _lib.lib()
+    d = _desc(dtype=torch.bfloat16)
+    rb = _lib.spt_route_buf()
+    lo = _lib.spt_lora(16, None, None, None, None)
+    gr = _lib.spt_lora_grads()
+    assert L.spt_ffn_lora_forward(ctypes.byref(d), None, None, None, ctypes.byref(lo),
+                                  ctypes.byref(rb), None, None, None, 0, None) == 1
+    assert L.spt_ffn_lora_forward(ctypes.byref(d), None, None, None, None, ctypes.byref(rb), None,
+                                  None, None, 0, None) == 1
+    assert L.spt_ffn_lora_backward(ctypes.byref(d), *([None] * 4), ctypes.byref(lo), ctypes.byref(rb),
+                                   None, None, None, ctypes.byref(gr), None, None, 0, None, 0, None,
+                                   None) == 1

@@ -1,0 +1,144 @@
+"""GPU parity of the LoRA-wrapped routed FFN (ABI 3) against
+the fp64 oracle (oracle/lora.py, pinned in test_oracle_lora.py).
+
+Same protocol as test_gpu_ffn.py: seeded synthetic inputs plus seeded LoRA
+factors (synthetic.make_lora), the GPU's own routing (its top-k checked equal to
+the oracle's on the same fp32 logits), infinity-norm relative error <= 2e-2
+(bf16, reading c14) on y, dx, dgate, dw_r and the four factor gradients.  Sizes
+span several 128-row tiles with ragged tails; the BASELINE shapes (d, D, G, k)
+at a few hundred tokens.
+"""
+import numpy as np
+import pytest
+
+import synthetic as S
+from helpers import TOL, relerr, to_dev
+from oracle import lora as OL
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ("y", "dx", "dgate", "dw_r", "db1", "dc1", "db2", "dc2")
+
+
+def gpu_run_lora(cfg, T, inp, lora, rank, balance_weight=0.0, accumulate_from=None):
+    import torch
+    import paper_2312_10365_b200 as P
+    f = P.RoutedLoRAFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, torch.bfloat16, cfg.act, rank, cfg.gate,
+                        balance_weight=balance_weight)
+    x, w1, w2, w_r, dy = (to_dev(inp[n], cfg) for n in ("x", "w1", "w2", "w_r", "dy"))
+    lo = {n: to_dev(v, cfg) for n, v in lora.items()}
+    f.route(x, w_r)
+    y = f.forward(x, w1, w2, lo)
+    out = {"logits": f.route_buf.logits.cpu().numpy(), "topk_idx": f.route_buf.topk_idx.cpu().numpy(),
+           "y": y.float().cpu().numpy()}
+    flags = 0
+    if accumulate_from is not None:
+        for n, v in accumulate_from.items():
+            (f.dw_r if n == "dw_r" else f.grads[n]).copy_(torch.from_numpy(np.ascontiguousarray(v, np.float32)))
+        flags = P.SPT_BWD_ACCUMULATE_DW
+    dx, grads, dw_r = f.backward(x, w1, w2, w_r, lo, dy, flags=flags, want_dgate=True)
+    out.update(dx=dx.float().cpu().numpy(), dw_r=dw_r.cpu().numpy(), dgate=f.dgate.cpu().numpy(),
+               **{n: v.cpu().numpy() for n, v in grads.items()})
+    torch.cuda.synchronize()
+    return out
+
+
+def oracle_lora(orc, cfg, inp, lora, lg, ti, lb_weight=0.0):
+    ref = OL.lora_backward(inp["x"], inp["w1"], inp["w2"], inp["w_r"], lora, lg, ti, inp["dy"],
+                           cfg.act, cfg.gate)
+    ref["y"] = OL.lora_forward(inp["x"], inp["w1"], inp["w2"], lora, lg, ti, cfg.act, cfg.gate)
+    if lb_weight:
+        _, dl = orc.balance(lg, ti)
+        ref["dx"] = ref["dx"] + lb_weight * (dl @ np.asarray(inp["w_r"], np.float64))
+        ref["dw_r"] = ref["dw_r"] + lb_weight * (dl.T @ np.asarray(inp["x"], np.float64))
+    return ref
+
+
+def _parity(orc, cfg, T, rank=16, lb_weight=0.0, names=NAMES):
+    inp = S.make_inputs(cfg, T)
+    lora = S.make_lora(cfg, rank)
+    got = gpu_run_lora(cfg, T, inp, lora, rank, balance_weight=lb_weight)
+    assert np.array_equal(got["topk_idx"], orc.topk(got["logits"], cfg.k))
+    lg = orc.router(inp["x"], inp["w_r"])
+    ref = oracle_lora(orc, cfg, inp, lora, lg, got["topk_idx"], lb_weight)
+    errs = {}
+    for n in names:
+        if n == "dw_r" and cfg.gate == S.GATE_NONE and not lb_weight:
+            assert np.all(got[n] == 0), "GATE_NONE: router gets no gradient"
+            continue
+        errs[n] = relerr(got[n].reshape(np.shape(ref[n])), ref[n])
+    bad = {n: e for n, e in errs.items() if not e <= TOL["bf16"]}
+    assert not bad, f"{cfg.name} r={rank}: {errs}"
+    return got, ref, errs
+
+
+@pytest.mark.parametrize("name,T", [("bert", 700), ("opt", 400), ("llama", 300)])
+def test_lora_configs(orc, name, T):
+    _parity(orc, S.CONFIGS[name], T)
+
+
+@pytest.mark.parametrize("rank", [1, 8, 32])
+def test_lora_ranks(orc, rank):
+    _parity(orc, S.CONFIGS["llama"], 260, rank=rank)          # SwiGLU: m' r up to 64
+
+
+def test_lora_rank64_single_projection(orc):
+    _parity(orc, S.CONFIGS["bert"], 300, rank=64)              # m' = 1: r = 64 fills the K stage
+
+
+def test_lora_gate_none(orc):
+    _parity(orc, S.CONFIGS["opt"].with_(gate=S.GATE_NONE), 257)
+
+
+def test_lora_with_balance_loss(orc):
+    _parity(orc, S.CONFIGS["bert"], 500, lb_weight=0.5)
+
+
+@pytest.mark.parametrize("name,d,D,G,k,act", [
+    ("g8k4", 512, 4096, 8, 4, S.ACT_RELU),          # the paper's G = 8, beta = 1/2 (bw 512)
+    ("wide512sw", 256, 1024, 2, 1, S.ACT_SWIGLU),   # SwiGLU m' bw = 1024
+    ("bw192", 256, 1536, 8, 3, S.ACT_GELU),
+])
+def test_lora_wide_blocks(orc, name, d, D, G, k, act):
+    _parity(orc, S.FfnConfig(name, d, D, G, k, 500, "bf16", act), 500)
+
+
+def test_lora_accumulate(orc):
+    cfg = S.CONFIGS["bert"]
+    T, rank = 300, 16
+    inp = S.make_inputs(cfg, T)
+    lora = S.make_lora(cfg, rank)
+    base = gpu_run_lora(cfg, T, inp, lora, rank)
+    rng = np.random.default_rng(0)
+    prev = {n: rng.standard_normal(base[n].shape).astype(np.float32)
+            for n in ("db1", "dc1", "db2", "dc2", "dw_r")}
+    acc = gpu_run_lora(cfg, T, inp, lora, rank, accumulate_from=prev)
+    for n, p in prev.items():
+        assert relerr(acc[n], base[n] + p) < 1e-6, n
+
+
+def test_lora_empty_batch():
+    import torch
+    import paper_2312_10365_b200 as P
+    cfg = S.CONFIGS["bert"]
+    f = P.RoutedLoRAFFN(0, cfg.d, cfg.D, cfg.G, cfg.k, torch.bfloat16, cfg.act, 16)
+    lora = {n: to_dev(v, cfg) for n, v in S.make_lora(cfg, 16).items()}
+    z = torch.empty(0, cfg.d, dtype=torch.bfloat16, device="cuda")
+    w = {n: to_dev(v, cfg) for n, v in S.make_inputs(cfg, 1, need=("w1", "w2", "w_r")).items()}
+    for g in f.grads.values():
+        g.fill_(7.0)
+    f.route(z, w["w_r"])
+    f.forward(z, w["w1"], w["w2"], lora)
+    _, grads, dw_r = f.backward(z, w["w1"], w["w2"], w["w_r"], lora, z)
+    torch.cuda.synchronize()
+    assert all(float(g.abs().max()) == 0 for g in grads.values()) and float(dw_r.abs().max()) == 0
+
+
+def test_lora_deterministic(orc):
+    cfg = S.CONFIGS["llama"]
+    inp = S.make_inputs(cfg, 200)
+    lora = S.make_lora(cfg, 16)
+    a = gpu_run_lora(cfg, 200, inp, lora, 16)
+    b = gpu_run_lora(cfg, 200, inp, lora, 16)
+    for n in NAMES:
+        assert np.array_equal(a[n], b[n]), n
