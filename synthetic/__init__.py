@@ -89,7 +89,7 @@ PAPER_CONFIGS = {
 ALL_CONFIGS = {**CONFIGS, **PAPER_CONFIGS}
 
 _TENSOR_IDS = {"x": 1, "w1": 2, "w2": 3, "w_r": 4, "dy": 5, "logits": 6,
-               "b1": 7, "c1": 8, "b2": 9, "c2": 10}
+               "b1": 7, "c1": 8, "b2": 9, "c2": 10, "pq": 11}
 
 
 def _stream(seed: int, name: str, extra: int = 0) -> np.random.Generator:
@@ -165,6 +165,64 @@ def make_lora(cfg: FfnConfig, r: int = LORA_RANK) -> dict:
         "b2": round_to_dtype(_stream(s, "b2", r).standard_normal((D, r)) / np.sqrt(k * bw), dt),
         "c2": round_to_dtype(_stream(s, "c2", r).standard_normal((r, d)) * c, dt),
     }
+
+
+# sparse-MHA top-L selection (Alg. 3) on PQ codes.  The paper's
+# PQ: codeword dimension d' = 8 and E = 16 codewords per codebook,
+# so M = head_dim / 8 codebooks (8 for 64-dim heads: BERT-base, OPT-1.3B; 16 for
+# LLaMA-7B's 128-dim heads); L = lambda n with lambda = 1/8 (the
+# paper's "top-L as lambda n").
+@dataclasses.dataclass(frozen=True)
+class ToplConfig:
+    name: str
+    heads: int      # batch x heads: independent (sequence, head) problems
+    n: int          # sequence length (queries = keys)
+    M: int          # codebooks
+    E: int = 16     # codewords per codebook
+    lam: float = 0.125
+    causal: bool = False
+    cfg_index: int = 10
+
+    @property
+    def L(self) -> int:
+        return max(1, int(self.lam * self.n))
+
+    @property
+    def seed(self) -> int:
+        return BASE_SEED + self.cfg_index
+
+    def with_(self, **kw) -> "ToplConfig":
+        return dataclasses.replace(self, **kw)
+
+
+TOPL_CONFIGS = {
+    "topl_tiny": ToplConfig("topl_tiny", 2, 256, 8, cfg_index=10),
+    "topl_bert": ToplConfig("topl_bert", 16 * 12, 512, 8, cfg_index=11),      # batch 16, 12 heads
+    "topl_opt": ToplConfig("topl_opt", 8 * 32, 1024, 8, causal=True, cfg_index=12),
+    "topl_llama": ToplConfig("topl_llama", 8 * 32, 2048, 16, causal=True, cfg_index=13),
+}
+
+
+def make_pq_codes(cfg: "ToplConfig", heads: int | None = None) -> tuple:
+    """Seeded PQ code matrices (queries, keys) [heads, n, M] uint8 in [0, E).
+
+    Real queries / keys are clustered (that is why PQ finds the top-L, PAPER.md:
+    306), so codes are drawn around per-head cluster templates: each token picks
+    one of 8 templates and keeps each codebook's template codeword with
+    probability 0.6, else draws it uniformly -- indicator scores then span 0..M
+    with many ties (the integer-ranking regime of Eq. 3).  No arithmetic of the
+    method is done here (no quantisation, no scoring)."""
+    H = cfg.heads if heads is None else heads
+    g = _stream(cfg.seed, "pq", H)
+    tmpl = g.integers(0, cfg.E, size=(H, 8, cfg.M))
+    out = []
+    for _ in range(2):
+        pick = g.integers(0, 8, size=(H, cfg.n))
+        base = np.take_along_axis(tmpl, pick[:, :, None].repeat(cfg.M, axis=2), axis=1)
+        keep = g.random((H, cfg.n, cfg.M)) < 0.6
+        codes = np.where(keep, base, g.integers(0, cfg.E, size=(H, cfg.n, cfg.M)))
+        out.append(codes.astype(np.uint8))
+    return out[0], out[1]
 
 
 _ROW_CHUNK = 1024
