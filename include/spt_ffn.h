@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SPT_FFN_ABI_VERSION 3
+#define SPT_FFN_ABI_VERSION 4
 /* Height of a bucket tile: tile_offsets counts ceil(n_b / SPT_TILE_M) per block. */
 #define SPT_TILE_M 128
 
@@ -219,6 +219,41 @@ spt_status spt_ffn_lora_backward(const spt_ffn_desc* desc, const void* x, const 
                                  void* dx, const spt_lora_grads* grads, float* dw_r, float* dgate,
                                  unsigned flags, void* ws, size_t ws_bytes, void* grad_event,
                                  void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Sparse-MHA top-L selection (ABI 4): SPT's bucket-sort
+ * top-L over product-quantisation codes (§4.1, §5.1
+ * Algorithm 3).  Each query / key vector is given as its M
+ * codeword ids (one per codebook); similarity is the integer
+ * count of shared codewords, Eq. 3:
+ *   s(q, k) = sum_m I[codes_q[q, m] == codes_k[k, m]]  in {0..M}
+ * and per query Algorithm 3 fills M+1 buckets of capacity L in ascending key
+ * order (a full bucket's slot L-1 is overwritten by each further key, line 7),
+ * then reads buckets from score M down until L keys are collected.  Readings
+ * (DESIGN.md c20-c23): empty buckets are skipped (line 11 as `while`); a
+ * bucket is read for min(#keys, L) slots; causal rows see keys k <= q only and
+ * rows with fewer than L candidates are padded with -1.  The result is the
+ * exact top-L by Eq. 3 (ties: a bucket's first keys, plus its last key when it
+ * overflowed) -- integer, deterministic, bit-exact.
+ * Layout (DEVICE, row-major): codes_q [H, n_q, M] uint8, codes_k [H, n_k, M]
+ * uint8, indices [H, n_q, L] int32 (bucket M's keys first; = the CSR column
+ * indices of Fig. 7 with indptr [0, L, 2L, ...]). */
+typedef struct {
+  int32_t n_heads;     /* H >= 0 independent (sequence, head) problems */
+  int32_t n_q;         /* queries per head >= 0 */
+  int32_t n_k;         /* keys per head >= 0 */
+  int32_t n_codebooks; /* M in [1, 31] (the paper: head_dim / 8) */
+  int32_t top_l;       /* L >= 1 (the paper: lambda n) */
+  int32_t causal;      /* 0 | 1: look-ahead mask applied before bucketing */
+} spt_topl_desc;
+
+/* Top-L key indices of every query.  SPT_ERR_INVALID_ARGUMENT: NULL desc, a
+ * negative size, M outside [1, 31], L < 1, causal not 0/1, a NULL pointer with
+ * a non-empty problem; SPT_ERR_UNSUPPORTED: the key codes of one head plus
+ * the per-warp score rows exceed the 227 KB of shared memory of one CTA
+ * (n_k (4 ceil(M/4) + 16) bytes), non-sm_100 device.  Asynchronous on stream. */
+spt_status spt_mha_topl(const spt_topl_desc* desc, const uint8_t* codes_q, const uint8_t* codes_k,
+                        int32_t* indices, void* stream);
 
 /* Static string for a status code (never NULL). */
 const char* spt_status_string(spt_status s);

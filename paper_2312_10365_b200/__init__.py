@@ -10,4 +10,4 @@ from ._lib import (SPT_ACT_GELU, SPT_ACT_RELU, SPT_ACT_SWIGLU, SPT_BF16, SPT_BWD
 from .ffn import (RouteBuffers, RoutedFFN, RoutedLoRAFFN, launch_count, make_desc,  # noqa: F401
                   profile_enable, profile_read, spt_ffn_backward, spt_ffn_balance_loss,
                   spt_ffn_forward, spt_ffn_lora_backward, spt_ffn_lora_forward, spt_ffn_lora_sizes,
-                  spt_ffn_route, spt_ffn_sizes, spt_status_string)
+                  spt_ffn_route, spt_ffn_sizes, spt_mha_topl, spt_status_string)

@@ -23,7 +23,8 @@ SPT_TILE_M = 128
 EXPORTED = ("spt_ffn_sizes", "spt_ffn_route", "spt_ffn_forward", "spt_ffn_backward",
             "spt_ffn_balance_loss", "spt_status_string", "spt_ffn_abi_version", "spt_ffn_launch_count",
             "spt_ffn_profile_enable", "spt_ffn_profile_read",
-            "spt_ffn_lora_sizes", "spt_ffn_lora_forward", "spt_ffn_lora_backward")  # ABI 3
+            "spt_ffn_lora_sizes", "spt_ffn_lora_forward", "spt_ffn_lora_backward",  # ABI 3
+            "spt_mha_topl")  # ABI 4
 
 
 class spt_ffn_desc(ctypes.Structure):
@@ -45,6 +46,11 @@ class spt_lora(ctypes.Structure):  # ABI 3: LoRA factors (device pointers)
 
 class spt_lora_grads(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("db1", "dc1", "db2", "dc2")]
+
+
+class spt_topl_desc(ctypes.Structure):  # ABI 4: sparse-MHA top-L selection
+    _fields_ = [(n, ctypes.c_int32) for n in ("n_heads", "n_q", "n_k", "n_codebooks", "top_l",
+                                              "causal")]
 
 
 class SptError(RuntimeError):
@@ -76,9 +82,10 @@ def lib() -> ctypes.CDLL:
         L.spt_ffn_lora_forward.argtypes = [D, P, P, P, LO, R, P, P, P, ctypes.c_size_t, P]
         L.spt_ffn_lora_backward.argtypes = [D, P, P, P, P, LO, R, P, P, P, LG, P, P, ctypes.c_uint,
                                             P, ctypes.c_size_t, P, P]
+        L.spt_mha_topl.argtypes = [ctypes.POINTER(spt_topl_desc), P, P, P, P]
         for f in ("spt_ffn_sizes", "spt_ffn_route", "spt_ffn_forward", "spt_ffn_backward",
                   "spt_ffn_balance_loss", "spt_ffn_lora_sizes", "spt_ffn_lora_forward",
-                  "spt_ffn_lora_backward"):
+                  "spt_ffn_lora_backward", "spt_mha_topl"):
             getattr(L, f).restype = ctypes.c_int
         L.spt_status_string.argtypes = [ctypes.c_int]
         L.spt_status_string.restype = ctypes.c_char_p

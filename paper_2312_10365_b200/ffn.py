@@ -143,6 +143,24 @@ def spt_ffn_lora_backward(desc, x, w1, w2, w_r, lora: dict, route: RouteBuffers,
         ws.numel() * ws.element_size(), ev, _stream(stream)))
 
 
+def spt_mha_topl(codes_q, codes_k, top_l: int, causal: bool = False, out=None, stream=None):
+    """Sparse-MHA top-L selection (ABI 4; Alg. 3 over PQ codes, Eq. 3).
+    codes_q [H, n_q, M], codes_k [H, n_k, M] uint8 device tensors; returns
+    indices [H, n_q, L] int32 (-1 = fewer than L candidates, causal rows)."""
+    H, nq, M = codes_q.shape
+    nk = codes_k.shape[1]
+    if codes_q.dtype != torch.uint8 or codes_k.dtype != torch.uint8:
+        raise ValueError("codes must be uint8")
+    if codes_k.shape[0] != H or codes_k.shape[2] != M:
+        raise ValueError("codes_q / codes_k disagree on heads or codebooks")
+    if out is None:
+        out = torch.empty(H, nq, int(top_l), dtype=torch.int32, device=codes_q.device)
+    d = L.spt_topl_desc(int(H), int(nq), int(nk), int(M), int(top_l), 1 if causal else 0)
+    L.check("spt_mha_topl", L.lib().spt_mha_topl(ctypes.byref(d), _p(codes_q), _p(codes_k), _p(out),
+                                                 _stream(stream)))
+    return out
+
+
 def spt_status_string(code: int) -> str:
     return L.status_string(code)
 
