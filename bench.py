@@ -198,6 +198,140 @@ def run_reference(args, cfg):
     }), flush=True)
 
 
+# ------------------------------------------------ f4: top-L selection (Alg. 3)
+TOPL_METRIC = "sparse-MHA top-L selection (Alg. 3) queries/s"
+
+
+def topl_alu_ops(cfg):
+    """Algorithmic integer ops of one selection: per (query, candidate key) pair,
+    Eq. 3 costs 10 ALU ops per 4-codebook word (XOR, 3 x shift+OR, AND, POPC, ADD);
+    candidates = n (bidirectional) or q+1 (causal)."""
+    pairs = cfg.n * (cfg.n + 1) / 2 if cfg.causal else float(cfg.n) * cfg.n
+    return cfg.heads * pairs * 10.0 * ((cfg.M + 3) // 4)
+
+
+def topl_workload(cfg, world):
+    return {"workload": f"{cfg.name}: top-L over PQ codes, {cfg.heads} (sequence, head) problems x "
+                        f"n={cfg.n} queries/keys, M={cfg.M} codebooks, E={cfg.E}, L={cfg.L} "
+                        f"(lambda={cfg.lam}), {'causal' if cfg.causal else 'bidirectional'}",
+            "queries_per_gpu": cfg.heads * cfg.n, "parallelism": f"dp{world}",
+            "l2": "L2 flushed (256 MB write) before every timed launch; codes %.0f MB, indices %.0f MB" % (
+                2 * cfg.heads * cfg.n * cfg.M / 1e6, cfg.heads * cfg.n * cfg.L * 4 / 1e6)}
+
+
+def topl_oracle_sample(cfg, n_heads, n_q):
+    from oracle import topl as OT
+    cq, ck = S.make_pq_codes(cfg, heads=n_heads)
+    if cfg.causal:
+        ck = cq
+    t = time.perf_counter()
+    for h in range(n_heads):
+        OT.topl_by_sort(cq[h][:n_q], ck[h], cfg.L, cfg.causal)
+    return time.perf_counter() - t
+
+
+def run_topl(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        nq = 64
+        for _ in range(args.warmup):
+            topl_oracle_sample(cfg, 1, nq)
+        tot = sum(topl_oracle_sample(cfg, 1, nq) for _ in range(args.steps))
+        value = nq * args.steps / tot
+        sample = f"{nq} queries of one head per step (numpy closed-form oracle, 1 thread)"
+        print(json.dumps({
+            "impl": "reference", "metric": TOPL_METRIC, "value": value, "unit": "queries/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": topl_workload(cfg, args.gpus),
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_2312_10365_b200 as P
+    from paper_2312_10365_b200 import dp
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cq, ck = S.make_pq_codes(cfg.with_(cfg_index=cfg.cfg_index + 100 * rank))  # per-rank sequences
+    if cfg.causal:
+        ck = cq
+    a, b = torch.from_numpy(cq).cuda(), torch.from_numpy(ck).cuda()
+    out = torch.empty(cfg.heads, cfg.n, cfg.L, dtype=torch.int32, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        P.spt_mha_topl(a, b, cfg.L, cfg.causal, out=out)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    if world > 1:
+        dist.barrier()
+    n0 = P.launch_count()
+    evs = []
+    for _ in range(args.steps):
+        flush.fill_(1)  # L2 flush, outside the timed pair
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        P.spt_mha_topl(a, b, cfg.L, cfg.causal, out=out)
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    launches = P.launch_count() - n0
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
+    clocks = sampler.stop()
+    ms_max = dp.max_over_ranks(ms, device="cuda")
+    q = cfg.heads * cfg.n
+    # end to end: codes from pinned host, indices back to pinned host, every step
+    ah, bh = a.cpu().pin_memory(), b.cpu().pin_memory()
+    oh = torch.empty(out.shape, dtype=torch.int32).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        a.copy_(ah, non_blocking=True)
+        b.copy_(bh, non_blocking=True)
+        P.spt_mha_topl(a, b, cfg.L, cfg.causal, out=out)
+        oh.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e = dp.max_over_ranks(e0.elapsed_time(e1) / args.steps, device="cuda")
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    f_hz = 1.965e9
+    peak = 148 * 64 * f_hz / 1e9  # alu-pipe lanes/clk/SM x SMs x max clock, Gops/s
+    ach = topl_alu_ops(cfg) / (ms / 1e3) / 1e9
+    res = {
+        "metric": TOPL_METRIC, "value": q * world / (ms_max / 1e3), "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded clustered PQ codes)",
+        "config": topl_workload(cfg, world),
+        "roofline": {"bound": "alu", "kernel": "topl_select", "achieved": ach, "peak": peak, "unit": "Gops/s",
+                     "frac": ach / peak, "traffic": None,
+                     "peak_src": "DESIGN.md: 64 alu-pipe lanes/clk/SM (B300_MICROARCH rt_SMSP=2) x 148 SMs "
+                                 "x 1.965 GHz", "algorithmic_per_launch": topl_alu_ops(cfg)},
+        "gpu_launches": launches, "clocks": clocks,
+        "e2e": {"value": q * world / (ms_e / 1e3), "unit": "queries/s", "ms_per_step": ms_e,
+                "h2d_bytes_per_step": int(a.numel() + b.numel()), "d2h_bytes_per_step": int(out.numel() * 4)},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        n_q = 256
+        secs = topl_oracle_sample(cfg, 1, n_q)
+        res["cpu_baseline"] = {"value": n_q / secs, "unit": "queries/s", "cores": 1, "kind": "oracle",
+                               "sample": f"{n_q} queries of one head, numpy closed-form oracle, {secs:.1f} s"}
+    print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def workload_config(cfg, world, T, balance_weight=0.0, lora=0):
     lb = f", load-balancing loss lambda={balance_weight}" if balance_weight else ""
     if lora:
@@ -269,10 +403,16 @@ def main():
     ap.add_argument("--no-dense", action="store_true", help="skip the dense cuBLAS context")
     ap.add_argument("--balance-weight", type=float, default=0.0,
                     help="lambda of the load-balancing loss (SURVEY f2; 0 = the north_star step)")
+    ap.add_argument("--topl", default="", choices=[""] + sorted(S.TOPL_CONFIGS),
+                    help="time the sparse-MHA top-L selection (SURVEY f4, Alg. 3) on this "
+                         "workload instead of the routed FFN")
     ap.add_argument("--lora", type=int, default=0, metavar="R",
                     help="LoRA-wrapped routed FFN of rank R (SURVEY f3; W frozen, factors trained); "
                          "0 = the north_star step")
     args = ap.parse_args()
+    if args.topl:
+        run_topl(args, S.TOPL_CONFIGS[args.topl])
+        return
     cfg = S.ALL_CONFIGS[args.config]
     if args.tokens:
         cfg = cfg.with_(T=args.tokens)

@@ -33,11 +33,10 @@ __device__ __forceinline__ int score_words(const uint32_t (&q)[NW], const uint32
   int diff = 0;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
-    uint32_t v = q[w] ^ k[w];  // byte is 0 iff the codewords agree
-    v |= v >> 4;
-    v |= v >> 2;
-    v |= v >> 1;
-    diff += __popc(v & 0x01010101u);  // differing codebooks in this word
+    const uint32_t v = q[w] ^ k[w];  // byte is 0 iff the codewords agree
+    // high bit of each byte set iff the byte is non-zero (no carry across bytes)
+    const uint32_t t = ((v & 0x7f7f7f7fu) + 0x7f7f7f7fu) | v;
+    diff += __popc(t & 0x80808080u);  // differing codebooks in this word
   }
   return diff;
 }
@@ -58,11 +57,13 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
   __shared__ int take[kToplWarps][kMaxScore + 1];
   __shared__ int seen[kToplWarps][kMaxScore + 1];
 
+  // CTA (h, c) takes the queries q = c, c + chunks, c + 2 chunks, ... of head h:
+  // interleaved, so causal rows (work ~ q) are balanced across CTAs
   const int chunks = (nq + qpb - 1) / qpb;
   const int h = blockIdx.x / chunks;
-  const int q0 = (blockIdx.x % chunks) * qpb;
-  const int q1 = min(nq, q0 + qpb);
-  const int nk_used = causal ? min(nk, q1) : nk;  // causal: keys > the chunk's last query unused
+  const int c = blockIdx.x % chunks;
+  const int q_last = c + ((nq - 1 - c) / chunks) * chunks;  // this CTA's last query
+  const int nk_used = causal ? min(nk, q_last + 1) : nk;   // causal: later keys unused
   const int pad = NW * 4 - M;                      // zero pad bytes compare equal: subtract
   // stage the head's key codes: key k -> words [k*KW, k*KW + NW), pad bytes 0
   {
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   uint8_t* my = sc + (size_t)warp * nk;
-  for (int q = q0 + warp; q < q1; q += kToplWarps) {
+  for (int q = c + warp * chunks; q < nq; q += kToplWarps * chunks) {
     uint32_t qv[NW];
     {
       const uint8_t* src = cq + ((size_t)h * nq + q) * M;
