@@ -10,16 +10,16 @@
 //   z   = x_t W_I[:,b] + u_t C_I[:,b]           FWD1 on X_aug = [x | hi(u) | lo(u) | 0],
 //                                                        W1_aug = [w1 | c1 | c1 | 0]
 //   h~  = g act(z);  P = h~ W_O[b]              FWD1 epilogue, FWD2 (unchanged)
-//   q_t = sum_b h~ B_O[b]                       lora_rowproj (per pair) + combine
+//   q_t = sum_b h~ B_O[b]                       lora_tile_mma (per pair rows) + combine
 //   y_t = sum_b P + q_t C_O                     lora_combine_fwd
 // Backward (W frozen; routing fixed):
 //   v_t = dy_t C_O^T                            tc_router GEMM (N = r)
 //   dA  = dy W_O[b]^T + v B_O[b]^T              dA kernel on dY_aug = [dy | hi(v) | lo(v) | 0],
 //                                                           W2_aug = [w2 | b2 | b2 | 0]
 //   dgate, dZ                                   dA epilogue (unchanged)
-//   dB_O[b] = sum_{t in b} h~^T v_t             lora_colgrad (per tile) + lora_grad_reduce
-//   dC_I[:,b]^T = sum_{t in b} dZ^T u_t         lora_colgrad + lora_grad_reduce
-//   du_t = sum_b dZ C_I[:,b]^T                  lora_rowproj (per pair) + combine
+//   dB_O[b] = sum_{t in b} h~^T v_t             lora_tile_mma (per tile) + lora_grad_reduce
+//   dC_I[:,b]^T = sum_{t in b} dZ^T u_t         lora_tile_mma + lora_grad_reduce
+//   du_t = sum_b dZ C_I[:,b]^T                  lora_tile_mma (per pair rows) + combine
 //   dx_t = sum_b dZ W_I[:,b]^T + router + du_t B_I^T    DX (unchanged) + lora_combine_bwd
 //   dB_I^T = du^T X,  dC_O = q^T dY             tcgen05 split-K GEMMs (the dW_R kernel)
 // u and v enter the tensor-core GEMMs as bf16 hi + lo halves (~16 significant
@@ -34,8 +34,6 @@
 namespace spt {
 
 namespace {
-
-__device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
 __device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8]) {
   const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
@@ -115,118 +113,11 @@ __global__ void __launch_bounds__(256) lora_aug_w_kernel(int64_t R, int d, int k
   }
 }
 
-struct TileRows {
-  int b, nvalid, pos0;  // block, live rows, bucket position of row 0
-  int64_t prow0;        // padded bucket row of row 0
-};
-__device__ __forceinline__ TileRows tile_rows(const RouteView& rv, const int32_t* tile_block,
-                                              int tile) {
-  TileRows tr;
-  tr.b = tile_block[tile];
-  const int mt = tile - rv.tile_offsets[tr.b];
-  const int nb = rv.block_offsets[tr.b + 1] - rv.block_offsets[tr.b];
-  tr.nvalid = min(kTileM, nb - mt * kTileM);
-  tr.pos0 = rv.block_offsets[tr.b] + mt * kTileM;
-  tr.prow0 = (int64_t)tile * kTileM;
-  return tr;
-}
-
-// Per pair (one thread per padded bucket row of a 128-row tile):
-//   out[prow, m r + q] = sum_{i < bw} A[prow, m bw + i] P[m][b bw + i][q]
-// fwd: A = h~ (m' = 1), P = B_O -> q rows;  bwd: A = dZ (m' halves), P = C_I^T -> du rows.
-template <int RP>
-__global__ void __launch_bounds__(128) lora_rowproj_kernel(int G, int bw, int mp, int r, int64_t D,
-                                                           RouteView rv,
-                                                           const int32_t* __restrict__ tile_block,
-                                                           const __nv_bfloat16* __restrict__ A,
-                                                           const __nv_bfloat16* __restrict__ P,
-                                                           float* __restrict__ out) {
-  const int tile = blockIdx.x;
-  if (tile >= rv.tile_offsets[G]) return;
-  const TileRows tr = tile_rows(rv, tile_block, tile);
-  __shared__ float Ps[64][RP];
-  const int64_t prow = tr.prow0 + threadIdx.x;
-  const bool live = (int)threadIdx.x < tr.nvalid;
-  const int aw = mp * bw;
-  for (int m = 0; m < mp; ++m) {
-    float acc[RP];
-#pragma unroll
-    for (int q = 0; q < RP; ++q) acc[q] = 0.f;
-    for (int i0 = 0; i0 < bw; i0 += 64) {
-      const int ni = min(64, bw - i0);  // bw % 16 == 0
-      __syncthreads();
-      for (int e = threadIdx.x; e < 64 * RP; e += blockDim.x) {
-        const int i = e / RP, q = e % RP;
-        Ps[i][q] = (i < ni && q < r) ? bf2f(P[((int64_t)m * D + (int64_t)tr.b * bw + i0 + i) * r + q])
-                                     : 0.f;
-      }
-      __syncthreads();
-      if (live) {
-        const __nv_bfloat16* ar = A + prow * aw + m * bw + i0;
-        for (int i = 0; i < ni; i += 8) {
-          float a[8];
-          load8(ar + i, a);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-#pragma unroll
-            for (int q = 0; q < RP; ++q) acc[q] = fmaf(a[j], Ps[i + j][q], acc[q]);
-          }
-        }
-      }
-    }
-    if (live) {
-      float* o = out + prow * kLoraK + m * r;
-      for (int q = 0; q < r; ++q) o[q] = acc[q];
-    }
-  }
-}
-
-// Per 128-row tile of block b, per feature i (one thread each):
-//   part[tile][m][i][q] = sum_{rows} A[prow, m bw + i] E[t(row), eoff + m r + q]
-// dC_I: A = dZ, E = the stashed u (f32, pitch m' r);  dB_O: A = h~, E = v (f32, pitch r).
-template <int RP, typename TE>
-__global__ void __launch_bounds__(128) lora_colgrad_kernel(int G, int bw, int mp, int r,
-                                                           RouteView rv,
-                                                           const int32_t* __restrict__ tile_block,
-                                                           const __nv_bfloat16* __restrict__ A,
-                                                           const TE* __restrict__ E, int epitch,
-                                                           float* __restrict__ part) {
-  const int tile = blockIdx.x;
-  if (tile >= rv.tile_offsets[G]) return;
-  const TileRows tr = tile_rows(rv, tile_block, tile);
-  __shared__ float Es[kTileM][RP];
-  __shared__ int tok[kTileM];
-  if (threadIdx.x < kTileM)
-    tok[threadIdx.x] = (int)threadIdx.x < tr.nvalid ? rv.bucket_token[tr.pos0 + threadIdx.x] : 0;
-  const int aw = mp * bw;
-  for (int m = 0; m < mp; ++m) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kTileM * RP; e += blockDim.x) {
-      const int row = e / RP, q = e % RP;
-      float v = 0.f;
-      if (row < tr.nvalid && q < r) v = (float)E[(int64_t)tok[row] * epitch + m * r + q];
-      Es[row][q] = v;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < bw; i += blockDim.x) {
-      float acc[RP];
-#pragma unroll
-      for (int q = 0; q < RP; ++q) acc[q] = 0.f;
-      const __nv_bfloat16* ac = A + tr.prow0 * aw + m * bw + i;
-      for (int row = 0; row < tr.nvalid; ++row) {
-        const float a = bf2f(ac[(int64_t)row * aw]);
-#pragma unroll
-        for (int q = 0; q < RP; ++q) acc[q] = fmaf(a, Es[row][q], acc[q]);
-      }
-      float* o = part + (((int64_t)tile * mp + m) * bw + i) * r;
-      for (int q = 0; q < r; ++q) o[q] = acc[q];
-    }
-  }
-}
-
-// out[m][b bw + i][q] (=|+=) sum over block b's tiles (ascending) of part[tile][m][i][q]
+// out[m][b bw + i][q] (=|+=) sum over block b's tiles (ascending) of
+// part[tile][slab0 + m][i][q] (per-tile partials with `slabs` slabs per tile)
 __global__ void __launch_bounds__(256) lora_grad_reduce_kernel(int G, int bw, int mp, int r,
-                                                               int64_t D, RouteView rv,
+                                                               int64_t D, RouteView rv, int slabs,
+                                                               int slab0,
                                                                const float* __restrict__ part,
                                                                float* __restrict__ out, int acc) {
   const int64_t n = (int64_t)mp * D * r;
@@ -239,7 +130,7 @@ __global__ void __launch_bounds__(256) lora_grad_reduce_kernel(int G, int bw, in
   const int b = (int)(unit / bw), i = (int)(unit % bw);
   float s = 0.f;
   for (int tile = rv.tile_offsets[b]; tile < rv.tile_offsets[b + 1]; ++tile)
-    s += part[(((int64_t)tile * mp + m) * bw + i) * r + q];
+    s += part[(((int64_t)tile * slabs + slab0 + m) * bw + i) * r + q];
   out[idx] = acc ? out[idx] + s : s;
 }
 
@@ -324,54 +215,12 @@ __global__ void __launch_bounds__(128) lora_combine_kernel(int64_t T, int d, int
   }
 }
 
-template <int RP>
-cudaError_t rowproj(const Geom& g, const RouteView& r, const Bufs& b, int mp, int rk,
-                    const void* A, const void* P, float* out, cudaStream_t s) {
-  lora_rowproj_kernel<RP><<<(unsigned)(ceil_div(g.pairs, kTileM) + g.G), 128, 0, s>>>(
-      g.G, g.bw, mp, rk, g.D, r, b.tile_block, (const __nv_bfloat16*)A, (const __nv_bfloat16*)P,
-      out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_rowproj(const Geom& g, const RouteView& r, const Bufs& b, int mp, int rk,
-                           const void* A, const void* P, float* out, cudaStream_t s) {
-  prof_begin("lora_rowproj", s);
-  cudaError_t e = rk <= 8    ? rowproj<8>(g, r, b, mp, rk, A, P, out, s)
-                  : rk <= 16 ? rowproj<16>(g, r, b, mp, rk, A, P, out, s)
-                  : rk <= 32 ? rowproj<32>(g, r, b, mp, rk, A, P, out, s)
-                             : rowproj<64>(g, r, b, mp, rk, A, P, out, s);
-  prof_end(s);
-  count_launch();
-  return e;
-}
-
-template <int RP, typename TE>
-cudaError_t colgrad(const Geom& g, const RouteView& r, const Bufs& b, int mp, int rk,
-                    const void* A, const TE* E, int epitch, float* part, cudaStream_t s) {
-  lora_colgrad_kernel<RP, TE><<<(unsigned)(ceil_div(g.pairs, kTileM) + g.G), 128, 0, s>>>(
-      g.G, g.bw, mp, rk, r, b.tile_block, (const __nv_bfloat16*)A, E, epitch, part);
-  return cudaGetLastError();
-}
-
-template <typename TE>
-cudaError_t launch_colgrad(const Geom& g, const RouteView& r, const Bufs& b, int mp, int rk,
-                           const void* A, const TE* E, int epitch, float* part, cudaStream_t s) {
-  prof_begin("lora_colgrad", s);
-  cudaError_t e = rk <= 8    ? colgrad<8, TE>(g, r, b, mp, rk, A, E, epitch, part, s)
-                  : rk <= 16 ? colgrad<16, TE>(g, r, b, mp, rk, A, E, epitch, part, s)
-                  : rk <= 32 ? colgrad<32, TE>(g, r, b, mp, rk, A, E, epitch, part, s)
-                             : colgrad<64, TE>(g, r, b, mp, rk, A, E, epitch, part, s);
-  prof_end(s);
-  count_launch();
-  return e;
-}
-
-cudaError_t launch_grad_reduce(const Geom& g, const RouteView& r, int mp, int rk,
-                               const float* part, float* out, bool acc, cudaStream_t s) {
+cudaError_t launch_grad_reduce(const Geom& g, const RouteView& r, int mp, int rk, int slabs,
+                               int slab0, const float* part, float* out, bool acc, cudaStream_t s) {
   const int64_t n = (int64_t)mp * g.D * rk;
   prof_begin("lora_grad_reduce", s);
-  lora_grad_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(g.G, g.bw, mp, rk, g.D, r,
-                                                                     part, out, acc ? 1 : 0);
+  lora_grad_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(
+      g.G, g.bw, mp, rk, g.D, r, slabs, slab0, part, out, acc ? 1 : 0);
   prof_end(s);
   count_launch();
   return cudaGetLastError();
@@ -400,6 +249,230 @@ cudaError_t aug_w(const Geom& g, int ka, int64_t R, const void* w, const void* P
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core (mma.sync m16n8k16 bf16 -> fp32) form of the rank-r per-tile
+// products, one CTA (8 warps) per 128-row bucket tile of block b:
+//   rows:  out[prow, m r + q]   = sum_i A[prow, m bw + i] P[m][b bw + i][q]       (q / du rows)
+//   cols:  part[tile][m][i][q]  = sum_rows A[prow, m bw + i] E[t(row), m r + q]   (dC_I, dB_O)
+// A tiles are staged in shared memory once per 128-feature chunk and feed
+// both products (ldmatrix for the row product, ldmatrix.trans for the column
+// product); E is split into bf16 hi + lo halves (two MMAs) so the gradient
+// keeps ~16 significant bits.
+constexpr int kMmaRows = 128;
+constexpr int kMmaChunk = 128;                 // features per staged chunk
+constexpr int kMmaPitch = kMmaChunk + 8;       // +16 B per row: conflict-free ldmatrix
+constexpr int kMmaEPitch = kMmaRows + 8;
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// mode 0 (forward): rows only, A = h~ (m' = 1), P = B_O  -> q rows
+// mode 1 (backward): A = dZ: rows (P = C_I^T -> du rows) and cols (E = u -> dC_I);
+//                    then A = h~: cols (E = v -> dB_O)
+template <int RP>
+__global__ void __launch_bounds__(256) lora_tile_mma_kernel(
+    int mode, int G, int bw, int mp, int r, int64_t D, RouteView rv,
+    const int32_t* __restrict__ tile_block, const __nv_bfloat16* __restrict__ A,
+    const __nv_bfloat16* __restrict__ P, const float* __restrict__ U, int upitch,
+    const __nv_bfloat16* __restrict__ H, const float* __restrict__ V, float* __restrict__ rows_out,
+    float* __restrict__ part) {
+  constexpr int NT = RP / 8;  // n8 tiles
+  extern __shared__ __align__(16) uint8_t mma_smem[];
+  __nv_bfloat16* As = reinterpret_cast<__nv_bfloat16*>(mma_smem);   // [row][feature]
+  __nv_bfloat16* Pt = As + kMmaRows * kMmaPitch;                     // [q][i]
+  __nv_bfloat16* Eh = Pt + RP * kMmaPitch;                           // [q][row] hi
+  __nv_bfloat16* El = Eh + RP * kMmaEPitch;                          // [q][row] lo
+  __shared__ int tok[kMmaRows];
+  const int tile = blockIdx.x;
+  if (tile >= rv.tile_offsets[G]) return;
+  const int b = tile_block[tile];
+  const int mt = tile - rv.tile_offsets[b];
+  const int nb = rv.block_offsets[b + 1] - rv.block_offsets[b];
+  const int nvalid = min(kMmaRows, nb - mt * kMmaRows);
+  const int pos0 = rv.block_offsets[b] + mt * kMmaRows;
+  const int64_t prow0 = (int64_t)tile * kMmaRows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  if (threadIdx.x < kMmaRows)
+    tok[threadIdx.x] = (int)threadIdx.x < nvalid ? rv.bucket_token[pos0 + threadIdx.x] : 0;
+
+  // stage rows [0,128) x features [f0, f0 + ni) of X (pitch xw) into As (zero rows >= nvalid)
+  auto stage_a = [&](const __nv_bfloat16* X, int xw, int f0, int ni) {
+    const int v8 = ni / 8;
+    for (int e = threadIdx.x; e < kMmaRows * v8; e += blockDim.x) {
+      const int row = e / v8, cc = (e % v8) * 8;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (row < nvalid) v = __ldg(reinterpret_cast<const uint4*>(X + (prow0 + row) * xw + f0 + cc));
+      *reinterpret_cast<uint4*>(&As[row * kMmaPitch + cc]) = v;
+    }
+  };
+  // stage E[t(row)][eoff + q] (fp32) as bf16 hi / lo, transposed [q][row]
+  auto stage_e = [&](const float* E, int epitch, int eoff) {
+    for (int e = threadIdx.x; e < RP * kMmaRows; e += blockDim.x) {
+      const int q = e / kMmaRows, row = e % kMmaRows;
+      float v = 0.f;
+      if (row < nvalid && q < r) v = E[(int64_t)tok[row] * epitch + eoff + q];
+      const __nv_bfloat16 hi = __float2bfloat16(v);
+      Eh[q * kMmaEPitch + row] = hi;
+      El[q * kMmaEPitch + row] = __float2bfloat16(v - __bfloat162float(hi));
+    }
+  };
+  // column product over the staged chunk: part rows [f0, f0 + ni) of slab m
+  auto cols = [&](int ni, float* dst) {
+    // warp w: features [16w, 16w + 16) of the chunk (ni <= 128 -> <= 8 m16 tiles)
+    if (warp * 16 < ni) {
+      float acc[NT][4];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+#pragma unroll 2
+      for (int k0 = 0; k0 < kMmaRows; k0 += 16) {
+        // A^T fragment (m = feature, k = row) from As[row][feature] via ldmatrix.trans
+        const int mi = lane >> 3, rr = lane & 7;
+        const int krow = k0 + rr + ((mi & 2) ? 8 : 0);
+        const int mcol = warp * 16 + ((mi & 1) ? 8 : 0);
+        uint32_t a[4];
+        ldsm_x4_t(a, &As[krow * kMmaPitch + mcol]);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const __nv_bfloat16* eh = &Eh[(n * 8 + g) * kMmaEPitch + k0 + 2 * c];
+          const __nv_bfloat16* el = &El[(n * 8 + g) * kMmaEPitch + k0 + 2 * c];
+          mma16816(acc[n], a, *reinterpret_cast<const uint32_t*>(eh),
+                   *reinterpret_cast<const uint32_t*>(eh + 8));
+          mma16816(acc[n], a, *reinterpret_cast<const uint32_t*>(el),
+                   *reinterpret_cast<const uint32_t*>(el + 8));
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int q0 = n * 8 + 2 * c;
+        const int i0 = warp * 16 + g;
+        if (q0 < r) {
+          dst[(int64_t)i0 * r + q0] = acc[n][0];
+          dst[(int64_t)(i0 + 8) * r + q0] = acc[n][2];
+        }
+        if (q0 + 1 < r) {
+          dst[(int64_t)i0 * r + q0 + 1] = acc[n][1];
+          dst[(int64_t)(i0 + 8) * r + q0 + 1] = acc[n][3];
+        }
+      }
+    }
+  };
+
+  const __nv_bfloat16* Arow = mode == 0 ? H : A;  // the row product's operand
+  const int aw = mode == 0 ? bw : mp * bw;
+  const int mrows = mode == 0 ? 1 : mp;
+  for (int m = 0; m < mrows; ++m) {
+    float racc[NT][4];  // row product: warp w owns rows [16w, 16w + 16)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) racc[n][0] = racc[n][1] = racc[n][2] = racc[n][3] = 0.f;
+    if (mode == 1) {
+      __syncthreads();
+      stage_e(U, upitch, m * r);
+    }
+    for (int i0 = 0; i0 < bw; i0 += kMmaChunk) {
+      const int ni = min(kMmaChunk, bw - i0);
+      __syncthreads();
+      stage_a(Arow, aw, m * bw + i0, ni);
+      for (int e = threadIdx.x; e < RP * ni; e += blockDim.x) {
+        const int q = e / ni, i = e % ni;
+        Pt[q * kMmaPitch + i] =
+            q < r ? P[((int64_t)m * D + (int64_t)b * bw + i0 + i) * r + q] : __float2bfloat16(0.f);
+      }
+      __syncthreads();
+      // row product: M = rows, K = features of the chunk, N = RP
+      for (int k0 = 0; k0 < ni; k0 += 16) {
+        const int mi = lane >> 3, rr = lane & 7;
+        uint32_t a[4];
+        ldsm_x4(a, &As[(warp * 16 + rr + ((mi & 1) ? 8 : 0)) * kMmaPitch + k0 + ((mi & 2) ? 8 : 0)]);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const __nv_bfloat16* pb = &Pt[(n * 8 + g) * kMmaPitch + k0 + 2 * c];
+          mma16816(racc[n], a, *reinterpret_cast<const uint32_t*>(pb),
+                   *reinterpret_cast<const uint32_t*>(pb + 8));
+        }
+      }
+      if (mode == 1)  // dC_I^T rows [b bw + i0, +ni) of slab m
+        cols(ni, part + (((int64_t)tile * (mp + 1) + m) * bw + i0) * r);
+    }
+    // rows out: [prow, m r + q]
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int q0 = n * 8 + 2 * c;
+      const int row = warp * 16 + g;
+      float* o0 = rows_out + (prow0 + row) * kLoraK + m * r;
+      float* o1 = rows_out + (prow0 + row + 8) * kLoraK + m * r;
+      if (row < nvalid) {
+        if (q0 < r) o0[q0] = racc[n][0];
+        if (q0 + 1 < r) o0[q0 + 1] = racc[n][1];
+      }
+      if (row + 8 < nvalid) {
+        if (q0 < r) o1[q0] = racc[n][2];
+        if (q0 + 1 < r) o1[q0 + 1] = racc[n][3];
+      }
+    }
+  }
+  if (mode == 1) {  // dB_O: A = h~, E = v
+    __syncthreads();
+    stage_e(V, r, 0);
+    for (int i0 = 0; i0 < bw; i0 += kMmaChunk) {
+      const int ni = min(kMmaChunk, bw - i0);
+      __syncthreads();
+      stage_a(H, bw, i0, ni);
+      __syncthreads();
+      cols(ni, part + (((int64_t)tile * (mp + 1) + mp) * bw + i0) * r);
+    }
+  }
+}
+
+template <int RP>
+constexpr size_t tile_mma_smem() {
+  return (size_t)(kMmaRows * kMmaPitch + RP * kMmaPitch + 2 * RP * kMmaEPitch) * 2;
+}
+
+template <int RP>
+cudaError_t tile_mma(int mode, const Geom& g, const RouteView& r, const Bufs& b, const LoraArgs& lo,
+                     const void* P, cudaStream_t s) {
+  constexpr size_t smem = tile_mma_smem<RP>();
+  cudaError_t e = cudaFuncSetAttribute(lora_tile_mma_kernel<RP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  lora_tile_mma_kernel<RP><<<(unsigned)(ceil_div(g.pairs, kTileM) + g.G), 256, smem, s>>>(
+      mode, g.G, g.bw, g.mp, lo.r, g.D, r, b.tile_block, (const __nv_bfloat16*)b.dz,
+      (const __nv_bfloat16*)P, lo.ust, g.mp * lo.r, (const __nv_bfloat16*)b.h, lo.uv, lo.rowp,
+      lo.gpart);
+  return cudaGetLastError();
+}
+
+// mode 0: q rows (h~ B_O[b]);  mode 1: du rows (dZ C_I[b]) + per-tile dC_I / dB_O partials
+cudaError_t launch_tile_mma(int mode, const Geom& g, const RouteView& r, const Bufs& b,
+                            const LoraArgs& lo, cudaStream_t s) {
+  const void* P = mode == 0 ? lo.b2 : lo.c1;
+  prof_begin(mode == 0 ? "lora_rows_fwd" : "lora_tiles_bwd", s);
+  cudaError_t e = lo.r <= 8    ? tile_mma<8>(mode, g, r, b, lo, P, s)
+                  : lo.r <= 16 ? tile_mma<16>(mode, g, r, b, lo, P, s)
+                  : lo.r <= 32 ? tile_mma<32>(mode, g, r, b, lo, P, s)
+                               : tile_mma<64>(mode, g, r, b, lo, P, s);
+  prof_end(s);
+  count_launch();
+  return e;
+}
+
 // geometry of the rank-r dense GEMMs: N (router kind) / M (dense_tn kind) = n rows
 Geom skinny(const Geom& g, int n) {
   Geom h = g;
@@ -421,7 +494,7 @@ cudaError_t lora_fwd_prep(const Geom& g, const void* x, const void* w1, const Lo
 
 cudaError_t lora_fwd_finish(const Geom& g, const RouteView& r, const Bufs& b, const LoraArgs& lo,
                             void* y, cudaStream_t s) {
-  cudaError_t e = launch_rowproj(g, r, b, 1, lo.r, b.h, lo.b2, lo.rowp, s);  // h~ B_O[b]
+  cudaError_t e = launch_tile_mma(0, g, r, b, lo, s);  // q rows: h~ B_O[b]
   if (e != cudaSuccess) return e;
   prof_begin("lora_combine_fwd", s);
   lora_combine_kernel<false><<<(unsigned)g.T, 128, 0, s>>>(
@@ -443,18 +516,14 @@ cudaError_t lora_bwd_prep(const Geom& g, const void* dy, const void* w2, const L
 
 cudaError_t lora_bwd_grads(const Geom& g, const RouteView& r, const Bufs& b, const LoraArgs& lo,
                            cudaStream_t s) {
-  const int64_t tiles = ceil_div(g.pairs, kTileM) + g.G;
-  float* pc1 = lo.gpart;                                     // [tiles, m', bw, r]
-  float* pb2 = lo.gpart + tiles * g.mp * g.bw * lo.r;        // [tiles, 1, bw, r]
-  cudaError_t e = launch_rowproj(g, r, b, g.mp, lo.r, b.dz, lo.c1, lo.rowp, s);  // du rows
+  // du rows (dZ C_I[b]) and per-tile [m' + 1] slabs: dC_I^T (m' slabs), dB_O
+  cudaError_t e = launch_tile_mma(1, g, r, b, lo, s);
   if (e != cudaSuccess) return e;
-  e = launch_colgrad<float>(g, r, b, g.mp, lo.r, b.dz, lo.ust, g.mp * lo.r, pc1, s);
-  if (e != cudaSuccess) return e;
-  e = launch_colgrad<float>(g, r, b, 1, lo.r, b.h, lo.uv, lo.r, pb2, s);
-  if (e != cudaSuccess) return e;
-  if ((e = launch_grad_reduce(g, r, g.mp, lo.r, pc1, lo.dc1, lo.accumulate, s)) != cudaSuccess)
+  const int slabs = g.mp + 1;
+  if ((e = launch_grad_reduce(g, r, g.mp, lo.r, slabs, 0, lo.gpart, lo.dc1, lo.accumulate, s)) !=
+      cudaSuccess)
     return e;
-  return launch_grad_reduce(g, r, 1, lo.r, pb2, lo.db2, lo.accumulate, s);
+  return launch_grad_reduce(g, r, 1, lo.r, slabs, g.mp, lo.gpart, lo.db2, lo.accumulate, s);
 }
 
 cudaError_t lora_bwd_finish(const Geom& g, const RouteView& r, const Bufs& b, const LoraArgs& lo,
