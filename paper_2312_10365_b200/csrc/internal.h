@@ -170,6 +170,10 @@ cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logi
 cudaError_t tc_dense_tn(const Geom& g, const void* ahl, const void* bmat, float* part, int n_split,
                         float* out, bool accumulate, cudaStream_t s);
 int dense_tn_splits(const Geom& g);
+// dense  out[T, d] (bf16) = A B  with A given as bf16 hi|lo halves [2, T, gpad] and
+// B [G, d] bf16 (the dx router term of the balance loss; the du B_I^T term of LoRA)
+cudaError_t tc_dense_nn(const Geom& g, const void* ahl, const void* bmat, void* out,
+                        cudaStream_t s);
 // lo != NULL: the LoRA-wrapped FFN (FWD1 on X_aug / W1_aug; dA on dY_aug / W2_aug;
 // no dW1 / dW2 -- W is frozen -- and the LoRA factor gradients instead)
 cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void* w2,

@@ -10,8 +10,8 @@
 //   z   = x_t W_I[:,b] + u_t C_I[:,b]           FWD1 on X_aug = [x | hi(u) | lo(u) | 0],
 //                                                        W1_aug = [w1 | c1 | c1 | 0]
 //   h~  = g act(z);  P = h~ W_O[b]              FWD1 epilogue, FWD2 (unchanged)
-//   q_t = sum_b h~ B_O[b]                       lora_tile_mma (per pair rows) + combine
-//   y_t = sum_b P + q_t C_O                     lora_combine_fwd
+//   q_t = sum_b h~ B_O[b]                       lora_tile_mma (per pair rows) + token reduce
+//   y_t = sum_b P + q_t C_O                     tc_dense_nn (q C_O) + lora_combine_fwd
 // Backward (W frozen; routing fixed):
 //   v_t = dy_t C_O^T                            tc_router GEMM (N = r)
 //   dA  = dy W_O[b]^T + v B_O[b]^T              dA kernel on dY_aug = [dy | hi(v) | lo(v) | 0],
@@ -19,8 +19,9 @@
 //   dgate, dZ                                   dA epilogue (unchanged)
 //   dB_O[b] = sum_{t in b} h~^T v_t             lora_tile_mma (per tile) + lora_grad_reduce
 //   dC_I[:,b]^T = sum_{t in b} dZ^T u_t         lora_tile_mma + lora_grad_reduce
-//   du_t = sum_b dZ C_I[:,b]^T                  lora_tile_mma (per pair rows) + combine
-//   dx_t = sum_b dZ W_I[:,b]^T + router + du_t B_I^T    DX (unchanged) + lora_combine_bwd
+//   du_t = sum_b dZ C_I[:,b]^T                  lora_tile_mma (per pair rows) + token reduce
+//   dx_t = sum_b dZ W_I[:,b]^T + router + du_t B_I^T    DX (unchanged) + tc_dense_nn
+//                                                       (du B_I^T) + lora_combine_bwd
 //   dB_I^T = du^T X,  dC_O = q^T dY             tcgen05 split-K GEMMs (the dW_R kernel)
 // u and v enter the tensor-core GEMMs as bf16 hi + lo halves (~16 significant
 // bits: the pre-activation z, and with it every ReLU sign decision, matches the
@@ -134,25 +135,22 @@ __global__ void __launch_bounds__(256) lora_grad_reduce_kernel(int G, int bw, in
   out[idx] = acc ? out[idx] + s : s;
 }
 
-// Per token t (one CTA): s[c] = sum_{j asc} rowp[prow(t,j)][c] for c < ns (q or du),
-// written as bf16 hi + lo halves [2, T, spitch] for the tcgen05 GEMM; then
-//   out[t] = sum_{j asc} part[prow(t,j)] + router term + sum_c s[c] F[c, :]
-// (fwd: F = C_O, no router term; bwd: F = B_I^T rows, router term as combine_bwd).
+// Per token t (one CTA):
+//   out[t] = sum_{j asc} part[prow(t,j)] + router term + lora[t]
+// router term as combine_bwd (dense [T,d] if `dense`, else sum_j dlogit w_r[b_j]
+// when w_r; none in the forward); lora = the dense rank-r term (q C_O forward,
+// du B_I^T backward) computed on tensor cores by tc_dense_nn.
 template <bool kBwd>
-__global__ void __launch_bounds__(128) lora_combine_kernel(int64_t T, int d, int k, int ns,
-                                                           int spitch, RouteView r,
+__global__ void __launch_bounds__(128) lora_combine_kernel(int64_t T, int d, int k, RouteView r,
                                                            const __nv_bfloat16* __restrict__ part,
-                                                           const float* __restrict__ rowp,
-                                                           const __nv_bfloat16* __restrict__ F,
                                                            const float* __restrict__ dlogit,
                                                            const __nv_bfloat16* __restrict__ w_r,
                                                            const __nv_bfloat16* __restrict__ dense,
-                                                           __nv_bfloat16* __restrict__ out,
-                                                           __nv_bfloat16* __restrict__ shl) {
+                                                           const __nv_bfloat16* __restrict__ lora,
+                                                           __nv_bfloat16* __restrict__ out) {
   __shared__ int64_t rows[kMaxBlocks];
   __shared__ int blk[kMaxBlocks];
   __shared__ float dl[kMaxBlocks];
-  __shared__ float sv[kLoraK];
   const int64_t t = blockIdx.x;
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     rows[j] = pair_row(r, t, k, j);
@@ -160,16 +158,6 @@ __global__ void __launch_bounds__(128) lora_combine_kernel(int64_t T, int d, int
       blk[j] = r.topk_idx[t * k + j];
       dl[j] = dlogit[rows[j]];
     }
-  }
-  __syncthreads();
-  if (threadIdx.x < spitch) {
-    float v = 0.f;
-    if ((int)threadIdx.x < ns)
-      for (int j = 0; j < k; ++j) v += rowp[rows[j] * kLoraK + threadIdx.x];
-    if ((int)threadIdx.x < kLoraK) sv[threadIdx.x] = v;
-    const __nv_bfloat16 hi = __float2bfloat16(v);
-    shl[t * spitch + threadIdx.x] = hi;
-    shl[(T + t) * spitch + threadIdx.x] = __float2bfloat16(v - __bfloat162float(hi));
   }
   __syncthreads();
   for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
@@ -205,12 +193,10 @@ __global__ void __launch_bounds__(128) lora_combine_kernel(int64_t T, int d, int
         for (int i = 0; i < 8; ++i) acc[i] = fmaf(dl[jj], w[i], acc[i]);
       }
     }
-    for (int q = 0; q < ns; ++q) {
-      float f[8];
-      load8(F + (int64_t)q * d + c, f);
+    float v[8];
+    load8(lora + t * d + c, v);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = fmaf(sv[q], f[i], acc[i]);
-    }
+    for (int i = 0; i < 8; ++i) acc[i] += v[i];
     *reinterpret_cast<uint4*>(out + t * d + c) = pack8(acc);
   }
 }
@@ -440,6 +426,25 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
   }
 }
 
+// Per token (one warp): s[c] = sum_{j asc} rowp[prow(t,j)][c] (c < ns) as bf16 hi|lo
+// halves [2, T, spitch] -- the A operand of the du B_I^T GEMM.
+__global__ void __launch_bounds__(256) lora_token_reduce_kernel(int64_t T, int k, int ns,
+                                                                int spitch, RouteView r,
+                                                                const float* __restrict__ rowp,
+                                                                __nv_bfloat16* __restrict__ shl) {
+  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  for (int c = lane; c < spitch; c += 32) {
+    float v = 0.f;
+    if (c < ns)
+      for (int j = 0; j < k; ++j) v += rowp[pair_row(r, t, k, j) * kLoraK + c];
+    const __nv_bfloat16 hi = __float2bfloat16(v);
+    shl[t * spitch + c] = hi;
+    shl[(T + t) * spitch + c] = __float2bfloat16(v - __bfloat162float(hi));
+  }
+}
+
 template <int RP>
 constexpr size_t tile_mma_smem() {
   return (size_t)(kMmaRows * kMmaPitch + RP * kMmaPitch + 2 * RP * kMmaEPitch) * 2;
@@ -496,11 +501,20 @@ cudaError_t lora_fwd_finish(const Geom& g, const RouteView& r, const Bufs& b, co
                             void* y, cudaStream_t s) {
   cudaError_t e = launch_tile_mma(0, g, r, b, lo, s);  // q rows: h~ B_O[b]
   if (e != cudaSuccess) return e;
+  // q = sum_b q rows -> hi|lo (stashed for dC_O); the dense q C_O term on tensor
+  // cores into the (now free) X_aug buffer; the combine adds it to the partials
+  const int qpad = lora_qpad(lo.r);
+  prof_begin("lora_token_reduce", s);
+  lora_token_reduce_kernel<<<(unsigned)ceil_div(g.T, 8), 256, 0, s>>>(
+      g.T, g.k, lo.r, qpad, r, lo.rowp, (__nv_bfloat16*)lo.qhl);
+  prof_end(s);
+  count_launch();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = tc_dense_nn(skinny(g, lo.r), lo.qhl, lo.c2, lo.xaug, s)) != cudaSuccess) return e;
   prof_begin("lora_combine_fwd", s);
   lora_combine_kernel<false><<<(unsigned)g.T, 128, 0, s>>>(
-      g.T, g.d, g.k, lo.r, lora_qpad(lo.r), r, (const __nv_bfloat16*)b.part, lo.rowp,
-      (const __nv_bfloat16*)lo.c2, nullptr, nullptr, nullptr, (__nv_bfloat16*)y,
-      (__nv_bfloat16*)lo.qhl);
+      g.T, g.d, g.k, r, (const __nv_bfloat16*)b.part, nullptr, nullptr, nullptr,
+      (const __nv_bfloat16*)lo.xaug, (__nv_bfloat16*)y);
   prof_end(s);
   count_launch();
   return cudaGetLastError();
@@ -530,18 +544,29 @@ cudaError_t lora_bwd_finish(const Geom& g, const RouteView& r, const Bufs& b, co
                             const void* x, const void* dy, const void* dense, const void* w_r,
                             void* dx, cudaStream_t s) {
   const int nu = g.mp * lo.r;
+  const int upad = lora_upad(g, lo.r);
   const void* wr = g.gate == SPT_GATE_SIGMOID ? w_r : nullptr;
-  prof_begin("lora_combine_bwd", s);
-  lora_combine_kernel<true><<<(unsigned)g.T, 128, 0, s>>>(
-      g.T, g.d, g.k, nu, lora_upad(g, lo.r), r, (const __nv_bfloat16*)b.part, lo.rowp,
-      (const __nv_bfloat16*)lo.b1, dense ? nullptr : b.dlogit, (const __nv_bfloat16*)wr,
-      (const __nv_bfloat16*)dense, (__nv_bfloat16*)dx, (__nv_bfloat16*)lo.dhl);
+  // dU rows -> hi|lo; the dense du B_I^T term on tensor cores into the (now free)
+  // dY_aug buffer; the combine adds it next to the partials and the router term
+  prof_begin("lora_token_reduce", s);
+  lora_token_reduce_kernel<<<(unsigned)ceil_div(g.T, 8), 256, 0, s>>>(
+      g.T, g.k, nu, upad, r, lo.rowp, (__nv_bfloat16*)lo.dhl);
   prof_end(s);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  Geom gu = skinny(g, nu);
+  if ((e = tc_dense_nn(gu, lo.dhl, lo.b1, lo.xaug, s)) != cudaSuccess) return e;
+  prof_begin("lora_combine_bwd", s);
+  lora_combine_kernel<true><<<(unsigned)g.T, 128, 0, s>>>(
+      g.T, g.d, g.k, r, (const __nv_bfloat16*)b.part, dense ? nullptr : b.dlogit,
+      (const __nv_bfloat16*)wr, (const __nv_bfloat16*)dense, (const __nv_bfloat16*)lo.xaug,
+      (__nv_bfloat16*)dx);
+  prof_end(s);
+  count_launch();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // dB_I^T [m' r, d] = dU^T X ;  dC_O [r, d] = q^T dY
-  e = tc_dense_tn(skinny(g, nu), lo.dhl, x, lo.spart, lo.n_split_u, lo.db1, lo.accumulate, s);
+  e = tc_dense_tn(gu, lo.dhl, x, lo.spart, lo.n_split_u, lo.db1, lo.accumulate, s);
   if (e != cudaSuccess) return e;
   return tc_dense_tn(skinny(g, lo.r), lo.qhl, dy, lo.spart, lo.n_split_v, lo.dc2, lo.accumulate,
                      s);

@@ -2059,6 +2059,18 @@ cudaError_t tc_dense_tn(const Geom& g, const void* ahl, const void* bmat, float*
   return cudaGetLastError();
 }
 
+cudaError_t tc_dense_nn(const Geom& g, const void* ahl, const void* bmat, void* out,
+                        cudaStream_t s) {
+  TcArgs a{};
+  base_args(a, g, RouteView{});
+  bool ok = make_tmap_bf16_2d(&a.ta, ahl, (uint64_t)2 * g.T, g.gpad, g.gpad, 64, 128) &&
+            make_tmap_bf16_2d(&a.tb, bmat, g.G, g.d, g.d, 64, 64);
+  a.BN = 256;
+  a.out = out;
+  TRY(launch<K_DXR>(a, (int)ceil_div(g.T, 128) * a.NT, s));
+  return cudaSuccess;
+}
+
 cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void* w2,
                         const void* w_r, const RouteView& r, const void* dy, void* dx, float* dw1,
                         float* dw2, float* dw_r, float* dgate_out, bool accumulate, const Bufs& b,
