@@ -142,3 +142,53 @@ def test_lora_deterministic(orc):
     b = gpu_run_lora(cfg, 200, inp, lora, 16)
     for n in NAMES:
         assert np.array_equal(a[n], b[n]), n
+
+
+# BASELINE sizes (bench.py's launch configuration), on outputs the oracle computes
+# one by one: the LoRA-wrapped FFN equals the plain routed FFN on the merged
+# weights W + BC (pinned in test_oracle_lora.py), so the per-token /
+# per-block C oracle on merged fp64 weights gives sampled rows of y, dx, dgate and,
+# through the chain rule, of dC_I and dB_O for sampled blocks.  dB_I and dC_O sum
+# over every block; they are checked by the exact rescaling invariances
+# <dB_I, B_I> = <dC_I, C_I> and <dB_O, B_O> = <dC_O, C_O> (y is unchanged under
+# B -> sB, C -> C/s).  ReLU configs are left to the small cases: at 10^5-10^6
+# pairs a few pre-activations sit within fp32 rounding of the kink.
+@pytest.mark.parametrize("name,n_blocks", [("bert", 2), ("llama_scale", 1)])
+def test_lora_fullsize_sampled(orc, name, n_blocks):
+    cfg = S.ALL_CONFIGS[name]
+    T, r = cfg.T, 16
+    inp = S.make_inputs(cfg, T)
+    lora = S.make_lora(cfg, r)
+    got = gpu_run_lora(cfg, T, inp, lora, r)
+    ti = orc.topk(got["logits"], cfg.k)
+    assert np.array_equal(got["topk_idx"], ti)
+    lg = got["logits"].astype(np.float64)
+    w1m, w2m = OL.merged_weights(inp["w1"], inp["w2"], lora, cfg.act)
+    rng = np.random.default_rng(cfg.seed + 1)
+    tokens = np.unique(np.concatenate([[0, T - 1], rng.integers(0, T, 14)])).astype(np.int64)
+    blocks = np.unique(rng.integers(0, cfg.G, n_blocks)).astype(np.int32)
+    tol = TOL["bf16"]
+    y = orc.forward(inp["x"], w1m, w2m, lg, ti, cfg.act, cfg.gate, tokens=tokens)
+    assert relerr(got["y"][tokens], y[tokens]) <= tol
+    ref = orc.backward(inp["x"], w1m, w2m, inp["w_r"], lg, ti, inp["dy"], cfg.act, cfg.gate,
+                       tokens=tokens, blocks=blocks)
+    for n in ("dx", "dgate"):
+        assert relerr(got[n][tokens], ref[n][tokens]) <= tol, n
+    assert relerr(got["dw_r"][blocks], ref["dw_r"][blocks]) <= tol
+    mp, bw = cfg.mprime, cfg.bw
+    rows = np.concatenate([np.arange(b * bw, (b + 1) * bw) for b in blocks])
+    dw1 = ref["dw1"].reshape((mp,) + ref["dw1"].shape[-2:])
+    b1 = np.asarray(lora["b1"], np.float64).reshape(mp, r, cfg.d)
+    gc1 = got["dc1"].reshape(mp, cfg.D, r)
+    for m in range(mp):  # w1' = w1 + c1 b1  =>  dc1 = dw1' b1^T
+        assert relerr(gc1[m][rows], dw1[m][rows] @ b1[m].T) <= tol
+    assert relerr(got["db2"][rows], ref["dw2"][rows] @ np.asarray(lora["c2"], np.float64).T) <= tol
+
+    def dot(a, b):
+        return float(np.sum(np.asarray(a, np.float64) * np.asarray(b, np.float64)))
+
+    for (ga, fa), (gb, fb) in [(("db1", "b1"), ("dc1", "c1")), (("db2", "b2"), ("dc2", "c2"))]:
+        lhs = dot(got[ga], np.asarray(lora[fa]).reshape(got[ga].shape))
+        rhs = dot(got[gb], np.asarray(lora[fb]).reshape(got[gb].shape))
+        scale = np.sqrt(dot(got[ga], got[ga]) * dot(lora[fa], lora[fa]))
+        assert abs(lhs - rhs) <= tol * scale, (ga, gb, lhs, rhs)

@@ -168,3 +168,16 @@ def test_synthetic_lora_shapes():
     lo = S.make_lora(cfg, 8)
     assert lo["b1"].shape == (8, cfg.d) and lo["c1"].shape == (cfg.D, 8)
     S.bf16_bits(lo["c1"])  # exactly representable in the storage dtype
+
+
+@pytest.mark.parametrize("act", ACTS)
+def test_rescaling_invariance(orc, act):
+    """y is unchanged under B -> sB, C -> C/s, so <dB, B> = <dC, C> for both
+    projections (used as a full-size GPU check of dB_I and dC_O)."""
+    x, w1, w2, w_r, dy, lo, lg, ti = setup(act, S.GATE_SIGMOID)
+    g = OL.lora_backward(x, w1, w2, w_r, lo, lg, ti, dy, act, S.GATE_SIGMOID)
+    for a, b in (("b1", "c1"), ("b2", "c2")):
+        lhs = float(np.sum(g["d" + a] * np.asarray(lo[a]).reshape(g["d" + a].shape)))
+        rhs = float(np.sum(g["d" + b] * np.asarray(lo[b]).reshape(g["d" + b].shape)))
+        assert abs(lhs - rhs) < 1e-12 * max(1.0, abs(lhs)), (a, lhs, rhs)
+        assert abs(lhs) > 1e-3
