@@ -204,10 +204,12 @@ TOPL_METRIC = "sparse-MHA top-L selection (Alg. 3) queries/s"
 
 def topl_alu_ops(cfg):
     """Algorithmic integer ops of one selection: per (query, candidate key) pair,
-    Eq. 3 costs 10 ALU ops per 4-codebook word (XOR, 3 x shift+OR, AND, POPC, ADD);
-    candidates = n (bidirectional) or q+1 (causal)."""
+    Eq. 3 costs 6 ALU ops per packed code word (XOR, AND, ADD, OR, AND, POPC -- the
+    zero-field test) plus 1 ADD; words = ceil(M / 8) for E <= 16 (nibbles), else
+    ceil(M / 4) (bytes); candidates = n (bidirectional) or q+1 (causal)."""
     pairs = cfg.n * (cfg.n + 1) / 2 if cfg.causal else float(cfg.n) * cfg.n
-    return cfg.heads * pairs * 10.0 * ((cfg.M + 3) // 4)
+    cpw = 8 if cfg.E <= 16 else 4
+    return cfg.heads * pairs * 7.0 * ((cfg.M + cpw - 1) // cpw)
 
 
 def topl_workload(cfg, world):
@@ -267,7 +269,7 @@ def run_topl(args, cfg):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        P.spt_mha_topl(a, b, cfg.L, cfg.causal, out=out)
+        P.spt_mha_topl(a, b, cfg.L, cfg.causal, out=out, n_codewords=cfg.E)
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
@@ -280,7 +282,7 @@ def run_topl(args, cfg):
         flush.fill_(1)  # L2 flush, outside the timed pair
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        P.spt_mha_topl(a, b, cfg.L, cfg.causal, out=out)
+        P.spt_mha_topl(a, b, cfg.L, cfg.causal, out=out, n_codewords=cfg.E)
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize()
@@ -297,7 +299,7 @@ def run_topl(args, cfg):
     for _ in range(args.steps):
         a.copy_(ah, non_blocking=True)
         b.copy_(bh, non_blocking=True)
-        P.spt_mha_topl(a, b, cfg.L, cfg.causal, out=out)
+        P.spt_mha_topl(a, b, cfg.L, cfg.causal, out=out, n_codewords=cfg.E)
         oh.copy_(out, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()

@@ -243,15 +243,19 @@ typedef struct {
   int32_t n_q;         /* queries per head >= 0 */
   int32_t n_k;         /* keys per head >= 0 */
   int32_t n_codebooks; /* M in [1, 31] (the paper: head_dim / 8) */
+  int32_t n_codewords; /* E in [1, 256]: every code is < E (the paper: 16);
+                          E <= 16 packs 8 codes per 32-bit word (half the compare work).
+                          Codes >= E are a caller error (results unspecified, no fault). */
   int32_t top_l;       /* L >= 1 (the paper: lambda n) */
   int32_t causal;      /* 0 | 1: look-ahead mask applied before bucketing */
 } spt_topl_desc;
 
 /* Top-L key indices of every query.  SPT_ERR_INVALID_ARGUMENT: NULL desc, a
- * negative size, M outside [1, 31], L < 1, causal not 0/1, a NULL pointer with
- * a non-empty problem; SPT_ERR_UNSUPPORTED: the key codes of one head plus
- * the per-warp score rows exceed the 227 KB of shared memory of one CTA
- * (n_k (4 ceil(M/4) + 16) bytes), non-sm_100 device.  Asynchronous on stream. */
+ * negative size, M outside [1, 31], E outside [1, 256], L < 1, causal not 0/1,
+ * a NULL pointer with a non-empty problem; SPT_ERR_UNSUPPORTED: the key codes
+ * of one head plus the per-warp score rows exceed the 227 KB of shared memory
+ * of one CTA (n_k (4 ceil(M/c) + 16) bytes, c = 8 codes per word for E <= 16
+ * else 4), non-sm_100 device.  Asynchronous on stream. */
 spt_status spt_mha_topl(const spt_topl_desc* desc, const uint8_t* codes_q, const uint8_t* codes_k,
                         int32_t* indices, void* stream);
 

@@ -49,8 +49,8 @@ class spt_lora_grads(ctypes.Structure):
 
 
 class spt_topl_desc(ctypes.Structure):  # ABI 4: sparse-MHA top-L selection
-    _fields_ = [(n, ctypes.c_int32) for n in ("n_heads", "n_q", "n_k", "n_codebooks", "top_l",
-                                              "causal")]
+    _fields_ = [(n, ctypes.c_int32) for n in ("n_heads", "n_q", "n_k", "n_codebooks",
+                                              "n_codewords", "top_l", "causal")]
 
 
 class SptError(RuntimeError):

@@ -156,10 +156,10 @@ cudaError_t lora_bwd_finish(const Geom& g, const RouteView& r, const Bufs& b, co
                             void* dx, cudaStream_t s);
 
 // sparse-MHA top-L selection (topl.cu, Alg. 3)
-size_t topl_smem_bytes(int nk, int M);
+size_t topl_smem_bytes(int nk, int M, int E);
 int topl_max_score();
-cudaError_t launch_topl(int H, int nq, int nk, int M, int L, int causal, const uint8_t* cq,
-                        const uint8_t* ck, int32_t* out, cudaStream_t s);
+cudaError_t launch_topl(int H, int nq, int nk, int M, int E, int L, int causal,
+                        const uint8_t* cq, const uint8_t* ck, int32_t* out, cudaStream_t s);
 
 // tcgen05 path (tc_ffn.cu), bf16 only
 bool tc_supported(const Geom& g);

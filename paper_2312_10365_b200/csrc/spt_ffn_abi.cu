@@ -510,16 +510,17 @@ spt_status spt_mha_topl(const spt_topl_desc* desc, const uint8_t* codes_q, const
   if (!desc) return SPT_ERR_INVALID_ARGUMENT;
   const spt_topl_desc& d = *desc;
   if (d.n_heads < 0 || d.n_q < 0 || d.n_k < 0 || d.top_l < 1 || d.n_codebooks < 1 ||
-      d.n_codebooks > topl_max_score() || (d.causal != 0 && d.causal != 1))
+      d.n_codebooks > topl_max_score() || d.n_codewords < 1 || d.n_codewords > 256 ||
+      (d.causal != 0 && d.causal != 1))
     return SPT_ERR_INVALID_ARGUMENT;
   const int64_t nout = (int64_t)d.n_heads * d.n_q;
   if (nout == 0) return SPT_OK;
   if (!indices || !codes_q || (d.n_k > 0 && !codes_k)) return SPT_ERR_INVALID_ARGUMENT;
-  if (topl_smem_bytes(d.n_k, d.n_codebooks) > 227 * 1024) return SPT_ERR_UNSUPPORTED;
+  if (topl_smem_bytes(d.n_k, d.n_codebooks, d.n_codewords) > 227 * 1024) return SPT_ERR_UNSUPPORTED;
   spt_status st = device_ok();
   if (st != SPT_OK) return st;
-  return to_status(launch_topl(d.n_heads, d.n_q, d.n_k, d.n_codebooks, d.top_l, d.causal, codes_q,
-                               codes_k, indices, (cudaStream_t)stream));
+  return to_status(launch_topl(d.n_heads, d.n_q, d.n_k, d.n_codebooks, d.n_codewords, d.top_l,
+                               d.causal, codes_q, codes_k, indices, (cudaStream_t)stream));
 }
 
 #pragma GCC visibility pop

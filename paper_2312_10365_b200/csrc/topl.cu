@@ -28,20 +28,37 @@ constexpr int kToplWarps = 16;
 constexpr int kToplThreads = kToplWarps * 32;
 constexpr int kMaxScore = 31;  // M <= 31: M + 1 buckets fit one warp
 
-template <int NW>  // 32-bit code words per vector (M <= 4 NW)
+// Codes are packed CPW per 32-bit word: 4 bytes, or 8 nibbles when every
+// codebook has E <= 16 codewords (the paper's setting: half the
+// words, half the ALU work).
+template <int NW, int CPW>
 __device__ __forceinline__ int score_words(const uint32_t (&q)[NW], const uint32_t* k) {
+  constexpr uint32_t lo = CPW == 4 ? 0x7f7f7f7fu : 0x77777777u;
+  constexpr uint32_t hi = CPW == 4 ? 0x80808080u : 0x88888888u;
   int diff = 0;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
-    const uint32_t v = q[w] ^ k[w];  // byte is 0 iff the codewords agree
-    // high bit of each byte set iff the byte is non-zero (no carry across bytes)
-    const uint32_t t = ((v & 0x7f7f7f7fu) + 0x7f7f7f7fu) | v;
-    diff += __popc(t & 0x80808080u);  // differing codebooks in this word
+    const uint32_t v = q[w] ^ k[w];  // field is 0 iff the codewords agree
+    // top bit of each field set iff the field is non-zero (no carry across fields)
+    const uint32_t t = ((v & lo) + lo) | v;
+    diff += __popc(t & hi);  // differing codebooks in this word
   }
   return diff;
 }
 
-template <int NW>
+template <int CPW>
+__device__ __forceinline__ uint32_t pack_codes(const uint8_t* src, int w, int M) {
+  constexpr int SH = 32 / CPW;
+  uint32_t v = 0;
+#pragma unroll
+  for (int b = 0; b < CPW; ++b) {
+    const int m = w * CPW + b;
+    if (m < M) v |= (uint32_t)src[m] << (SH * b);
+  }
+  return v;
+}
+
+template <int NW, int CPW>
 __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int nk, int M, int L,
                                                            int causal, int qpb,
                                                            const uint8_t* __restrict__ cq,
@@ -51,10 +68,9 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
   constexpr int KW = NW == 3 ? 4 : NW;  // smem words per key (16-byte aligned rows for NW = 3)
   uint32_t* kw = reinterpret_cast<uint32_t*>(smem);                         // [nk][KW]
   uint8_t* sc = smem + (size_t)nk * KW * 4;                                  // [warps][nk]
-  __shared__ int hist[kToplWarps][kMaxScore + 1];
-  __shared__ int last[kToplWarps][kMaxScore + 1];
+  __shared__ __align__(16) uint16_t cnt[kToplWarps][kMaxScore + 1][32];  // per-lane counts
   __shared__ int base[kToplWarps][kMaxScore + 1];
-  __shared__ int take[kToplWarps][kMaxScore + 1];
+  __shared__ int lim[kToplWarps][kMaxScore + 1];   // first keys of the bucket to emit
   __shared__ int seen[kToplWarps][kMaxScore + 1];
 
   // CTA (h, c) takes the queries q = c, c + chunks, c + 2 chunks, ... of head h:
@@ -64,54 +80,33 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
   const int c = blockIdx.x % chunks;
   const int q_last = c + ((nq - 1 - c) / chunks) * chunks;  // this CTA's last query
   const int nk_used = causal ? min(nk, q_last + 1) : nk;   // causal: later keys unused
-  const int pad = NW * 4 - M;                      // zero pad bytes compare equal: subtract
+  const int pad = NW * CPW - M;                    // zero pad fields compare equal: subtract
   // stage the head's key codes: key k -> words [k*KW, k*KW + NW), pad bytes 0
   {
     const uint8_t* src = ck + (size_t)h * nk * M;
     for (int e = threadIdx.x; e < nk_used * KW; e += blockDim.x) {
       const int k = e / KW, w = e % KW;
-      uint32_t v = 0;
-      if (w < NW) {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int m = w * 4 + b;
-          if (m < M) v |= (uint32_t)src[(size_t)k * M + m] << (8 * b);
-        }
-      }
-      kw[e] = v;
+      kw[e] = w < NW ? pack_codes<CPW>(src + (size_t)k * M, w, M) : 0u;
     }
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
+  const unsigned lt = (1u << lane) - 1u;  // lanes below this one
   uint8_t* my = sc + (size_t)warp * nk;
   for (int q = c + warp * chunks; q < nq; q += kToplWarps * chunks) {
     uint32_t qv[NW];
     {
       const uint8_t* src = cq + ((size_t)h * nq + q) * M;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        uint32_t v = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int m = w * 4 + b;
-          if (m < M) v |= (uint32_t)__ldg(src + m) << (8 * b);
-        }
-        qv[w] = v;
-      }
+      for (int w = 0; w < NW; ++w) qv[w] = pack_codes<CPW>(src, w, M);
     }
     const int nc = causal ? min(nk, q + 1) : nk;  // candidates (c23)
-    if (lane <= M) {
-      hist[warp][lane] = 0;
-      seen[warp][lane] = 0;
-    }
-    __syncwarp();
-    // pass 1 (Alg. 3 lines 3-8): scores, bucket counts, last key per bucket
+    for (int v = 0; v <= M; ++v) cnt[warp][v][lane] = 0;  // this lane's column
+    // pass 1 (Alg. 3 lines 3-8): scores and bucket counts (per lane, no
+    // cross-lane traffic: every lane counts the keys it scored)
     for (int k0 = 0; k0 < nc; k0 += 32) {
       const int k = k0 + lane;
-      const bool ok = k < nc;
-      int s = -1;
-      if (ok) {
+      if (k < nc) {
         uint32_t kv[KW];
         if (KW == 4) {
           const uint4 t = *reinterpret_cast<const uint4*>(kw + (size_t)k * KW);
@@ -123,24 +118,29 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
 #pragma unroll
           for (int w = 0; w < KW; ++w) kv[w] = kw[(size_t)k * KW + w];
         }
-        s = NW * 4 - pad - score_words<NW>(qv, kv);  // Eq. 3
+        const int s = NW * CPW - pad - score_words<NW, CPW>(qv, kv);  // Eq. 3
         my[k] = (uint8_t)s;
+        cnt[warp][s][lane] += 1;
       }
-      const unsigned act = __ballot_sync(0xffffffffu, ok);
-      if (ok) {
-        const unsigned grp = __match_any_sync(act, s);
-        if ((grp & lt) == 0) {  // group leader: lowest lane of this score value
-          hist[warp][s] += __popc(grp);
-          last[warp][s] = k0 + 31 - __clz(grp);  // highest key of the group so far
-        }
-      }
-      __syncwarp();  // leaders' hist / last updates visible to the next chunk's leaders
     }
+    __syncwarp();
     // Alg. 3 lines 9-16 as a scan: bucket M first; bucket s is read for
     // min(count, L) slots (c21) until L keys are collected (c20)
+    int s_over = -1;  // the bucket read to its slot L-1 (holds its last key), if any
+    int remaining;    // keys pass 2 must place
     {
       const int s = M - lane;  // lane 0 = bucket M
-      const int rd = s >= 0 ? min(hist[warp][s], L) : 0;
+      int count = 0;
+      if (s >= 0) {
+        const uint4* row = reinterpret_cast<const uint4*>(&cnt[warp][s][0]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 v = row[i];
+          count += (int)(v.x & 0xffff) + (int)(v.x >> 16) + (int)(v.y & 0xffff) + (int)(v.y >> 16) +
+                   (int)(v.z & 0xffff) + (int)(v.z >> 16) + (int)(v.w & 0xffff) + (int)(v.w >> 16);
+        }
+      }
+      const int rd = min(count, L);
       int inc = rd;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -148,78 +148,114 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
         if (lane >= o) inc += v;
       }
       const int b = inc - rd;
+      const int take = max(0, min(rd, L - b));
+      const int lm = min(take, L - 1);  // slot L-1 is written separately
       if (s >= 0) {
         base[warp][s] = b;
-        take[warp][s] = max(0, min(rd, L - b));
+        lim[warp][s] = lm;
+        seen[warp][s] = 0;
       }
+      const unsigned ov = __ballot_sync(0xffffffffu, s >= 0 && take == L);
+      if (ov) s_over = M - (__ffs(ov) - 1);
+      remaining = lm;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) remaining += __shfl_xor_sync(0xffffffffu, remaining, o);
     }
     __syncwarp();
     int32_t* orow = out + ((size_t)h * nq + q) * L;
     // rows with fewer than L candidates: pad (c23)
     for (int i = min(nc, L) + lane; i < L; i += 32) orow[i] = -1;
-    // slot L-1 of a bucket read to its end holds its last key (line 7 overwrite)
-    if (lane <= M && take[warp][lane] == L) orow[base[warp][lane] + L - 1] = last[warp][lane];
-    // pass 2: first keys of each bucket in key order -> positions base + rank
-    for (int k0 = 0; k0 < nc; k0 += 32) {
+    // slot L-1 of the bucket read to its end holds its last key (line 7 overwrite):
+    // the highest key of that score, found scanning back from the end
+    if (s_over >= 0) {
+      for (int k0 = ((nc - 1) / 32) * 32; k0 >= 0; k0 -= 32) {
+        const int k = k0 + lane;
+        const unsigned hit = __ballot_sync(0xffffffffu, k < nc && (int)my[k] == s_over);
+        if (hit) {
+          if (lane == 0) orow[base[warp][s_over] + L - 1] = k0 + 31 - __clz(hit);
+          break;
+        }
+      }
+    }
+    // pass 2: the first keys of each bucket, in key order, to base + rank; lanes
+    // whose bucket is already placed (or not read) drop out before any ranking
+    for (int k0 = 0; k0 < nc && remaining > 0; k0 += 32) {
       const int k = k0 + lane;
-      const bool ok = k < nc;
-      const int s = ok ? (int)my[k] : -1;
-      const unsigned act = __ballot_sync(0xffffffffu, ok);
-      if (ok) {
-        const unsigned grp = __match_any_sync(act, s);
+      const int s = k < nc ? (int)my[k] : 0;
+      const bool need = k < nc && seen[warp][s] < lim[warp][s];
+      const unsigned cand = __ballot_sync(0xffffffffu, need);
+      if (!cand) continue;
+      unsigned put = 0;
+      if (need) {
+        const unsigned grp = __match_any_sync(cand, s);
         const int pos = seen[warp][s] + __popc(grp & lt);
-        const int lim = min(take[warp][s], L - 1);  // slot L-1 handled above
-        if (pos < lim) orow[base[warp][s] + pos] = k;
-        __syncwarp(act);
+        const bool w = pos < lim[warp][s];
+        if (w) orow[base[warp][s] + pos] = k;
+        put = __ballot_sync(cand, w);
+        __syncwarp(cand);
         if ((grp & lt) == 0) seen[warp][s] += __popc(grp);
       }
+      remaining -= __popc(__shfl_sync(0xffffffffu, put, __ffs(cand) - 1));
       __syncwarp();
     }
     __syncwarp();
   }
 }
 
-template <int NW>
+template <int NW, int CPW>
 cudaError_t launch_topl_nw(int H, int nq, int nk, int M, int L, int causal, const uint8_t* cq,
                            const uint8_t* ck, int32_t* out, size_t smem, int qpb, cudaStream_t s) {
   const int chunks = (nq + qpb - 1) / qpb;
-  cudaError_t e = cudaFuncSetAttribute(topl_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(topl_kernel<NW, CPW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  topl_kernel<NW><<<(unsigned)((int64_t)H * chunks), kToplThreads, smem, s>>>(H, nq, nk, M, L,
-                                                                             causal, qpb, cq, ck, out);
+  topl_kernel<NW, CPW><<<(unsigned)((int64_t)H * chunks), kToplThreads, smem, s>>>(
+      H, nq, nk, M, L, causal, qpb, cq, ck, out);
   return cudaGetLastError();
 }
 
+int code_fields(int E) { return E <= 16 ? 8 : 4; }
+
 }  // namespace
 
-size_t topl_smem_bytes(int nk, int M) {
-  const int NW = (M + 3) / 4;
+size_t topl_smem_bytes(int nk, int M, int E) {
+  const int cpw = code_fields(E);
+  const int NW = (M + cpw - 1) / cpw;
   const int KW = NW == 3 ? 4 : NW;
   return (size_t)nk * KW * 4 + (size_t)kToplWarps * nk;
 }
 
 int topl_max_score() { return kMaxScore; }
 
-cudaError_t launch_topl(int H, int nq, int nk, int M, int L, int causal, const uint8_t* cq,
-                        const uint8_t* ck, int32_t* out, cudaStream_t s) {
-  const size_t smem = topl_smem_bytes(nk, M);
-  // queries per CTA: enough CTAs to fill the SMs, each staging its head's keys once
+cudaError_t launch_topl(int H, int nq, int nk, int M, int E, int L, int causal,
+                        const uint8_t* cq, const uint8_t* ck, int32_t* out, cudaStream_t s) {
+  const size_t smem = topl_smem_bytes(nk, M, E);
+  // queries per CTA: >= 8 waves of 2 CTAs per SM (small tail), each CTA
+  // staging its head's keys once
   int qpb = 64;
-  while (qpb < 1024 && (int64_t)H * ((nq + 2 * qpb - 1) / (2 * qpb)) >= 2 * 148) qpb *= 2;
+  while (qpb < 1024 && (int64_t)H * ((nq + 2 * qpb - 1) / (2 * qpb)) >= 8 * 2 * 148) qpb *= 2;
   prof_begin("topl_select", s);
-  const int NW = (M + 3) / 4;
+  const int cpw = code_fields(E);
+  const int NW = (M + cpw - 1) / cpw;
   cudaError_t e;
+#define TOPL_CASE(nw)                                                                       \
+  case nw:                                                                                  \
+    e = cpw == 8 ? launch_topl_nw<nw, 8>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s) \
+                 : launch_topl_nw<nw, 4>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s); \
+    break;
   switch (NW) {
-    case 1: e = launch_topl_nw<1>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s); break;
-    case 2: e = launch_topl_nw<2>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s); break;
-    case 3: e = launch_topl_nw<3>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s); break;
-    case 4: e = launch_topl_nw<4>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s); break;
-    case 5: e = launch_topl_nw<5>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s); break;
-    case 6: e = launch_topl_nw<6>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s); break;
-    case 7: e = launch_topl_nw<7>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s); break;
-    default: e = launch_topl_nw<8>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s); break;
+    TOPL_CASE(1)
+    TOPL_CASE(2)
+    TOPL_CASE(3)
+    TOPL_CASE(4)
+    TOPL_CASE(5)
+    TOPL_CASE(6)
+    TOPL_CASE(7)
+    default:
+      e = launch_topl_nw<8, 4>(H, nq, nk, M, L, causal, cq, ck, out, smem, qpb, s);
+      break;
   }
+#undef TOPL_CASE
   prof_end(s);
   count_launch();
   return e;

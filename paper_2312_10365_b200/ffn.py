@@ -143,9 +143,11 @@ def spt_ffn_lora_backward(desc, x, w1, w2, w_r, lora: dict, route: RouteBuffers,
         ws.numel() * ws.element_size(), ev, _stream(stream)))
 
 
-def spt_mha_topl(codes_q, codes_k, top_l: int, causal: bool = False, out=None, stream=None):
+def spt_mha_topl(codes_q, codes_k, top_l: int, causal: bool = False, out=None, stream=None,
+                 n_codewords: int = 256):
     """Sparse-MHA top-L selection (ABI 4; Alg. 3 over PQ codes, Eq. 3).
-    codes_q [H, n_q, M], codes_k [H, n_k, M] uint8 device tensors; returns
+    codes_q [H, n_q, M], codes_k [H, n_k, M] uint8 device tensors with every code
+    < n_codewords (E; the paper's 16 enables the packed path); returns
     indices [H, n_q, L] int32 (-1 = fewer than L candidates, causal rows)."""
     H, nq, M = codes_q.shape
     nk = codes_k.shape[1]
@@ -155,7 +157,8 @@ def spt_mha_topl(codes_q, codes_k, top_l: int, causal: bool = False, out=None, s
         raise ValueError("codes_q / codes_k disagree on heads or codebooks")
     if out is None:
         out = torch.empty(H, nq, int(top_l), dtype=torch.int32, device=codes_q.device)
-    d = L.spt_topl_desc(int(H), int(nq), int(nk), int(M), int(top_l), 1 if causal else 0)
+    d = L.spt_topl_desc(int(H), int(nq), int(nk), int(M), int(n_codewords), int(top_l),
+                        1 if causal else 0)
     L.check("spt_mha_topl", L.lib().spt_mha_topl(ctypes.byref(d), _p(codes_q), _p(codes_k), _p(out),
                                                  _stream(stream)))
     return out

@@ -157,10 +157,11 @@ def test_lora_null_pointers_rejected_before_any_launch():
 
 # ------------------------------------------------------------ top-L (ABI 4)
 @pytest.mark.parametrize("kw", [dict(n_codebooks=0), dict(n_codebooks=32), dict(top_l=0),
-                                dict(n_heads=-1), dict(n_q=-2), dict(causal=2)])
+                                dict(n_heads=-1), dict(n_q=-2), dict(causal=2),
+                                dict(n_codewords=0), dict(n_codewords=257)])
 def test_topl_invalid_arguments(kw):
     from paper_2312_10365_b200 import _lib
-    a = dict(n_heads=2, n_q=8, n_k=8, n_codebooks=8, top_l=2, causal=0)
+    a = dict(n_heads=2, n_q=8, n_k=8, n_codebooks=8, n_codewords=16, top_l=2, causal=0)
     a.update(kw)
     d = _lib.spt_topl_desc(**a)
     dummy = ctypes.c_void_p(16)  # never dereferenced: validation fails first
@@ -170,11 +171,11 @@ def test_topl_invalid_arguments(kw):
 def test_topl_null_and_unsupported():
     from paper_2312_10365_b200 import _lib
     L = _lib.lib()
-    d = _lib.spt_topl_desc(2, 8, 8, 8, 2, 0)
+    d = _lib.spt_topl_desc(2, 8, 8, 8, 16, 2, 0)
     assert L.spt_mha_topl(ctypes.byref(d), None, None, None, None) == 1
     assert L.spt_mha_topl(None, None, None, None, None) == 1
-    big = _lib.spt_topl_desc(1, 8, 20000, 16, 4, 0)  # 20000 keys x 32 B > 227 KB smem
+    big = _lib.spt_topl_desc(1, 8, 20000, 16, 256, 4, 0)  # 20000 keys x 32 B > 227 KB smem
     dummy = ctypes.c_void_p(16)
     assert L.spt_mha_topl(ctypes.byref(big), dummy, dummy, dummy, None) == 2
-    empty = _lib.spt_topl_desc(0, 8, 8, 8, 2, 0)
+    empty = _lib.spt_topl_desc(0, 8, 8, 8, 16, 2, 0)
     assert L.spt_mha_topl(ctypes.byref(empty), None, None, None, None) == 0

@@ -16,25 +16,34 @@ from oracle import topl as OT
 pytestmark = pytest.mark.gpu
 
 
-def gpu_topl(cq, ck, L, causal=False):
+def gpu_topl(cq, ck, L, causal=False, E=None):
+    """E: codewords per codebook (default: max code + 1 -> the packed path when <= 16)."""
     import torch
     import paper_2312_10365_b200 as P
     a = torch.from_numpy(np.ascontiguousarray(cq, np.uint8)).cuda()
     b = torch.from_numpy(np.ascontiguousarray(ck, np.uint8)).cuda()
-    out = P.spt_mha_topl(a, b, L, causal)
+    if E is None:
+        E = int(max(np.max(cq, initial=0), np.max(ck, initial=0))) + 1
+    out = P.spt_mha_topl(a, b, L, causal, n_codewords=E)
     torch.cuda.synchronize()
     return out.cpu().numpy()
 
 
+@pytest.mark.parametrize("E", [3, 16, 200])   # packed nibbles (E <= 16) and bytes
 @pytest.mark.parametrize("M", [1, 3, 4, 8, 13, 16, 31])
 @pytest.mark.parametrize("causal", [False, True])
-def test_step_by_step_small(M, causal):
+def test_step_by_step_small(M, causal, E):
     rng = np.random.default_rng(M)
     H, n = 2, 77
-    cq = rng.integers(0, 3, (H, n, M)).astype(np.uint8)
-    ck = cq if causal else rng.integers(0, 3, (H, n, M)).astype(np.uint8)
+    hi = 3 if E == 3 else E  # E = 3: heavy ties; 16 / 200: the full code range
+    cq = rng.integers(0, hi, (H, n, M)).astype(np.uint8)
+    ck = cq if causal else rng.integers(0, hi, (H, n, M)).astype(np.uint8)
+    if E == 200:  # bytes path: also put equal codes where nibbles would alias (x vs x + 16)
+        cq[..., 0] = 17
+        if not causal:
+            ck[..., 0] = rng.choice([1, 17], size=ck.shape[:2])
     for L in (1, 2, 9, 40, 100):
-        got = gpu_topl(cq, ck, L, causal)
+        got = gpu_topl(cq, ck, L, causal, E=E)
         for h in range(H):
             ref = OT.alg3_topl(cq[h], ck[h], L, causal)
             assert np.array_equal(got[h], ref), (M, causal, L, h)
