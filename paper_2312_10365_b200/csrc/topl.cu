@@ -69,9 +69,8 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
   uint32_t* kw = reinterpret_cast<uint32_t*>(smem);                         // [nk][KW]
   uint8_t* sc = smem + (size_t)nk * KW * 4;                                  // [warps][nk]
   __shared__ __align__(16) uint16_t cnt[kToplWarps][kMaxScore + 1][32];  // per-lane counts
-  __shared__ int base[kToplWarps][kMaxScore + 1];
-  __shared__ int lim[kToplWarps][kMaxScore + 1];   // first keys of the bucket to emit
-  __shared__ int seen[kToplWarps][kMaxScore + 1];
+  // per bucket: {keys still to place, first keys to place, output base, -}
+  __shared__ int4 bk[kToplWarps][kMaxScore + 1];
 
   // CTA (h, c) takes the queries q = c, c + chunks, c + 2 chunks, ... of head h:
   // interleaved, so causal rows (work ~ q) are balanced across CTAs
@@ -103,26 +102,30 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
     const int nc = causal ? min(nk, q + 1) : nk;  // candidates (c23)
     for (int v = 0; v <= M; ++v) cnt[warp][v][lane] = 0;  // this lane's column
     // pass 1 (Alg. 3 lines 3-8): scores and bucket counts (per lane, no
-    // cross-lane traffic: every lane counts the keys it scored)
-    for (int k0 = 0; k0 < nc; k0 += 32) {
-      const int k = k0 + lane;
-      if (k < nc) {
-        uint32_t kv[KW];
-        if (KW == 4) {
-          const uint4 t = *reinterpret_cast<const uint4*>(kw + (size_t)k * KW);
-          kv[0] = t.x; kv[1] = t.y; kv[2] = t.z; kv[3] = t.w;
-        } else if (KW == 2) {
-          const uint2 t = *reinterpret_cast<const uint2*>(kw + (size_t)k * KW);
-          kv[0] = t.x; kv[1] = t.y;
-        } else {
+    // cross-lane traffic: every lane counts the keys it scored).  Full 32-key
+    // batches run unguarded; the ragged tail once.
+    const int full_score = NW * CPW - pad;
+    uint16_t* mycnt = &cnt[warp][0][lane];
+    auto score_key = [&](int k) {
+      uint32_t kv[KW];
+      if (KW == 4) {
+        const uint4 t = *reinterpret_cast<const uint4*>(kw + k * KW);
+        kv[0] = t.x; kv[1] = t.y; kv[2] = t.z; kv[3] = t.w;
+      } else if (KW == 2) {
+        const uint2 t = *reinterpret_cast<const uint2*>(kw + k * KW);
+        kv[0] = t.x; kv[1] = t.y;
+      } else {
 #pragma unroll
-          for (int w = 0; w < KW; ++w) kv[w] = kw[(size_t)k * KW + w];
-        }
-        const int s = NW * CPW - pad - score_words<NW, CPW>(qv, kv);  // Eq. 3
-        my[k] = (uint8_t)s;
-        cnt[warp][s][lane] += 1;
+        for (int w = 0; w < KW; ++w) kv[w] = kw[k * KW + w];
       }
-    }
+      const int s = full_score - score_words<NW, CPW>(qv, kv);  // Eq. 3
+      my[k] = (uint8_t)s;
+      mycnt[s * 32] += 1;
+    };
+    const int nfull = nc & ~31;
+#pragma unroll 4
+    for (int k0 = 0; k0 < nfull; k0 += 32) score_key(k0 + lane);
+    if (nfull + lane < nc) score_key(nfull + lane);
     __syncwarp();
     // Alg. 3 lines 9-16 as a scan: bucket M first; bucket s is read for
     // min(count, L) slots (c21) until L keys are collected (c20)
@@ -150,11 +153,7 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
       const int b = inc - rd;
       const int take = max(0, min(rd, L - b));
       const int lm = min(take, L - 1);  // slot L-1 is written separately
-      if (s >= 0) {
-        base[warp][s] = b;
-        lim[warp][s] = lm;
-        seen[warp][s] = 0;
-      }
+      if (s >= 0) bk[warp][s] = make_int4(lm, lm, b, 0);
       const unsigned ov = __ballot_sync(0xffffffffu, s >= 0 && take == L);
       if (ov) s_over = M - (__ffs(ov) - 1);
       remaining = lm;
@@ -172,7 +171,7 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
         const int k = k0 + lane;
         const unsigned hit = __ballot_sync(0xffffffffu, k < nc && (int)my[k] == s_over);
         if (hit) {
-          if (lane == 0) orow[base[warp][s_over] + L - 1] = k0 + 31 - __clz(hit);
+          if (lane == 0) orow[bk[warp][s_over].z + L - 1] = k0 + 31 - __clz(hit);
           break;
         }
       }
@@ -182,18 +181,19 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
     for (int k0 = 0; k0 < nc && remaining > 0; k0 += 32) {
       const int k = k0 + lane;
       const int s = k < nc ? (int)my[k] : 0;
-      const bool need = k < nc && seen[warp][s] < lim[warp][s];
+      const int4 e = bk[warp][s];
+      const bool need = k < nc && e.x > 0;
       const unsigned cand = __ballot_sync(0xffffffffu, need);
       if (!cand) continue;
       unsigned put = 0;
       if (need) {
         const unsigned grp = __match_any_sync(cand, s);
-        const int pos = seen[warp][s] + __popc(grp & lt);
-        const bool w = pos < lim[warp][s];
-        if (w) orow[base[warp][s] + pos] = k;
+        const int rank = __popc(grp & lt);
+        const bool w = rank < e.x;
+        if (w) orow[e.z + (e.y - e.x) + rank] = k;
         put = __ballot_sync(cand, w);
         __syncwarp(cand);
-        if ((grp & lt) == 0) seen[warp][s] += __popc(grp);
+        if ((grp & lt) == 0) bk[warp][s].x = e.x - __popc(grp);
       }
       remaining -= __popc(__shfl_sync(0xffffffffu, put, __ffs(cand) - 1));
       __syncwarp();
