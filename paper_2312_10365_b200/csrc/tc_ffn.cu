@@ -1439,6 +1439,7 @@ static int num_sms() {
   }
   return n;
 }
+static int gemm_sms() { return num_sms(); }
 
 // SPT_FFN_TRACE=1: per-CTA role cycle counters (slots: kTraceSlots above),
 // summed over the grid and printed after a synchronising readback
@@ -1508,7 +1509,7 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int grid = std::max(1, std::min(tiles_upper, num_sms()));
+  const int grid = std::max(1, std::min(tiles_upper, gemm_sms()));
   static const char* kNames[] = {"tc_router", "tc_fwd1_gate_up", "tc_fwd2_down", "tc_bwd_dA",
                                  "tc_bwd_dX", "tc_bwd_dW1", "tc_bwd_dW2", "tc_bwd_dWR",
                                  "tc_bwd_dAT", "tc_bwd_dXR"};
@@ -2153,51 +2154,49 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   if (lo) {  // W frozen: the LoRA factor gradients dC_I, dB_O from dZ, h~ (no dW1 / dW2)
     if ((e0 = lora_bwd_grads(g, r, b, *lo, s)) != cudaSuccess) return e0;
   }
-  if (!lo) {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features: <= 2 halves, or 256-feature tiles)
-    TcArgs a{};
-    base_args(a, g, r);
-    bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
-                                (uint64_t)g.mp * g.bw, 64, kind_bk(K_DW1)) &&
-              make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 1);
-    a.BN = 256;
-    a.MH = (int)std::min<int64_t>(2, ceil_div(g.mp * g.bw, 128));
-    a.nu = (int)ceil_div(g.mp * g.bw, 256);
-    a.aux2 = x;
-    a.out = dw1;
-    a.acc_mode = accumulate;
-    TRY(launch<K_DW1>(a, g.G * a.nu * a.NT, s));
-  }
-  if (!lo) {  // a9: dW2_b = H~_b^T dY[bucket_b]
-    TcArgs a{};
-    base_args(a, g, r);
-    bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, kind_bk(K_DW2)) &&
-              make_tmap_bf16_2d(&a.tb, dy, g.T, g.d, g.d, 64, 1);
-    a.BN = 256;
-    a.MH = (int)std::min<int64_t>(2, ceil_div(g.bw, 128));
-    a.nu = (int)ceil_div(g.bw, 256);
-    a.aux2 = dy;
-    a.out = dw2;
-    a.acc_mode = accumulate;
-    TRY(launch<K_DW2>(a, g.G * a.nu * a.NT, s));
-  }
-  // f2: + lambda dL_balance/dx_R for every (token, block), into the dense dlogits
-  if (lb) {
-    cudaError_t e = launch_balance_grad(g, r, b.dlg, nullptr, s);
-    if (e != cudaSuccess) return e;
-  }
-  // a10: dW_R = dLogits^T X  (split-K, hi + lo bf16 halves of dlogit)
-  if (sig || lb) {
-    cudaError_t e = tc_dense_tn(g, b.dlg, x, b.dwr_part, b.n_split, dw_r, accumulate, s);
-    if (e != cudaSuccess) return e;
-  } else if (!accumulate) {
-    if (cudaMemsetAsync(dw_r, 0, (size_t)g.G * g.d * 4, s) != cudaSuccess) return cudaErrorUnknown;
-  }
-  // all of dw1 | dw2 | dw_r are final here: a data-parallel caller can start the
-  // gradient all-reduce at this event while dX is computed below
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  if (!lo && dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
-  {  // a8: dXp = dZ W1_b, then combine with the router term
+  auto run_dw = [&]() -> cudaError_t {
+    {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features: <= 2 halves, or 256-feature tiles)
+      TcArgs a{};
+      base_args(a, g, r);
+      bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
+                                  (uint64_t)g.mp * g.bw, 64, kind_bk(K_DW1)) &&
+                make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 1);
+      a.BN = 256;
+      a.MH = (int)std::min<int64_t>(2, ceil_div(g.mp * g.bw, 128));
+      a.nu = (int)ceil_div(g.mp * g.bw, 256);
+      a.aux2 = x;
+      a.out = dw1;
+      a.acc_mode = accumulate;
+      TRY(launch<K_DW1>(a, g.G * a.nu * a.NT, s));
+    }
+    {  // a9: dW2_b = H~_b^T dY[bucket_b]
+      TcArgs a{};
+      base_args(a, g, r);
+      bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, kind_bk(K_DW2)) &&
+                make_tmap_bf16_2d(&a.tb, dy, g.T, g.d, g.d, 64, 1);
+      a.BN = 256;
+      a.MH = (int)std::min<int64_t>(2, ceil_div(g.bw, 128));
+      a.nu = (int)ceil_div(g.bw, 256);
+      a.aux2 = dy;
+      a.out = dw2;
+      a.acc_mode = accumulate;
+      TRY(launch<K_DW2>(a, g.G * a.nu * a.NT, s));
+    }
+    return cudaSuccess;
+  };
+  auto run_dwr = [&]() -> cudaError_t {
+    // f2: + lambda dL_balance/dx_R for every (token, block), into the dense dlogits
+    if (lb) {
+      cudaError_t e = launch_balance_grad(g, r, b.dlg, nullptr, s);
+      if (e != cudaSuccess) return e;
+    }
+    // a10: dW_R = dLogits^T X  (split-K, hi + lo bf16 halves of dlogit)
+    if (sig || lb) return tc_dense_tn(g, b.dlg, x, b.dwr_part, b.n_split, dw_r, accumulate, s);
+    if (!accumulate && cudaMemsetAsync(dw_r, 0, (size_t)g.G * g.d * 4, s) != cudaSuccess)
+      return cudaErrorUnknown;
+    return cudaSuccess;
+  };
+  auto run_dx = [&]() -> cudaError_t {  // a8: dXp = dZ W1_b (partials)
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
@@ -2213,7 +2212,17 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     } else {
       TRY(launch_bres<K_DX>(a, units_upper(g), s));
     }
-  }
+    return cudaSuccess;
+  };
+  cudaError_t e;
+  if (!lo && (e = run_dw()) != cudaSuccess) return e;
+  if ((e = run_dwr()) != cudaSuccess) return e;
+  // all of dw1 | dw2 | dw_r are final here: a data-parallel caller can start the
+  // gradient all-reduce at this event while dX is computed below
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (!lo && dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
+  if ((e = run_dx()) != cudaSuccess) return e;
   if (lb) {
     // router term of dx from the dense dlogits (task + balance): dXR = dLogits W_R
     TcArgs a{};
