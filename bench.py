@@ -348,6 +348,48 @@ def workload_config(cfg, world, T, balance_weight=0.0, lora=0):
 
 
 # ------------------------------------------------------- dense context
+def dense_lora_context(cfg, x, w1, w2, dy, lora, ms_routed, iters=5, warmup=2):
+    """The dense LoRA FFN fwd+bwd at the same shape through cuBLAS (torch.matmul,
+    W frozen: backward = dX + the LoRA factor gradients, no dW) -- the B200
+    analogue of the paper's own comparison, LoRA vs SPT (Table 1's FFN time
+    128.8 -> 54.9 ms, Table 5).  Context only: not this library's path."""
+    import torch
+    import torch.nn.functional as F
+    D, mp = cfg.D, cfg.mprime
+    w1 = w1.reshape(-1, cfg.d)                              # [m'D, d]
+    b1 = lora["b1"].reshape(mp, -1, cfg.d)                  # [m', r, d]
+    c1 = lora["c1"].reshape(mp, D, -1)                      # [m', D, r]
+    b2, c2 = lora["b2"], lora["c2"]
+
+    def act(z):
+        if cfg.act == S.ACT_SWIGLU:
+            return F.silu(z[:, :D]) * z[:, D:]
+        return F.relu(z) if cfg.act == S.ACT_RELU else F.gelu(z)
+
+    def step():
+        xr = x.detach().requires_grad_(True)
+        fac = [t.detach().requires_grad_(True) for t in (b1, c1, b2, c2)]
+        B1, C1, B2, C2 = fac
+        z = xr @ w1.t() + torch.cat([(xr @ B1[m].t()) @ C1[m].t() for m in range(mp)], dim=1)
+        h = act(z)
+        y = h @ w2 + (h @ B2) @ C2
+        torch.autograd.grad(y, [xr] + fac, dy)
+
+    for _ in range(warmup):
+        step()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    return {"ms_per_step": ms, "routed_speedup": ms / ms_routed, "ideal_speedup": cfg.G / cfg.k,
+            "what": "dense LoRA FFN fwd+bwd (torch autograd on cuBLAS bf16; W frozen: dX + LoRA "
+                    "factor grads), same T, d, D, rank"}
+
+
 def dense_context(cfg, x, w1, w2, dy, ms_routed, iters=5, warmup=2):
     """the dense FFN fwd+bwd at the same shape through cuBLAS
     (torch.matmul, bf16 in / fp32 accumulate) + torch elementwise activation --
@@ -600,7 +642,8 @@ def main():
     }
     if world == 1 and not args.no_dense and cfg.dtype == "bf16":
         try:
-            out["dense_context"] = dense_context(cfg, x, w1, w2, dy, ms_max)
+            out["dense_context"] = (dense_lora_context(cfg, x, w1, w2, dy, lora, ms_max) if lora
+                                    else dense_context(cfg, x, w1, w2, dy, ms_max))
         except Exception as ex:  # e.g. out of memory: context only
             out["dense_context"] = {"error": str(ex)[:200]}
     if world == 1 and not args.no_cpu_baseline:
