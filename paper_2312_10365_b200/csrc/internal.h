@@ -129,7 +129,8 @@ struct LoraArgs {
   void* xaug;    // [T, d+ka] bf16: fwd X_aug, bwd dY_aug
   void* waug;    // [m'D, d+ka] bf16: fwd W1_aug, bwd W2_aug
   float* uv;     // [T, m'r] f32: fwd U = x B_I, bwd V = dy C_O^T ([T, r])
-  float* rowp;   // [rows_cap, 64] f32 per pair: fwd q rows (h~ B_O[b]), bwd du rows (dZ C_I[b])
+  float* rowp;   // [chunks, rows_cap, 64] f32 per pair and 128-feature chunk: fwd q rows
+                 // (h~ B_O[b]), bwd du rows (dZ C_I[b]); summed over chunks by the token reduce
   float* gpart;  // [tiles, m'+1, bw, r] f32 per-tile partials of dC_I (m' slabs) and dB_O
   float* spart;  // split-K partials of dB_I / dC_O
   int n_split_u, n_split_v;
@@ -139,6 +140,9 @@ struct LoraArgs {
   void* qhl;     // [2, T, qpad] bf16 (hi, lo) q = sum_b h~ B_O[b] for the dC_O GEMM
 };
 inline int lora_upad(const Geom& g, int r) { return (int)ceil_div(g.mp * r, 16) * 16; }
+// per-pair rank-r rows are produced per 128-feature chunk of a block
+inline int lora_chunks(const Geom& g) { return (int)ceil_div(g.bw, 128); }
+inline int64_t lora_rows_stride(const Geom& g) { return g.rows_cap * kLoraK; }
 inline int lora_qpad(int r) { return (int)ceil_div(r, 16) * 16; }
 
 cudaError_t lora_fwd_prep(const Geom& g, const void* x, const void* w1, const LoraArgs& lo,

@@ -268,6 +268,9 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// Grid: (tile, 128-feature chunk of the block); each chunk writes its own
+// partial row products (summed by the token reduce), so wide blocks
+// (bw = 1024-2752) spread over bw/128 CTAs per tile.
 // mode 0 (forward): rows only, A = h~ (m' = 1), P = B_O  -> q rows
 // mode 1 (backward): A = dZ: rows (P = C_I^T -> du rows) and cols (E = u -> dC_I);
 //                    then A = h~: cols (E = v -> dB_O)
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
     const int32_t* __restrict__ tile_block, const __nv_bfloat16* __restrict__ A,
     const __nv_bfloat16* __restrict__ P, const float* __restrict__ U, int upitch,
     const __nv_bfloat16* __restrict__ H, const float* __restrict__ V, float* __restrict__ rows_out,
-    float* __restrict__ part) {
+    int64_t rows_stride, float* __restrict__ part) {
   constexpr int NT = RP / 8;  // n8 tiles
   extern __shared__ __align__(16) uint8_t mma_smem[];
   __nv_bfloat16* As = reinterpret_cast<__nv_bfloat16*>(mma_smem);   // [row][feature]
@@ -371,7 +374,8 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
       __syncthreads();
       stage_e(U, upitch, m * r);
     }
-    for (int i0 = 0; i0 < bw; i0 += kMmaChunk) {
+    {  // this CTA's 128-feature chunk (blockIdx.y) of the block
+      const int i0 = blockIdx.y * kMmaChunk;
       const int ni = min(kMmaChunk, bw - i0);
       __syncthreads();
       stage_a(Arow, aw, m * bw + i0, ni);
@@ -396,13 +400,14 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
       if (mode == 1)  // dC_I^T rows [b bw + i0, +ni) of slab m
         cols(ni, part + (((int64_t)tile * (mp + 1) + m) * bw + i0) * r);
     }
-    // rows out: [prow, m r + q]
+    // rows out: [chunk][prow, m r + q] (the chunks' partial sums, added by the token reduce)
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
       const int q0 = n * 8 + 2 * c;
       const int row = warp * 16 + g;
-      float* o0 = rows_out + (prow0 + row) * kLoraK + m * r;
-      float* o1 = rows_out + (prow0 + row + 8) * kLoraK + m * r;
+      float* rb = rows_out + blockIdx.y * rows_stride;
+      float* o0 = rb + (prow0 + row) * kLoraK + m * r;
+      float* o1 = rb + (prow0 + row + 8) * kLoraK + m * r;
       if (row < nvalid) {
         if (q0 < r) o0[q0] = racc[n][0];
         if (q0 + 1 < r) o0[q0 + 1] = racc[n][1];
@@ -416,7 +421,8 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
   if (mode == 1) {  // dB_O: A = h~, E = v
     __syncthreads();
     stage_e(V, r, 0);
-    for (int i0 = 0; i0 < bw; i0 += kMmaChunk) {
+    {
+      const int i0 = blockIdx.y * kMmaChunk;
       const int ni = min(kMmaChunk, bw - i0);
       __syncthreads();
       stage_a(H, bw, i0, ni);
@@ -431,6 +437,7 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
 __global__ void __launch_bounds__(256) lora_token_reduce_kernel(int64_t T, int k, int ns,
                                                                 int spitch, RouteView r,
                                                                 const float* __restrict__ rowp,
+                                                                int nch, int64_t rows_stride,
                                                                 __nv_bfloat16* __restrict__ shl) {
   const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -438,7 +445,10 @@ __global__ void __launch_bounds__(256) lora_token_reduce_kernel(int64_t T, int k
   for (int c = lane; c < spitch; c += 32) {
     float v = 0.f;
     if (c < ns)
-      for (int j = 0; j < k; ++j) v += rowp[pair_row(r, t, k, j) * kLoraK + c];
+      for (int j = 0; j < k; ++j) {
+        const int64_t row = pair_row(r, t, k, j) * kLoraK + c;
+        for (int ch = 0; ch < nch; ++ch) v += rowp[ch * rows_stride + row];
+      }
     const __nv_bfloat16 hi = __float2bfloat16(v);
     shl[t * spitch + c] = hi;
     shl[(T + t) * spitch + c] = __float2bfloat16(v - __bfloat162float(hi));
@@ -457,10 +467,11 @@ cudaError_t tile_mma(int mode, const Geom& g, const RouteView& r, const Bufs& b,
   cudaError_t e = cudaFuncSetAttribute(lora_tile_mma_kernel<RP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  lora_tile_mma_kernel<RP><<<(unsigned)(ceil_div(g.pairs, kTileM) + g.G), 256, smem, s>>>(
+  const dim3 grid((unsigned)(ceil_div(g.pairs, kTileM) + g.G), (unsigned)lora_chunks(g));
+  lora_tile_mma_kernel<RP><<<grid, 256, smem, s>>>(
       mode, g.G, g.bw, g.mp, lo.r, g.D, r, b.tile_block, (const __nv_bfloat16*)b.dz,
       (const __nv_bfloat16*)P, lo.ust, g.mp * lo.r, (const __nv_bfloat16*)b.h, lo.uv, lo.rowp,
-      lo.gpart);
+      lora_rows_stride(g), lo.gpart);
   return cudaGetLastError();
 }
 
@@ -506,7 +517,8 @@ cudaError_t lora_fwd_finish(const Geom& g, const RouteView& r, const Bufs& b, co
   const int qpad = lora_qpad(lo.r);
   prof_begin("lora_token_reduce", s);
   lora_token_reduce_kernel<<<(unsigned)ceil_div(g.T, 8), 256, 0, s>>>(
-      g.T, g.k, lo.r, qpad, r, lo.rowp, (__nv_bfloat16*)lo.qhl);
+      g.T, g.k, lo.r, qpad, r, lo.rowp, lora_chunks(g), lora_rows_stride(g),
+      (__nv_bfloat16*)lo.qhl);
   prof_end(s);
   count_launch();
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -550,7 +562,8 @@ cudaError_t lora_bwd_finish(const Geom& g, const RouteView& r, const Bufs& b, co
   // dY_aug buffer; the combine adds it next to the partials and the router term
   prof_begin("lora_token_reduce", s);
   lora_token_reduce_kernel<<<(unsigned)ceil_div(g.T, 8), 256, 0, s>>>(
-      g.T, g.k, nu, upad, r, lo.rowp, (__nv_bfloat16*)lo.dhl);
+      g.T, g.k, nu, upad, r, lo.rowp, lora_chunks(g), lora_rows_stride(g),
+      (__nv_bfloat16*)lo.dhl);
   prof_end(s);
   count_launch();
   cudaError_t e = cudaGetLastError();

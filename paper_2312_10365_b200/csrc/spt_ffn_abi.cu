@@ -183,7 +183,7 @@ static LoraSizes lora_sizes(const Geom& g, int r) {
   s.xaug = align256((size_t)g.T * (g.d + ka) * 2);
   s.waug = align256((size_t)g.mp * g.D * (g.d + ka) * 2);
   s.uv = align256((size_t)g.T * g.mp * r * 4);
-  s.rowp = align256((size_t)g.rows_cap * kLoraK * 4);
+  s.rowp = align256((size_t)lora_chunks(g) * g.rows_cap * kLoraK * 4);
   s.gpart = align256((size_t)tiles * (g.mp + 1) * g.bw * r * 4);
   s.n_split_u = dense_tn_splits(skinny_geom(g, g.mp * r));
   s.n_split_v = dense_tn_splits(skinny_geom(g, r));
