@@ -94,3 +94,65 @@ def test_flat_grads_views_share_storage():
     assert fg.flat.sum().item() == 12.0
     assert fg["dw1"].data_ptr() == fg.flat.data_ptr()
     assert dp.allreduce_grads(fg) is None        # single process: no-op
+
+
+class _FakeLoRA:
+    """The gradient attributes of a RoutedLoRAFFN (dp.attach_flat_grads's LoRA branch)."""
+
+    def __init__(self, shapes, G, d):
+        self.grads = {n: torch.empty(s) for n, s in shapes.items()}
+        self.dw_r = torch.empty(G, d)
+
+
+def _lora_worker(rank, world, port, T, out_q):
+    import oracle
+    from oracle import lora as OL
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = S.CONFIGS["tiny"].with_(act=S.ACT_SWIGLU, d=64, D=256, G=8, k=3)
+    inp = S.make_inputs(cfg, T)
+    lo = S.make_lora(cfg, 4)
+    t0, t1 = dp.shard_range(T, rank, world)
+    x, dy = inp["x"][t0:t1], inp["dy"][t0:t1]
+    lg = oracle.router(x, inp["w_r"])
+    ti = oracle.topk(lg.astype(np.float32), cfg.k)
+    g = OL.lora_backward(x, inp["w1"], inp["w2"], inp["w_r"], lo, lg, ti, dy, cfg.act, cfg.gate)
+    f = _FakeLoRA({n: g[n].shape for n in ("db1", "dc1", "db2", "dc2")}, cfg.G, cfg.d)
+    fg = dp.attach_flat_grads(f, device="cpu")
+    for n in ("db1", "dc1", "db2", "dc2"):
+        f.grads[n].copy_(torch.from_numpy(g[n].astype(np.float32)))
+    f.dw_r.copy_(torch.from_numpy(g["dw_r"].astype(np.float32)))
+    assert f.grads["db1"].data_ptr() == fg.flat.data_ptr()  # views of the one flat buffer
+    dp.allreduce_grads(fg)
+    out_q.put((rank, {n: f.grads[n].numpy().copy() for n in f.grads} | {"dw_r": f.dw_r.numpy().copy()}))
+    dist.destroy_process_group()
+
+
+def test_lora_allreduce_equals_full_batch(orc):
+    """LoRA-wrapped FFN: the flat buffer carries the factor gradients and
+    dW_R (W is frozen); SUM over token shards = the full-batch gradients."""
+    import oracle
+    from oracle import lora as OL
+    world, T = 2, 50
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lora_worker, args=(r, world, port, T, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = S.CONFIGS["tiny"].with_(act=S.ACT_SWIGLU, d=64, D=256, G=8, k=3)
+    inp = S.make_inputs(cfg, T)
+    lo = S.make_lora(cfg, 4)
+    lg = oracle.router(inp["x"], inp["w_r"])
+    ti = oracle.topk(lg.astype(np.float32), cfg.k)
+    full = OL.lora_backward(inp["x"], inp["w1"], inp["w2"], inp["w_r"], lo, lg, ti, inp["dy"], cfg.act,
+                            cfg.gate)
+    for n in ("db1", "dc1", "db2", "dc2", "dw_r"):
+        ref = np.asarray(full[n], np.float64)
+        for r in range(world):
+            got = res[r][n].astype(np.float64).reshape(ref.shape)
+            assert np.max(np.abs(got - ref)) <= 1e-5 * max(1.0, np.max(np.abs(ref))), n
