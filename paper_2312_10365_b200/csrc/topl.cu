@@ -185,17 +185,18 @@ __global__ void __launch_bounds__(kToplThreads) topl_kernel(int H, int nq, int n
       const bool need = k < nc && e.x > 0;
       const unsigned cand = __ballot_sync(0xffffffffu, need);
       if (!cand) continue;
-      unsigned put = 0;
+      unsigned grp = 0;
+      bool w = false;
       if (need) {
-        const unsigned grp = __match_any_sync(cand, s);
+        grp = __match_any_sync(cand, s);
         const int rank = __popc(grp & lt);
-        const bool w = rank < e.x;
+        w = rank < e.x;
         if (w) orow[e.z + (e.y - e.x) + rank] = k;
-        put = __ballot_sync(cand, w);
-        __syncwarp(cand);
-        if ((grp & lt) == 0) bk[warp][s].x = e.x - __popc(grp);
       }
-      remaining -= __popc(__shfl_sync(0xffffffffu, put, __ffs(cand) - 1));
+      const unsigned put = __ballot_sync(0xffffffffu, w);
+      __syncwarp();  // every lane's read of bk (above) before the leaders update it
+      if (need && (grp & lt) == 0) bk[warp][s].x = e.x - __popc(grp);
+      remaining -= __popc(put);
       __syncwarp();
     }
     __syncwarp();
