@@ -450,10 +450,10 @@ def main():
     ap.add_argument("--topl", default="", choices=[""] + sorted(S.TOPL_CONFIGS),
                     help="time the sparse-MHA top-L selection (SURVEY f4, Alg. 3) on this "
                          "workload instead of the routed FFN")
-    ap.add_argument("--graph", action="store_true",
-                    help="N=1: capture the step once into a CUDA graph and replay it (removes the "
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="N=1 runs capture the step once into a CUDA graph and replay it (no "
                          "per-kernel launch gaps; the library's host-side argument checks and "
-                         "tensor-map encodes run once, at capture)")
+                         "tensor-map encodes run once, at capture); this flag times eager launches")
     ap.add_argument("--lora", type=int, default=0, metavar="R",
                     help="LoRA-wrapped routed FFN of rank R (SURVEY f3; W frozen, factors trained); "
                          "0 = the north_star step")
@@ -529,16 +529,20 @@ def main():
     run_step = step
     launches_per_step = None
     if args.graph and world == 1:
-        n0 = P.launch_count()
-        step()
-        torch.cuda.synchronize()
-        launches_per_step = P.launch_count() - n0
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+        try:
+            n0 = P.launch_count()
             step()
-        graph.replay()
-        torch.cuda.synchronize()
-        run_step = graph.replay
+            torch.cuda.synchronize()
+            n1 = P.launch_count() - n0
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+            graph.replay()
+            torch.cuda.synchronize()
+            run_step, launches_per_step = graph.replay, n1
+        except Exception as ex:  # capture unsupported here: time eager launches
+            log(f"[bench] CUDA graph capture failed ({ex}); timing eager launches")
+            torch.cuda.synchronize()
 
     sampler = ClockSampler(local)
     sampler.start()
