@@ -2033,8 +2033,9 @@ __global__ void __launch_bounds__(256) dgate_reduce_kernel(int64_t T, int G, int
 }
 
 int dense_tn_splits(const Geom& g) {
+  // one wave: (N tiles) x (splits) <= #SMs (ceil gave 160 CTAs on 148 SMs at d = 4096)
   const int tiles = (int)(ceil_div(g.G, 128) * ceil_div(g.d, 256));
-  int s = (int)ceil_div(148, tiles);
+  int s = std::max(1, num_sms() / tiles);
   const int max_s = (int)ceil_div(g.T, 64);
   if (s > max_s) s = max_s;
   return s < 1 ? 1 : s;
