@@ -259,6 +259,15 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
   asm volatile(
@@ -302,13 +311,15 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
     tok[threadIdx.x] = (int)threadIdx.x < nvalid ? rv.bucket_token[pos0 + threadIdx.x] : 0;
 
   // stage rows [0,128) x features [f0, f0 + ni) of X (pitch xw) into As (zero rows >= nvalid)
+  // issue (cp.async, no wait) rows [0,128) x features [f0, f0 + ni) of X (pitch xw)
+  // into As; rows >= nvalid are zero.  Completed by cp_async_wait_all + barrier.
   auto stage_a = [&](const __nv_bfloat16* X, int xw, int f0, int ni) {
     const int v8 = ni / 8;
     for (int e = threadIdx.x; e < kMmaRows * v8; e += blockDim.x) {
       const int row = e / v8, cc = (e % v8) * 8;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (row < nvalid) v = __ldg(reinterpret_cast<const uint4*>(X + (prow0 + row) * xw + f0 + cc));
-      *reinterpret_cast<uint4*>(&As[row * kMmaPitch + cc]) = v;
+      __nv_bfloat16* dst = &As[row * kMmaPitch + cc];
+      if (row < nvalid) cp_async16(dst, X + (prow0 + row) * xw + f0 + cc);
+      else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
     }
   };
   // stage E[t(row)][eoff + q] (fp32) as bf16 hi / lo, transposed [q][row]
@@ -370,20 +381,18 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
     float racc[NT][4];  // row product: warp w owns rows [16w, 16w + 16)
 #pragma unroll
     for (int n = 0; n < NT; ++n) racc[n][0] = racc[n][1] = racc[n][2] = racc[n][3] = 0.f;
-    if (mode == 1) {
-      __syncthreads();
-      stage_e(U, upitch, m * r);
-    }
     {  // this CTA's 128-feature chunk (blockIdx.y) of the block
       const int i0 = blockIdx.y * kMmaChunk;
       const int ni = min(kMmaChunk, bw - i0);
-      __syncthreads();
-      stage_a(Arow, aw, m * bw + i0, ni);
+      __syncthreads();  // the previous stage's readers are done
+      stage_a(Arow, aw, m * bw + i0, ni);  // async; overlaps the E / P staging below
+      if (mode == 1) stage_e(U, upitch, m * r);
       for (int e = threadIdx.x; e < RP * ni; e += blockDim.x) {
         const int q = e / ni, i = e % ni;
         Pt[q * kMmaPitch + i] =
             q < r ? P[((int64_t)m * D + (int64_t)b * bw + i0 + i) * r + q] : __float2bfloat16(0.f);
       }
+      cp_async_wait_all();
       __syncthreads();
       // row product: M = rows, K = features of the chunk, N = RP
       for (int k0 = 0; k0 < ni; k0 += 16) {
@@ -419,13 +428,13 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
     }
   }
   if (mode == 1) {  // dB_O: A = h~, E = v
-    __syncthreads();
-    stage_e(V, r, 0);
     {
       const int i0 = blockIdx.y * kMmaChunk;
       const int ni = min(kMmaChunk, bw - i0);
       __syncthreads();
       stage_a(H, bw, i0, ni);
+      stage_e(V, r, 0);
+      cp_async_wait_all();
       __syncthreads();
       cols(ni, part + (((int64_t)tile * (mp + 1) + mp) * bw + i0) * r);
     }
