@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
   // stage E[t(row)][eoff + q] (fp32) as bf16 hi / lo, transposed [q][row]
   auto stage_e = [&](const float* E, int epitch, int eoff) {
     for (int e = threadIdx.x; e < RP * kMmaRows; e += blockDim.x) {
-      const int q = e / kMmaRows, row = e % kMmaRows;
+      const int row = e / RP, q = e % RP;  // consecutive threads read one token's row
       float v = 0.f;
       if (row < nvalid && q < r) v = E[(int64_t)tok[row] * epitch + eoff + q];
       const __nv_bfloat16 hi = __float2bfloat16(v);
