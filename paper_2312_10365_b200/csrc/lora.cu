@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(256) lora_tile_mma_kernel(
       stage_a(Arow, aw, m * bw + i0, ni);  // async; overlaps the E / P staging below
       if (mode == 1) stage_e(U, upitch, m * r);
       for (int e = threadIdx.x; e < RP * ni; e += blockDim.x) {
-        const int q = e / ni, i = e % ni;
+        const int i = e / RP, q = e % RP;  // consecutive threads read one feature's r values
         Pt[q * kMmaPitch + i] =
             q < r ? P[((int64_t)m * D + (int64_t)b * bw + i0 + i) * r + q] : __float2bfloat16(0.f);
       }
