@@ -448,14 +448,18 @@ __global__ void __launch_bounds__(256) lora_token_reduce_kernel(int64_t T, int k
                                                                 const float* __restrict__ rowp,
                                                                 int nch, int64_t rows_stride,
                                                                 __nv_bfloat16* __restrict__ shl) {
-  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (t >= T) return;
+  __shared__ int64_t rows[8][kMaxBlocks];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * 8 + w;
+  if (t >= T) return;  // whole warp
+  for (int j = lane; j < k; j += 32) rows[w][j] = pair_row(r, t, k, j) * kLoraK;  // in parallel
+  __syncwarp();
   for (int c = lane; c < spitch; c += 32) {
     float v = 0.f;
     if (c < ns)
-      for (int j = 0; j < k; ++j) {
-        const int64_t row = pair_row(r, t, k, j) * kLoraK + c;
+#pragma unroll 4
+      for (int j = 0; j < k; ++j) {  // ascending blocks (c12); independent loads
+        const int64_t row = rows[w][j] + c;
         for (int ch = 0; ch < nch; ++ch) v += rowp[ch * rows_stride + row];
       }
     const __nv_bfloat16 hi = __float2bfloat16(v);
