@@ -58,36 +58,44 @@ __device__ __forceinline__ uint4 pack8(const float (&v)[8]) {
 }
 
 // out[t] = [src[t, 0:d] | hi(u[t, 0:nu]) | lo(u[t, 0:nu]) | 0 ...] (width d + ka), with
-// hi = bf16(u), lo = bf16(u - hi); ust[t] = u[t] (fp32, for the backward)
+// hi = bf16(u), lo = bf16(u - hi); ust[t] = u[t] (fp32, for the backward).
+// One flat grid-stride loop over the 16-byte chunks of the output (a streaming copy
+// with several chunks in flight per thread); the ka / 8 tail chunks of a row build
+// the hi | lo columns.
 __global__ void __launch_bounds__(256) lora_aug_rows_kernel(int64_t T, int d, int ka,
                                                             const __nv_bfloat16* __restrict__ src,
                                                             const float* __restrict__ u, int nu,
                                                             __nv_bfloat16* __restrict__ out,
                                                             float* __restrict__ ust) {
-  const int dv = d / 8;
-  for (int64_t t = blockIdx.x; t < T; t += gridDim.x) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(src + t * d);
-    uint4* o4 = reinterpret_cast<uint4*>(out + t * (d + ka));
-    for (int c = threadIdx.x; c < dv; c += blockDim.x) o4[c] = __ldg(s4 + c);
-    if ((int)threadIdx.x < ka / 8) {
-      const int c0 = threadIdx.x * 8;
-      float v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int c = c0 + i;
-        float x = 0.f;
-        if (c < nu) {
-          x = __bfloat162float(__float2bfloat16(u[t * nu + c]));
-        } else if (c < 2 * nu) {
-          const float f = u[t * nu + c - nu];
-          x = f - __bfloat162float(__float2bfloat16(f));
-        }
-        v[i] = x;
-      }
-      o4[dv + threadIdx.x] = pack8(v);
+  const int dv = d / 8, wv = (d + ka) / 8;
+  const int64_t n = T * wv;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* o4 = reinterpret_cast<uint4*>(out);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+    const int64_t t = e / wv;
+    const int c = (int)(e - t * wv);
+    if (c < dv) {
+      o4[e] = __ldg(s4 + t * dv + c);
+      continue;
     }
-    if (ust)
-      for (int c = threadIdx.x; c < nu; c += blockDim.x) ust[t * nu + c] = u[t * nu + c];
+    const int c0 = (c - dv) * 8;  // tail column of the augmented K stage
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int cc = c0 + i;
+      float x = 0.f;
+      if (cc < nu) {
+        const float f = u[t * nu + cc];
+        x = __bfloat162float(__float2bfloat16(f));
+        if (ust) ust[t * nu + cc] = f;
+      } else if (cc < 2 * nu) {
+        const float f = u[t * nu + cc - nu];
+        x = f - __bfloat162float(__float2bfloat16(f));
+      }
+      v[i] = x;
+    }
+    o4[e] = pack8(v);
   }
 }
 
@@ -215,7 +223,7 @@ cudaError_t launch_grad_reduce(const Geom& g, const RouteView& r, int mp, int rk
 cudaError_t aug_rows(const Geom& g, int ka, const void* src, const float* u, int nu, void* out,
                      float* ust, cudaStream_t s) {
   prof_begin("lora_aug_rows", s);
-  const unsigned grid = (unsigned)std::min<int64_t>(g.T, 148 * 16);
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(g.T * ((g.d + ka) / 8), 256), 148 * 32);
   lora_aug_rows_kernel<<<grid, 256, 0, s>>>(g.T, g.d, ka, (const __nv_bfloat16*)src, u, nu,
                                             (__nv_bfloat16*)out, ust);
   prof_end(s);
