@@ -107,18 +107,28 @@ __global__ void __launch_bounds__(256) lora_aug_w_kernel(int64_t R, int d, int k
                                                          const __nv_bfloat16* __restrict__ P, int r,
                                                          int nu, int64_t rows_half,
                                                          __nv_bfloat16* __restrict__ out) {
-  const int dv = d / 8;
-  for (int64_t i = blockIdx.x; i < R; i += gridDim.x) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(w + i * d);
-    uint4* o4 = reinterpret_cast<uint4*>(out + i * (d + ka));
-    for (int c = threadIdx.x; c < dv; c += blockDim.x) o4[c] = __ldg(s4 + c);
-    const int off = (int)(i / rows_half) * r;
-    if ((int)threadIdx.x < ka) {
-      const int c = threadIdx.x;
-      const int q = (c < nu ? c : c - nu) - off;
-      out[i * (d + ka) + d + c] =
-          (c < 2 * nu && q >= 0 && q < r) ? P[i * r + q] : __float2bfloat16(0.f);
+  // flat grid-stride loop over the 16-byte chunks of the output rows
+  const int dv = d / 8, wv = (d + ka) / 8;
+  const int64_t n = R * wv;
+  const uint4* s4 = reinterpret_cast<const uint4*>(w);
+  uint4* o4 = reinterpret_cast<uint4*>(out);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+    const int64_t i = e / wv;
+    const int c = (int)(e - i * wv);
+    if (c < dv) {
+      o4[e] = __ldg(s4 + i * dv + c);
+      continue;
     }
+    const int off = (int)(i / rows_half) * r;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int cc = (c - dv) * 8 + j;  // augmented column
+      const int q = (cc < nu ? cc : cc - nu) - off;
+      v[j] = (cc < 2 * nu && q >= 0 && q < r) ? P[i * r + q] : __float2bfloat16(0.f);
+    }
+    o4[e] = *reinterpret_cast<const uint4*>(v);
   }
 }
 
@@ -234,7 +244,7 @@ cudaError_t aug_rows(const Geom& g, int ka, const void* src, const float* u, int
 cudaError_t aug_w(const Geom& g, int ka, int64_t R, const void* w, const void* P, int rk, int nu,
                   void* out, cudaStream_t s) {
   prof_begin("lora_aug_w", s);
-  const unsigned grid = (unsigned)std::min<int64_t>(R, 148 * 16);
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(R * ((g.d + ka) / 8), 256), 148 * 32);
   lora_aug_w_kernel<<<grid, 256, 0, s>>>(R, g.d, ka, (const __nv_bfloat16*)w,
                                          (const __nv_bfloat16*)P, rk, nu, g.D,
                                          (__nv_bfloat16*)out);
