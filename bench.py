@@ -69,7 +69,16 @@ def kernel_work(cfg, T):
         "combine_bwd": ("hbm", P * d * e + 12.0 * P + T * d * e),
         "topk_hist": ("hbm", 4.0 * T * G + 8.0 * T * cfg.k),
         "bucket_scatter": ("hbm", 20.0 * P),
+        # fp32 path (tiny config): CUDA-core FFMA kernels, no tensor cores (reading c13)
+        "simt_f1": ("alu", 2.0 * P * mp * bw * d),
+        "simt_f2": ("alu", 2.0 * P * bw * d),
+        "simt_b1": ("alu", 2.0 * P * bw * d),
+        "simt_dw": ("alu", (2.0 * P * mp * bw * d + 2.0 * P * bw * d) / 2),  # dW1, dW2: mean per launch
+        "simt_b2": ("alu", 2.0 * P * mp * bw * d),
     }
+
+
+FP32_FMA_PEAK = 148 * 128 * 2 * 1.965e9 / 1e12  # TFLOP/s: 128 FP32 lanes/SM x 2 FLOP x SMs x max clock
 
 
 def step_gemm_flops(cfg, T, lora=0):
@@ -621,7 +630,7 @@ def main():
         kernels[name] = {"launches_per_step": cnt / args.steps, "ms_per_launch": per}
         if name in work:
             kind, amt = work[name]
-            if kind == "tensor":
+            if kind in ("tensor", "alu"):
                 kernels[name]["tflops"] = amt / (per / 1e3) / 1e12
             else:
                 kernels[name]["gbs"] = amt / (per / 1e3) / 1e9
@@ -638,7 +647,15 @@ def main():
             kt = json.load(open(tp))["kernels"].get(dom)
             if kt:
                 traffic = kt["dram_read_bytes"] + kt["dram_write_bytes"]
-        if kind == "tensor":
+        if kind == "alu":
+            ach = amt / (per / 1e3) / 1e12
+            roofline = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": FP32_FMA_PEAK,
+                        "unit": "TFLOP/s", "frac": ach / FP32_FMA_PEAK, "traffic": traffic,
+                        "peak_src": "fp32 FFMA: 148 SMs x 128 lanes x 2 FLOP x 1.965 GHz (B200 unit "
+                                    "counts, max clock)",
+                        "algorithmic_per_launch": amt, "ms_per_launch": per,
+                        "share_of_step": tot / args.steps / step_ms_prof}
+        elif kind == "tensor":
             ach = amt / (per / 1e3) / 1e12
             roofline = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk["bf16_sustained"],
                         "unit": "TFLOP/s", "frac": ach / pk["bf16_sustained"], "traffic": traffic,
