@@ -56,6 +56,7 @@ struct Bufs {
   int32_t* chunk_counts;  // [n_chunks, G]
   int32_t* chunk_base;    // [n_chunks, G]
   int32_t* n_b;           // [G]
+  // device tile schedules (stash: built by the forward, reused by the backward)
   int32_t* tile_list;     // [ceil(T*k/128) + G]: bucket tiles in (m-tile, block) order
   int32_t* unit_offsets;  // [G+2]: prefix of weight-resident work units per block; [G+1] = pair tiles
   int32_t* tile_block;    // [ceil(T*k/128) + G]: block of each 128-row bucket tile

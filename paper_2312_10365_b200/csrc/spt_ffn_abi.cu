@@ -99,7 +99,12 @@ static Sizes compute_sizes(const Geom& g) {
   const size_t e = (size_t)g.esize;
   s.z = align256((size_t)g.rows_cap * g.mp * g.bw * e);
   s.h = align256((size_t)g.rows_cap * g.bw * e);
-  s.stash = s.z + s.h;
+  // the device tile schedules live in the stash: the forward builds them, the
+  // backward reuses them (same routing)
+  s.tl = align256((size_t)(ceil_div(g.pairs, kTileM) + g.G) * 4);
+  s.uo = align256((size_t)(g.G + 2) * 4);
+  s.tb = s.tl;
+  s.stash = s.z + s.h + s.tl + s.uo + s.tb;
   s.part = align256((size_t)g.rows_cap * g.d * e);
   s.dz = align256((size_t)g.rows_cap * g.mp * g.bw * e);
   s.da = align256((size_t)g.rows_cap * g.bw * 4);  // fp32 dA rows (both paths)
@@ -110,14 +115,11 @@ static Sizes compute_sizes(const Geom& g) {
   s.counts = align256((size_t)g.n_chunks * g.G * 4);
   s.base = s.counts;
   s.nb = align256((size_t)g.G * 4);
-  s.tl = align256((size_t)(ceil_div(g.pairs, kTileM) + g.G) * 4);
-  s.uo = align256((size_t)(g.G + 2) * 4);
-  s.tb = s.tl;
   s.lbp = align256((size_t)g.n_chunks * g.G * 4);  // balance loss: per-chunk softmax sums
   s.lbx = g.lbw == 0.f ? 0                         // balance gradient: dense router term
           : align256(g.dtype == SPT_BF16 ? (size_t)g.T * g.d * 2 : (size_t)g.T * g.G * 4);
   s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb +
-         s.tl + s.uo + s.tb + s.lbp + s.lbx;
+         s.lbp + s.lbx;
   return s;
 }
 
@@ -128,6 +130,10 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
   if (p) {
     b.z = p;
     b.h = p + s.z;
+    uint8_t* q = p + s.z + s.h;
+    b.tile_list = (int32_t*)q; q += s.tl;
+    b.unit_offsets = (int32_t*)q; q += s.uo;
+    b.tile_block = (int32_t*)q;
   }
   uint8_t* w = (uint8_t*)ws;
   b.part = w; w += s.part;
@@ -141,9 +147,6 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
   b.chunk_counts = (int32_t*)w; w += s.counts;
   b.chunk_base = (int32_t*)w; w += s.base;
   b.n_b = (int32_t*)w; w += s.nb;
-  b.tile_list = (int32_t*)w; w += s.tl;
-  b.unit_offsets = (int32_t*)w; w += s.uo;
-  b.tile_block = (int32_t*)w; w += s.tb;
   b.lb_part = (float*)w; w += s.lbp;
   b.lb_x = s.lbx ? (void*)w : nullptr; w += s.lbx;
   return b;

@@ -2080,8 +2080,8 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   const int up = bucket_tiles_upper(g);
   const bool sig = g.gate == SPT_GATE_SIGMOID;
   const bool lb = g.lbw != 0.f;  // load-balancing loss: dense router gradient (every block)
-  cudaError_t e0 = build_schedules(g, r, b, s);
-  if (e0 != cudaSuccess) return e0;
+  // the tile schedules are the forward's (in the stash: same routing)
+  cudaError_t e0 = cudaSuccess;
   if ((sig || lb) && cudaMemsetAsync(b.dlg, 0, (size_t)2 * g.T * g.gpad * 2, s) != cudaSuccess)
     return cudaErrorUnknown;
   // LoRA: dA runs on dY_aug / W2_aug (K = d + 64: the (dy C_O^T) B_O^T term)
