@@ -10,6 +10,7 @@ namespace spt {
 
 constexpr int kTileM = SPT_TILE_M;   // bucket tile height (rows of a grouped-GEMM M tile)
 constexpr int kRouteChunk = 256;     // tokens per bucketing chunk (one CTA)
+constexpr int kTopkChunk = 32;       // tokens per top-k CTA (= per bucket-count row)
 constexpr int kMaxBlocks = 256;      // G limit (routing keeps 8 logits per lane)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -22,6 +23,7 @@ struct Geom {
   int64_t pairs;     // T*k
   int64_t rows_cap;  // padded bucket rows: T*k + G*kTileM (>= sum_b ceil(n_b/128)*128)
   int64_t n_chunks;  // ceil(T / kRouteChunk)
+  int64_t n_sub;     // ceil(T / kTopkChunk): rows of the per-chunk bucket counts
   int gpad;          // G rounded up to 16 (router GEMM N, dense dlogit width)
   int esize;         // bytes per act element
   float lbw;         // load-balancing loss weight lambda (desc->balance_weight; 0 = off)
@@ -53,8 +55,8 @@ struct Bufs {
   void* dlg;      // [2, T, gpad] bf16 (hi, lo) dense dlogits (tcgen05 dW_R GEMM)
   float* dwr_part;// [n_split, G, d] f32 split-K partials of dW_R
   int n_split;
-  int32_t* chunk_counts;  // [n_chunks, G]
-  int32_t* chunk_base;    // [n_chunks, G]
+  int32_t* chunk_counts;  // [n_sub, G] bucket counts per kTopkChunk tokens
+  int32_t* chunk_base;    // [n_sub, G] exclusive prefix over the sub-chunks
   int32_t* n_b;           // [G]
   // device tile schedules (stash: built by the forward, reused by the backward)
   int32_t* tile_list;     // [ceil(T*k/128) + G]: bucket tiles in (m-tile, block) order

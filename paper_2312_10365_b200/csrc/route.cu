@@ -68,7 +68,7 @@ cudaError_t launch_router_simt(const Geom& g, const void* x, const void* w_r, fl
 // order).  Same set as k rounds of (key desc, id asc) argmax, ~6x fewer
 // instructions (the round form was issue-bound: 2.5 K warp-instr per token).
 template <int NSLOT>
-__global__ void __launch_bounds__(1024) topk_hist_kernel(int64_t T, int G, int k, int gate_mode,
+__global__ void __launch_bounds__(256) topk_hist_kernel(int64_t T, int G, int k, int gate_mode,
                                                         const float* __restrict__ logits,
                                                         int32_t* __restrict__ topk_idx,
                                                         float* __restrict__ topk_gate,
@@ -78,10 +78,10 @@ __global__ void __launch_bounds__(1024) topk_hist_kernel(int64_t T, int G, int k
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t chunk = blockIdx.x;
-  const int per_warp = kRouteChunk / (blockDim.x >> 5);
+  const int per_warp = kTopkChunk / (blockDim.x >> 5);
   const unsigned lt = (1u << lane) - 1u;
   for (int i = 0; i < per_warp; ++i) {
-    const int64_t t = chunk * kRouteChunk + warp * per_warp + i;
+    const int64_t t = chunk * kTopkChunk + warp * per_warp + i;
     if (t >= T) break;
     uint32_t v[NSLOT];
     float lg[NSLOT];
@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
     for (int j = 0; j < k; ++j) {
       const int b = topk_idx[t * k + j];
       const int pos =
-          boff[b] + chunk_base[chunk * G + b] + wbase[warp][b] + __popc(mask[warp][b] & lt);
+          boff[b] + chunk_base[chunk * (kRouteChunk / kTopkChunk) * G + b] + wbase[warp][b] +
+          __popc(mask[warp][b] & lt);
       bucket_token[pos] = (int32_t)t;
       bucket_gate[pos] = topk_gate[t * k + j];
       pair_slot[t * k + j] = pos;
@@ -236,9 +237,12 @@ cudaError_t launch_topk_bucket(const Geom& g, const RouteView& r, const Bufs& b,
   const unsigned nch = (unsigned)g.n_chunks;
   prof_begin("topk_hist", s);
   const int nslot = (g.G + 31) / 32;
-#define SPT_TOPK(NS)                                                                          \
-  topk_hist_kernel<NS><<<nch, 1024, 0, s>>>(g.T, g.G, g.k, g.gate, r.logits, r.topk_idx, \
-                                            r.topk_gate, b.chunk_counts)
+  // one CTA of 8 warps per kTopkChunk tokens (4 per warp): T / 32 CTAs, so even
+  // 8 K-token batches spread over every SM (the selection is a serial 32-step
+  // search per token)
+#define SPT_TOPK(NS)                                                                         \
+  topk_hist_kernel<NS><<<(unsigned)g.n_sub, 256, 0, s>>>(g.T, g.G, g.k, g.gate, r.logits, \
+                                                         r.topk_idx, r.topk_gate, b.chunk_counts)
   if (nslot <= 1) SPT_TOPK(1);
   else if (nslot == 2) SPT_TOPK(2);
   else if (nslot == 3) SPT_TOPK(3);
@@ -247,7 +251,7 @@ cudaError_t launch_topk_bucket(const Geom& g, const RouteView& r, const Bufs& b,
 #undef SPT_TOPK
   prof_end(s);
   prof_begin("bucket_scan", s);
-  bucket_scan_kernel<<<g.G, 256, 0, s>>>(g.n_chunks, g.G, b.chunk_counts, b.chunk_base, b.n_b);
+  bucket_scan_kernel<<<g.G, 256, 0, s>>>(g.n_sub, g.G, b.chunk_counts, b.chunk_base, b.n_b);
   prof_end(s);
   prof_begin("bucket_scatter", s);
   bucket_scatter_kernel<<<nch, 256, 0, s>>>(g.T, g.G, g.k, b.n_b, b.chunk_base, r.topk_idx,

@@ -76,6 +76,7 @@ static spt_status make_geom(const spt_ffn_desc* d, Geom* g) {
   g->pairs = g->T * g->k;
   g->rows_cap = g->pairs + (int64_t)g->G * kTileM;
   g->n_chunks = ceil_div(g->T, kRouteChunk);
+  g->n_sub = ceil_div(g->T, kTopkChunk);
   g->gpad = (int)ceil_div(g->G, 16) * 16;
   g->esize = d->dtype == SPT_BF16 ? 2 : 4;
   g->lbw = d->balance_weight;
@@ -112,7 +113,7 @@ static Sizes compute_sizes(const Geom& g) {
   s.dgate = align256((size_t)g.rows_cap * 4);
   s.dlg = g.dtype == SPT_BF16 ? align256((size_t)2 * g.T * g.gpad * 2) : 0;
   s.dwr = g.dtype == SPT_BF16 ? align256((size_t)dwr_splits(g) * g.G * g.d * 4) : 0;
-  s.counts = align256((size_t)g.n_chunks * g.G * 4);
+  s.counts = align256((size_t)g.n_sub * g.G * 4);
   s.base = s.counts;
   s.nb = align256((size_t)g.G * 4);
   s.lbp = align256((size_t)g.n_chunks * g.G * 4);  // balance loss: per-chunk softmax sums
