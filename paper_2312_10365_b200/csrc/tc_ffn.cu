@@ -1895,7 +1895,7 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
 // stash: dgate = sum_u dA_u act(z_u); dZ = g dA act'(Z); dlogit = dgate g (1-g)
 // (as sigma(z) sigma(-z)); dense hi/lo bf16 dlogits for the dW_R GEMM.  Padding
 // rows get dZ = 0 (the K tails of the dW1 GEMM rely on it).
-__global__ void __launch_bounds__(256) da_post_kernel(int64_t T, int G, int bw, int mp, int act,
+__global__ void __launch_bounds__(256, 4) da_post_kernel(int64_t T, int G, int bw, int mp, int act,
                                                       int gate, int gpad, RouteView r,
                                                       const int32_t* __restrict__ tile_block,
                                                       const float* __restrict__ da,
