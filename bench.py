@@ -200,7 +200,7 @@ def run_reference(args, cfg):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(cfg, args.gpus, cfg.T, args.balance_weight, args.lora),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -463,6 +463,12 @@ def main():
                     help="N=1 runs capture the step once into a CUDA graph and replay it (no "
                          "per-kernel launch gaps; the library's host-side argument checks and "
                          "tensor-map encodes run once, at capture); this flag times eager launches")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: lets several ranks share one GPU, "
+                         "to exercise the multi-rank path where only one device is available)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: the config's tokens on every rank; strong: the config's tokens split "
+                         "over the ranks (dp.shard_range)")
     ap.add_argument("--lora", type=int, default=0, metavar="R",
                     help="LoRA-wrapped routed FFN of rank R (SURVEY f3; W frozen, factors trained); "
                          "0 = the north_star step")
@@ -486,13 +492,25 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())  # gloo: several ranks may share a device
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    T = cfg.T
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    if args.scaling == "strong":  # the config's global batch split over the ranks
+        t0, t1 = dp.shard_range(cfg.T, rank, world)
+        T, offset = t1 - t0, t0
+        if offset % 1024:
+            raise SystemExit("strong scaling needs shards that start at multiples of 1024 tokens")
+    else:                         # the config's batch on every rank
+        T = cfg.T
+        offset = rank * ((T + 1023) // 1024) * 1024
+    T_global = dp.shard_range(cfg.T, 0, 1)[1] if args.scaling == "strong" else T * world
     dt = torch.float32 if cfg.dtype == "f32" else torch.bfloat16
     t_gen = time.time()
-    inp = S.make_inputs(cfg, T, token_offset=rank * ((T + 1023) // 1024) * 1024)
+    inp = S.make_inputs(cfg, T, token_offset=offset)
     log(f"[rank {rank}] inputs generated in {time.time() - t_gen:.1f}s")
     dev = {n: torch.from_numpy(inp[n]).to(dt).cuda() for n in ("x", "w1", "w2", "w_r", "dy")}
     del inp
@@ -572,7 +590,7 @@ def main():
         launches = launches_per_step * args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_max = dp.max_over_ranks(ms, device="cuda")
-    value = T * world / (ms_max / 1e3)
+    value = T_global / (ms_max / 1e3)   # every rank's tokens / the slowest rank's time
 
     # ---- per-kernel device times (CUDA events around each library launch)
     prof = {}
@@ -612,7 +630,7 @@ def main():
         pipe.synchronize()
         ms_e = dp.max_over_ranks(e0.elapsed_time(e1) / k2, device="cuda")
         hb, db = pipe.bytes_per_step()
-        e2e = {"value": T * world / (ms_e / 1e3), "unit": UNIT, "ms_per_step": ms_e,
+        e2e = {"value": T_global / (ms_e / 1e3), "unit": UNIT, "ms_per_step": ms_e,
                "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db,
                "what": "per step: H2D x, dy from pinned host -> route/fwd/bwd(+allreduce) -> D2H y, dx "
                        "to pinned host; copies of adjacent steps overlap the kernels (copy streams)"}
@@ -672,10 +690,12 @@ def main():
     step_tf = step_gemm_flops(cfg, T, args.lora) / (ms_max / 1e3) / 1e12
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded random tokens and weights)",
         "config": dict(workload_config(cfg, world, T, args.balance_weight, args.lora),
-                       **({"cuda_graph": True} if launches_per_step is not None else {})),
+                       **({"cuda_graph": True} if launches_per_step is not None else {}),
+                       **({"backend": args.backend} if world > 1 else {}),
+                       global_tokens=T_global),
         "tensor_pipe_frac_of_bf16_peak": {"step_gemm_tflops": step_tf, "peak": pk["bf16_sustained"],
                                           "frac": step_tf / pk["bf16_sustained"],
                                           "peak_src": pk["src"] + " bf16 sustained"},

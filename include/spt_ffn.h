@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SPT_FFN_ABI_VERSION 4
+#define SPT_FFN_ABI_VERSION 5
 /* Height of a bucket tile: tile_offsets counts ceil(n_b / SPT_TILE_M) per block. */
 #define SPT_TILE_M 128
 
@@ -84,7 +84,25 @@ typedef struct {
   /* lambda >= 0 (finite): spt_ffn_backward adds the gradient of lambda * L_balance
    * (spt_ffn_balance_loss) to dw_r and dx.  0 disables it.  (ABI 2) */
   float balance_weight;
+  /* SPT_FFN_* option bits (ABI 5); unknown bits -> SPT_ERR_INVALID_ARGUMENT. */
+  uint32_t flags;
 } spt_ffn_desc;
+
+/* desc.flags: the k-way sum of the per-block outputs of each token (Alg. 4
+ * line 5, y_t = sum_{b in S_t} g act(x_t W_I[b]) W_O[b]; and its grad-input
+ * counterpart dx_t) runs in fp32 in either of two orders:
+ *   0 (default, bf16 path, blocks of <= 256 units): each block's output rows are
+ *     added in fp32 straight into an L2-resident token accumulator by the
+ *     GEMM epilogue (TMA reduce-add, no per-block rows in HBM); the summation
+ *     order follows the hardware, so results may differ run to run at fp32
+ *     rounding level (before the final rounding to the act dtype);
+ *   SPT_FFN_DETERMINISTIC: every (token, block) output row is materialised and
+ *     a separate pass sums them in ascending block id -- bitwise reproducible
+ *     (SPEC's fixed order), at the cost of T*k*d act-dtype
+ *     elements written and read back through HBM.
+ * The fp32 path, the LoRA-wrapped calls and blocks wider than 256 units always
+ * take the deterministic order. */
+#define SPT_FFN_DETERMINISTIC 1u
 
 /* Routing decision and bucket layout (all DEVICE buffers, caller-allocated).
  * Written by spt_ffn_route, read by spt_ffn_forward / spt_ffn_backward. */
@@ -253,9 +271,11 @@ typedef struct {
 /* Top-L key indices of every query.  SPT_ERR_INVALID_ARGUMENT: NULL desc, a
  * negative size, M outside [1, 31], E outside [1, 256], L < 1, causal not 0/1,
  * a NULL pointer with a non-empty problem; SPT_ERR_UNSUPPORTED: the key codes
- * of one head plus the per-warp score rows exceed the 227 KB of shared memory
- * of one CTA (n_k (4 ceil(M/c) + 16) bytes, c = 8 codes per word for E <= 16
- * else 4), non-sm_100 device.  Asynchronous on stream. */
+ * of one head plus the per-warp score rows plus the kernel's 40,960 bytes of
+ * static bucket state exceed the 227 KB of shared memory of one CTA
+ * (n_k (4 ceil(M/c) + 16) + 40960 bytes, c = 8 codes per word for E <= 16
+ * else 4; ceil(M/c) = 3 is stored as 4), non-sm_100 device.  Asynchronous on
+ * stream. */
 spt_status spt_mha_topl(const spt_topl_desc* desc, const uint8_t* codes_q, const uint8_t* codes_k,
                         int32_t* indices, void* stream);
 

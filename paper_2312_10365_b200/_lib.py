@@ -17,6 +17,7 @@ SPT_ACT_RELU, SPT_ACT_GELU, SPT_ACT_SWIGLU = 0, 1, 2
 SPT_GATE_SIGMOID, SPT_GATE_NONE = 0, 1
 SPT_ROUTE_LOGITS_IN = 1
 SPT_BWD_ACCUMULATE_DW = 1
+SPT_FFN_DETERMINISTIC = 1
 SPT_TILE_M = 128
 
 # every symbol include/spt_ffn.h declares
@@ -31,7 +32,8 @@ class spt_ffn_desc(ctypes.Structure):
     _fields_ = [("n_tokens", ctypes.c_int64), ("d_model", ctypes.c_int32), ("d_ff", ctypes.c_int32),
                 ("n_blocks", ctypes.c_int32), ("top_k", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("act", ctypes.c_int32), ("gate", ctypes.c_int32),
-                ("balance_weight", ctypes.c_float)]  # ABI 2
+                ("balance_weight", ctypes.c_float),  # ABI 2
+                ("flags", ctypes.c_uint32)]  # ABI 5: SPT_FFN_DETERMINISTIC
 
 
 class spt_route_buf(ctypes.Structure):

@@ -53,7 +53,10 @@ __device__ __forceinline__ uint32_t pack_codes(const uint8_t* src, int w, int M)
 #pragma unroll
   for (int b = 0; b < CPW; ++b) {
     const int m = w * CPW + b;
-    if (m < M) v |= (uint32_t)src[m] << (SH * b);
+    // mask to the field width: an out-of-range code (>= E, "unspecified result"
+    // per the header) must not spill into the next field, or a score could
+    // exceed M and index the bucket arrays out of bounds
+    if (m < M) v |= ((uint32_t)src[m] & (CPW == 8 ? 0xFu : 0xFFu)) << (SH * b);
   }
   return v;
 }
@@ -209,7 +212,10 @@ cudaError_t launch_topl_nw(int H, int nq, int nk, int M, int L, int causal, cons
   const int chunks = (nq + qpb - 1) / qpb;
   cudaError_t e = cudaFuncSetAttribute(topl_kernel<NW, CPW>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // do not leave the failure in the thread's error state
+    return e;
+  }
   topl_kernel<NW, CPW><<<(unsigned)((int64_t)H * chunks), kToplThreads, smem, s>>>(
       H, nq, nk, M, L, causal, qpb, cq, ck, out);
   return cudaGetLastError();
@@ -227,6 +233,12 @@ size_t topl_smem_bytes(int nk, int M, int E) {
 }
 
 int topl_max_score() { return kMaxScore; }
+
+// static shared memory of topl_kernel (per-lane bucket counts + bucket records):
+// the dynamic part may use at most the 227 KB opt-in limit minus this
+size_t topl_static_smem_bytes() {
+  return sizeof(uint16_t) * kToplWarps * (kMaxScore + 1) * 32 + sizeof(int4) * kToplWarps * (kMaxScore + 1);
+}
 
 cudaError_t launch_topl(int H, int nq, int nk, int M, int E, int L, int causal,
                         const uint8_t* cq, const uint8_t* ck, int32_t* out, cudaStream_t s) {

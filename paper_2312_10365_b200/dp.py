@@ -10,6 +10,15 @@ full-batch gradient of the summed loss; any mean is left to the caller).
 
 The gradients live in ONE flat fp32 buffer so the exchange is a single NCCL
 all-reduce (over NVLink/NVSwitch on a B200 node) with no packing copies.
+
+Load-balancing loss (desc.balance_weight = lambda): each rank's
+backward differentiates lambda * L_r, the loss of ITS shard's routing
+statistics (f_g, pbar_g over its T_r tokens), so the SUM all-reduce yields the
+gradient of sum_r lambda * L_r -- a per-shard balance loss, the usual
+data-parallel reading of a Switch-style auxiliary loss; it is not the loss of
+the global batch's statistics (that would need the per-block counts and
+softmax sums all-reduced before the backward).  A caller wanting the mean over
+shards passes lambda / world.  tests/test_dp_gloo.py pins this semantics.
 """
 from __future__ import annotations
 

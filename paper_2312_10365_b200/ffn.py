@@ -17,12 +17,14 @@ _DT = {torch.float32: L.SPT_F32, torch.bfloat16: L.SPT_BF16}
 
 
 def make_desc(T: int, d: int, D: int, G: int, k: int, dtype: torch.dtype, act: int,
-              gate: int = L.SPT_GATE_SIGMOID, balance_weight: float = 0.0) -> L.spt_ffn_desc:
-    """balance_weight = lambda of the load-balancing loss (0 = off; spt_ffn_balance_loss)."""
+              gate: int = L.SPT_GATE_SIGMOID, balance_weight: float = 0.0,
+              deterministic: bool = False) -> L.spt_ffn_desc:
+    """balance_weight = lambda of the load-balancing loss (0 = off; spt_ffn_balance_loss);
+    deterministic = SPT_FFN_DETERMINISTIC (bitwise-reproducible ascending-block k-way sums)."""
     if dtype not in _DT:
         raise ValueError(f"unsupported dtype {dtype}")
     return L.spt_ffn_desc(int(T), int(d), int(D), int(G), int(k), _DT[dtype], int(act), int(gate),
-                          float(balance_weight))
+                          float(balance_weight), L.SPT_FFN_DETERMINISTIC if deterministic else 0)
 
 
 def spt_ffn_sizes(desc: L.spt_ffn_desc) -> tuple[int, int]:
@@ -194,8 +196,8 @@ class RoutedFFN:
     the three methods are the ABI calls)."""
 
     def __init__(self, T, d, D, G, k, dtype, act, gate=L.SPT_GATE_SIGMOID, device="cuda",
-                 balance_weight=0.0):
-        self.desc = make_desc(T, d, D, G, k, dtype, act, gate, balance_weight)
+                 balance_weight=0.0, deterministic=False):
+        self.desc = make_desc(T, d, D, G, k, dtype, act, gate, balance_weight, deterministic)
         self.T, self.d, self.D, self.G, self.k = T, d, D, G, k
         self.dtype, self.act, self.gate = dtype, act, gate
         self.mp = 2 if act == L.SPT_ACT_SWIGLU else 1

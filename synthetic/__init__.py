@@ -81,10 +81,24 @@ CONFIGS = {
 # Table 3 shapes): OPT-2048 / LLaMA-4096 2-matrix FFNs, batch
 # 16 x 512 tokens, G = 8 blocks, beta = k/G = 1/2.  The
 # paper's LLaMA-family block uses GELU in its 2-matrix form.
+# Table 5 also times beta = 3/4 ("SPT (3/4)"), and the router
+# section names G = 4 as the other default group count ("a small G (e.g., 4 or
+# 8)"): k = beta * G gives k = 6 of 8, k = 2 of 4 and k = 3 of 4.
 PAPER_CONFIGS = {
     "opt2048_g8": FfnConfig("opt2048_g8", 2048, 8192, 8, 4, 16 * 512, "bf16", ACT_RELU, cfg_index=5),
     "llama4096_g8": FfnConfig("llama4096_g8", 4096, 11008, 8, 4, 16 * 512, "bf16", ACT_GELU,
                               cfg_index=6),
+    "opt2048_g8_b34": FfnConfig("opt2048_g8_b34", 2048, 8192, 8, 6, 16 * 512, "bf16", ACT_RELU,
+                                cfg_index=7),
+    "llama4096_g8_b34": FfnConfig("llama4096_g8_b34", 4096, 11008, 8, 6, 16 * 512, "bf16", ACT_GELU,
+                                  cfg_index=8),
+    "opt2048_g4": FfnConfig("opt2048_g4", 2048, 8192, 4, 2, 16 * 512, "bf16", ACT_RELU, cfg_index=9),
+    "llama4096_g4": FfnConfig("llama4096_g4", 4096, 11008, 4, 2, 16 * 512, "bf16", ACT_GELU,
+                              cfg_index=20),
+    "opt2048_g4_b34": FfnConfig("opt2048_g4_b34", 2048, 8192, 4, 3, 16 * 512, "bf16", ACT_RELU,
+                                cfg_index=21),
+    "llama4096_g4_b34": FfnConfig("llama4096_g4_b34", 4096, 11008, 4, 3, 16 * 512, "bf16", ACT_GELU,
+                                  cfg_index=22),
 }
 ALL_CONFIGS = {**CONFIGS, **PAPER_CONFIGS}
 

@@ -2,6 +2,9 @@
 the same seeded inputs, and the error metric of SURVEY §8(c) reading c14."""
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 
 import synthetic as S
@@ -16,7 +19,49 @@ def relerr(got, ref) -> float:
     den = np.max(np.abs(ref)) if ref.size else 0.0
     if ref.size == 0:
         return 0.0
-    return float(np.max(np.abs(got - ref)) / max(den, 1e-30))
+    err = float(np.max(np.abs(got - ref)) / max(den, 1e-30))
+    _log_elementwise(got, ref, err)
+    return err
+
+
+def elemerr(got, ref, floor=1e-3) -> float:
+    """Reading c14's companion metric: elementwise relative error with a floor,
+    max_i |a_i - o_i| / max(|o_i|, floor * max|o|).  Errors confined to
+    small-magnitude entries (one block's dw_r row, a low-gate pair) show up
+    here although they hide under the infinity-norm bound's global max."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    if ref.size == 0:
+        return 0.0
+    den = np.maximum(np.abs(ref), floor * max(np.max(np.abs(ref)), 1e-30))
+    return float(np.max(np.abs(got - ref) / den))
+
+
+def relerr_rows(got, ref, floor=1e-3) -> float:
+    """Per-row infinity-norm relative error (rows = the leading axis after
+    flattening the rest), each row against its own max|o| floored at
+    floor * (global max|o|); returns the worst row.  Used for per-block
+    quantities (a block's dw rows, each block's dw_r row) so that one small
+    block cannot hide under a large one."""
+    got = np.asarray(got, np.float64).reshape(len(got), -1)
+    ref = np.asarray(ref, np.float64).reshape(len(ref), -1)
+    if ref.size == 0:
+        return 0.0
+    gmax = max(float(np.max(np.abs(ref))), 1e-30)
+    den = np.maximum(np.max(np.abs(ref), axis=1), floor * gmax)
+    return float(np.max(np.max(np.abs(got - ref), axis=1) / den))
+
+
+_ERRLOG = os.environ.get("SPT_ERRLOG")  # optional JSON-lines log of both metrics per check
+
+
+def _log_elementwise(got, ref, err):
+    if not _ERRLOG:
+        return
+    test = os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0]
+    with open(_ERRLOG, "a") as f:
+        f.write(json.dumps({"test": test, "shape": list(ref.shape), "inf_rel": err,
+                            "elem_floored": elemerr(got, ref)}) + "\n")
 
 
 def torch_dtype(cfg):
@@ -30,13 +75,14 @@ def to_dev(a, cfg):
 
 
 def gpu_run(cfg: S.FfnConfig, T: int, inputs: dict, logits_in=None, backward=True,
-            accumulate_from=None, want_dgate=True, balance_weight=0.0):
+            accumulate_from=None, want_dgate=True, balance_weight=0.0, deterministic=False):
     """Route -> forward -> backward through the ABI; returns numpy outputs
-    (balance_weight: lambda of the load-balancing loss; adds "loss_lb")."""
+    (balance_weight: lambda of the load-balancing loss; adds "loss_lb";
+    deterministic: SPT_FFN_DETERMINISTIC, the ascending-block k-way sums)."""
     import torch
     import paper_2312_10365_b200 as P
     f = P.RoutedFFN(T, cfg.d, cfg.D, cfg.G, cfg.k, torch_dtype(cfg), cfg.act, cfg.gate,
-                    balance_weight=balance_weight)
+                    balance_weight=balance_weight, deterministic=deterministic)
     x, w1, w2, w_r, dy = (to_dev(inputs[n], cfg) for n in ("x", "w1", "w2", "w_r", "dy"))
     flags = 0
     if logits_in is not None:

@@ -22,7 +22,7 @@ def test_library_exports_every_declared_symbol():
     assert set(decl) == set(_lib.EXPORTED), decl
     for name in decl:
         assert hasattr(L, name), name
-    assert L.spt_ffn_abi_version() == 4
+    assert L.spt_ffn_abi_version() == 5
 
 
 def test_status_strings():
@@ -98,7 +98,7 @@ def test_desc_layout_and_balance_weight_validation():
     import ctypes
     import torch
     from paper_2312_10365_b200 import _lib, spt_ffn_sizes
-    assert ctypes.sizeof(_lib.spt_ffn_desc) == 40
+    assert ctypes.sizeof(_lib.spt_ffn_desc) == 48  # ABI 5: + uint32 flags (padded)
     for bad in (-1.0, float("nan"), float("inf")):
         d = _desc(balance_weight=bad)
         s, w = ctypes.c_size_t(), ctypes.c_size_t()
@@ -107,6 +107,30 @@ def test_desc_layout_and_balance_weight_validation():
         _, w0 = spt_ffn_sizes(_desc(dtype=dt))
         _, w1 = spt_ffn_sizes(_desc(dtype=dt, balance_weight=0.01))
         assert w1 - w0 == extra, (dt, w1 - w0)
+
+
+def test_desc_flags():
+    """ABI 5: desc.flags -- unknown bits are rejected; SPT_FFN_DETERMINISTIC (bf16)
+    brings back the per-pair partial rows (T k d act elements) in place of the fp32
+    token accumulator of the fused k-way sums."""
+    import ctypes
+    import torch
+    from paper_2312_10365_b200 import _lib, spt_ffn_sizes
+    for bad in (2, 0x80000000):
+        d = _desc(dtype=torch.bfloat16)
+        d.flags = bad
+        s, w = ctypes.c_size_t(), ctypes.c_size_t()
+        assert _lib.lib().spt_ffn_sizes(ctypes.byref(d), ctypes.byref(s), ctypes.byref(w)) == 1
+    df = _desc(dtype=torch.bfloat16, d=256, D=1024, G=8, k=2)
+    dd = _desc(dtype=torch.bfloat16, d=256, D=1024, G=8, k=2)
+    dd.flags = _lib.SPT_FFN_DETERMINISTIC
+    (sf, wf), (sd, wd) = spt_ffn_sizes(df), spt_ffn_sizes(dd)
+    T = df.n_tokens
+    assert wd > wf and sf >= sd   # partial rows vs accumulator; window schedule in the stash
+    # fp32 path: the flag changes nothing
+    f0, f1 = _desc(), _desc()
+    f1.flags = _lib.SPT_FFN_DETERMINISTIC
+    assert spt_ffn_sizes(f0) == spt_ffn_sizes(f1)
 
 
 # ------------------------------------------------------------ LoRA (ABI 3)
@@ -177,5 +201,11 @@ def test_topl_null_and_unsupported():
     big = _lib.spt_topl_desc(1, 8, 20000, 16, 256, 4, 0)  # 20000 keys x 32 B > 227 KB smem
     dummy = ctypes.c_void_p(16)
     assert L.spt_mha_topl(ctypes.byref(big), dummy, dummy, dummy, None) == 2
+    # the kernel's 40,960 B of static smem count too: M = 16, E = 16 -> 24 B per key,
+    # (227 * 1024 - 40960) / 24 = 7978.67 keys fit
+    edge = _lib.spt_topl_desc(1, 8, 7979, 16, 16, 4, 0)
+    assert L.spt_mha_topl(ctypes.byref(edge), dummy, dummy, dummy, None) == 2
+    edge2 = _lib.spt_topl_desc(1, 8, 8192, 16, 16, 4, 0)
+    assert L.spt_mha_topl(ctypes.byref(edge2), dummy, dummy, dummy, None) == 2
     empty = _lib.spt_topl_desc(0, 8, 8, 8, 16, 2, 0)
     assert L.spt_mha_topl(ctypes.byref(empty), None, None, None, None) == 0

@@ -156,3 +156,56 @@ def test_lora_allreduce_equals_full_batch(orc):
         for r in range(world):
             got = res[r][n].astype(np.float64).reshape(ref.shape)
             assert np.max(np.abs(got - ref)) <= 1e-5 * max(1.0, np.max(np.abs(ref))), n
+
+
+def _balance_worker(rank, world, port, T, lam, out_q):
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = S.CONFIGS["tiny"].with_(act=S.ACT_GELU, d=64, D=256, G=8, k=3)
+    inp = S.make_inputs(cfg, T)
+    t0, t1 = dp.shard_range(T, rank, world)
+    x, dy = inp["x"][t0:t1], inp["dy"][t0:t1]
+    lg = oracle.router(x, inp["w_r"])
+    ti = oracle.topk(lg.astype(np.float32), cfg.k)
+    g = oracle.backward(x, inp["w1"], inp["w2"], inp["w_r"], lg, ti, dy, cfg.act, cfg.gate, lb_weight=lam)
+    fg = dp.FlatGrads({"dw1": g["dw1"].shape, "dw2": g["dw2"].shape, "dw_r": g["dw_r"].shape}, device="cpu")
+    for n in ("dw1", "dw2", "dw_r"):
+        fg[n].copy_(torch.from_numpy(g[n].astype(np.float32)))
+    dp.allreduce_grads(fg)
+    out_q.put((rank, fg["dw_r"].numpy().copy()))
+    dist.destroy_process_group()
+
+
+def test_balance_loss_is_per_shard(orc):
+    """dp.py's documented semantics of the load-balancing term under DP: the SUM
+    all-reduce gives sum_r lambda dL_r/dW_R with L_r the shard's own loss (its
+    f_g, pbar_g) -- equal to the sum of per-shard oracle gradients and NOT the
+    gradient of the global batch's loss."""
+    world, T, lam = 2, 80, 0.5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_balance_worker, args=(r, world, port, T, lam, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = S.CONFIGS["tiny"].with_(act=S.ACT_GELU, d=64, D=256, G=8, k=3)
+    inp = S.make_inputs(cfg, T)
+    per_shard = 0
+    for r in range(world):
+        t0, t1 = dp.shard_range(T, r, world)
+        lg = orc.router(inp["x"][t0:t1], inp["w_r"])
+        ti = orc.topk(lg.astype(np.float32), cfg.k)
+        per_shard = per_shard + orc.backward(inp["x"][t0:t1], inp["w1"], inp["w2"], inp["w_r"], lg, ti,
+                                             inp["dy"][t0:t1], cfg.act, cfg.gate, lb_weight=lam)["dw_r"]
+    lg = orc.router(inp["x"], inp["w_r"])
+    ti = orc.topk(lg.astype(np.float32), cfg.k)
+    glob = orc.backward(inp["x"], inp["w1"], inp["w2"], inp["w_r"], lg, ti, inp["dy"], cfg.act, cfg.gate,
+                        lb_weight=lam)["dw_r"]
+    for r in range(world):
+        np.testing.assert_allclose(res[r], per_shard, rtol=1e-5, atol=1e-6)
+    assert np.max(np.abs(per_shard - glob)) > 1e-4 * np.max(np.abs(glob))  # the readings differ

@@ -23,7 +23,9 @@ def _run(orc, cfg, T, lam, kind=None):
     inp = S.make_inputs(cfg, T)
     logits = None if kind is None else S.make_logits(T, cfg.G, cfg.k, kind, seed=cfg.seed)
     got = gpu_run(cfg, T, inp, logits_in=logits, balance_weight=lam)
-    lg = got["logits"].astype(np.float64)
+    # the oracle's own logits: the fixed ones, else its fp64 x W_R (never the GPU's)
+    lg = logits.astype(np.float64) if logits is not None else orc.router(inp["x"], inp["w_r"])
+    assert np.array_equal(got["topk_idx"], orc.topk(got["logits"], cfg.k))
     L, _ = orc.balance(lg, got["topk_idx"])
     assert abs(got["loss_lb"] - L) <= 1e-5 * max(1.0, abs(L)), (got["loss_lb"], L)
     ref = oracle_run(orc, cfg, inp, lg, got["topk_idx"], lb_weight=lam)

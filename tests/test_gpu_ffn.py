@@ -102,6 +102,15 @@ def test_wide_blocks_tiled(orc, name, d, D, G, k, act):
     _parity(orc, S.FfnConfig(name, d, D, G, k, 600, "bf16", act), 600)
 
 
+@pytest.mark.parametrize("name", ["opt2048_g8_b34", "llama4096_g8_b34", "opt2048_g4", "llama4096_g4",
+                                  "opt2048_g4_b34", "llama4096_g4_b34"])
+def test_paper_g4_g8_beta(orc, name):
+    """the paper's G = 4 / 8 groups at beta = 1/2 and 3/4 (Table 5,
+    PAPER.md:1023-1026, 1043-1046; "G (e.g., 4 or 8)"), full shapes
+    (bw 1024-2752) at a T the oracle's full backward covers in seconds."""
+    _parity(orc, S.PAPER_CONFIGS[name], 300)
+
+
 def test_k1_bf16(orc):
     cfg = S.FfnConfig("k1", 256, 2048, 16, 1, 400, "bf16", S.ACT_GELU)
     _parity(orc, cfg, 400)
@@ -137,15 +146,56 @@ def test_accumulate_dw(orc, name):
         assert relerr(acc[n] - prior[n], base[n]) < 1e-5
 
 
-@pytest.mark.parametrize("name", ["tiny", "llama"])
+@pytest.mark.parametrize("name", ["tiny", "bert", "llama"])
 def test_deterministic(orc, name):
+    """SPT_FFN_DETERMINISTIC: bitwise-reproducible results (ascending-block k-way
+    sums, reading c12); the fp32 path is deterministic either way."""
     cfg = S.CONFIGS[name]
     T = 513
     inp = S.make_inputs(cfg, T)
-    a = gpu_run(cfg, T, inp)
-    b = gpu_run(cfg, T, inp)
+    a = gpu_run(cfg, T, inp, deterministic=True)
+    b = gpu_run(cfg, T, inp, deterministic=True)
     for n in NAMES + ("logits", "bucket_token"):
         assert np.array_equal(a[n], b[n]), n
+
+
+@pytest.mark.parametrize("name,T", [("bert", 1000), ("opt", 600), ("llama", 513)])
+def test_fused_sums_match_deterministic(orc, name, T):
+    """The default fused k-way sums (fp32 reduce-add into the token accumulator in
+    hardware order, reading c12') against the deterministic ascending-order pass:
+    everything but y / dx is bitwise identical (same kernels), y / dx agree to the
+    fp32 summation-order level (plus one rounding to bf16); both pass the oracle."""
+    cfg = S.CONFIGS[name]
+    inp = S.make_inputs(cfg, T)
+    a = gpu_run(cfg, T, inp)
+    b = gpu_run(cfg, T, inp, deterministic=True)
+    for n in ("logits", "topk_idx", "bucket_token", "dw1", "dw2", "dw_r", "dgate"):
+        assert np.array_equal(a[n], b[n]), n
+    for n in ("y", "dx"):
+        scale = np.max(np.abs(b[n]))
+        assert np.max(np.abs(a[n] - b[n])) <= 2 ** -7 * scale, n   # <= one bf16 rounding step
+    lg = orc.router(inp["x"], inp["w_r"])
+    ref = oracle_run(orc, cfg, inp, lg, a["topk_idx"])
+    _check(cfg, b, ref)
+
+
+def test_fused_ragged_window(orc):
+    """T = 5000 with the default 4096-token window: a full and a ragged window of
+    the fused FWD2 / dX units."""
+    _parity(orc, S.CONFIGS["bert"], 5000)
+
+
+@pytest.mark.parametrize("kind", ["zipf", "same"])
+def test_deterministic_path_skewed(orc, kind):
+    """The deterministic (partial rows + ordered combine) path keeps its parity
+    coverage on skewed buckets too."""
+    cfg = S.CONFIGS["llama"]
+    T = 700
+    inp = S.make_inputs(cfg, T)
+    logits = S.make_logits(T, cfg.G, cfg.k, kind, seed=cfg.seed)
+    got = gpu_run(cfg, T, inp, logits_in=logits, deterministic=True)
+    ref = oracle_run(orc, cfg, inp, logits.astype(np.float64), got["topk_idx"])
+    _check(cfg, got, ref)
 
 
 @pytest.mark.parametrize("name", ["tiny", "llama"])

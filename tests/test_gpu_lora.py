@@ -162,7 +162,8 @@ def test_lora_fullsize_sampled(orc, name, n_blocks):
     got = gpu_run_lora(cfg, T, inp, lora, r)
     ti = orc.topk(got["logits"], cfg.k)
     assert np.array_equal(got["topk_idx"], ti)
-    lg = got["logits"].astype(np.float64)
+    lg = orc.router(inp["x"], inp["w_r"])   # the oracle's own fp64 logits (gates), full T
+    assert relerr(got["logits"], lg) <= 1e-4
     w1m, w2m = OL.merged_weights(inp["w1"], inp["w2"], lora, cfg.act)
     rng = np.random.default_rng(cfg.seed + 1)
     tokens = np.unique(np.concatenate([[0, T - 1], rng.integers(0, T, 14)])).astype(np.int64)

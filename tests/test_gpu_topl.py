@@ -109,3 +109,32 @@ def test_deterministic():
     a = gpu_topl(cq, ck, cfg.L)
     b = gpu_topl(cq, ck, cfg.L)
     assert np.array_equal(a, b)
+
+
+def test_max_keys_at_smem_limit():
+    """n_k at the shared-memory edge (dynamic + the kernel's static bucket state
+    = 227 KB): runs and matches the oracle on sampled queries."""
+    rng = np.random.default_rng(11)
+    M, nk, L = 16, 7978, 16
+    cq = rng.integers(0, 16, (1, 64, M)).astype(np.uint8)
+    ck = rng.integers(0, 16, (1, nk, M)).astype(np.uint8)
+    got = gpu_topl(cq, ck, L, E=16)
+    for q in (0, 31, 63):
+        ref = OT.topl_by_sort(cq[0][q:q + 1], ck[0], L, False)
+        assert np.array_equal(got[0][q:q + 1], ref)
+
+
+def test_out_of_range_codes_do_not_fault():
+    """Codes >= E are a caller error with unspecified indices but no fault (header):
+    on the packed path each code is masked to its nibble, so a score never exceeds M.
+    The next call on the same stream still succeeds and is exact."""
+    rng = np.random.default_rng(12)
+    M, n, L = 5, 300, 8
+    cq = rng.integers(0, 256, (2, n, M)).astype(np.uint8)
+    ck = rng.integers(0, 256, (2, n, M)).astype(np.uint8)
+    got = gpu_topl(cq, ck, L, E=16)
+    assert got.shape == (2, n, L) and np.all((got >= -1) & (got < n))
+    ok_q, ok_k = cq & 0x7, ck & 0x7
+    got2 = gpu_topl(ok_q, ok_k, L, E=16)
+    for h in range(2):
+        assert np.array_equal(got2[h], OT.alg3_topl(ok_q[h], ok_k[h], L, False))
