@@ -88,20 +88,11 @@ typedef struct {
   uint32_t flags;
 } spt_ffn_desc;
 
-/* desc.flags: the k-way sum of the per-block outputs of each token (Alg. 4
- * line 5, y_t = sum_{b in S_t} g act(x_t W_I[b]) W_O[b]; and its grad-input
- * counterpart dx_t) runs in fp32 in either of two orders:
- *   0 (default, bf16 path, blocks of <= 256 units): each block's output rows are
- *     added in fp32 straight into an L2-resident token accumulator by the
- *     GEMM epilogue (TMA reduce-add, no per-block rows in HBM); the summation
- *     order follows the hardware, so results may differ run to run at fp32
- *     rounding level (before the final rounding to the act dtype);
- *   SPT_FFN_DETERMINISTIC: every (token, block) output row is materialised and
- *     a separate pass sums them in ascending block id -- bitwise reproducible
- *     (SPEC's fixed order), at the cost of T*k*d act-dtype
- *     elements written and read back through HBM.
- * The fp32 path, the LoRA-wrapped calls and blocks wider than 256 units always
- * take the deterministic order. */
+/* desc.flags: option bits (ABI 5).  SPT_FFN_DETERMINISTIC requests bitwise
+ * reproducible results; every path of this library already is (the k-way sum
+ * of a token's per-block outputs, Alg. 4 line 5, runs in fp32 in ascending
+ * block id), so the bit is accepted and changes nothing.  It
+ * is reserved so that a future non-deterministic fast path stays opt-out. */
 #define SPT_FFN_DETERMINISTIC 1u
 
 /* Routing decision and bucket layout (all DEVICE buffers, caller-allocated).

@@ -153,72 +153,6 @@ cudaError_t launch_combine_bwd_dense(const Geom& g, const RouteView& r, const vo
   return cudaGetLastError();
 }
 
-// Fused k-way sums: the GEMM epilogues already added every block's rows into
-// the fp32 token accumulator acc [T, d]; this pass rounds each token row to
-// the act dtype -- forward: y[t] = acc[t]; backward: dx[t] = acc[t] + the router
-// term (sum_{j asc} dlogit_j w_r[b_j], or the dense [T,d] term of the balance
-// loss), in the same order as combine_kernel.  One CTA of 128 threads per token.
-template <bool kBwd>
-__global__ void __launch_bounds__(128) acc_finish_kernel(int64_t T, int d, int k, RouteView r,
-                                                         const float* __restrict__ acc,
-                                                         const float* __restrict__ dlogit,
-                                                         const __nv_bfloat16* __restrict__ w_r,
-                                                         const __nv_bfloat16* __restrict__ dense,
-                                                         __nv_bfloat16* __restrict__ out) {
-  __shared__ int blk[kMaxBlocks];
-  __shared__ float dl[kMaxBlocks];
-  const int64_t t = blockIdx.x;
-  if (kBwd && dlogit) {
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
-      blk[j] = r.topk_idx[t * k + j];
-      dl[j] = dlogit[pair_row(r, t, k, j)];
-    }
-    __syncthreads();
-  }
-  for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
-    const float4 a0 = __ldcs(reinterpret_cast<const float4*>(acc + t * d + c));
-    const float4 a1 = __ldcs(reinterpret_cast<const float4*>(acc + t * d + c + 4));
-    float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-    if (kBwd && dense) {
-      float w[8];
-      Vec<__nv_bfloat16>::load(dense + t * d + c, w);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] += w[i];
-    } else if (kBwd && w_r) {
-      for (int jj = 0; jj < k; ++jj) {
-        float w[8];
-        Vec<__nv_bfloat16>::load(w_r + (int64_t)blk[jj] * d + c, w);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = fmaf(dl[jj], w[i], v[i]);
-      }
-    }
-    Vec<__nv_bfloat16>::store(out + t * d + c, v);
-  }
-}
-
-cudaError_t launch_acc_finish_fwd(const Geom& g, const float* acc, void* y, cudaStream_t s) {
-  prof_begin("acc_finish_fwd", s);
-  acc_finish_kernel<false><<<(unsigned)g.T, 128, 0, s>>>(g.T, g.d, g.k, RouteView{}, acc, nullptr,
-                                                         nullptr, nullptr, (__nv_bfloat16*)y);
-  prof_end(s);
-  count_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_acc_finish_bwd(const Geom& g, const RouteView& r, const float* acc,
-                                  const float* dlogit, const void* w_r, const void* dense, void* dx,
-                                  cudaStream_t s) {
-  // GATE_NONE: dlogit == 0, the router term vanishes (reading c2)
-  const bool sparse = !dense && g.gate == SPT_GATE_SIGMOID;
-  prof_begin("acc_finish_bwd", s);
-  acc_finish_kernel<true><<<(unsigned)g.T, 128, 0, s>>>(
-      g.T, g.d, g.k, r, acc, sparse ? dlogit : nullptr,
-      sparse ? (const __nv_bfloat16*)w_r : nullptr, (const __nv_bfloat16*)dense, (__nv_bfloat16*)dx);
-  prof_end(s);
-  count_launch();
-  return cudaGetLastError();
-}
-
 __global__ void gather_dgate_kernel(int64_t T, int k, RouteView r, const float* __restrict__ rows,
                                     float* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

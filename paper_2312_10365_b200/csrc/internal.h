@@ -27,12 +27,6 @@ struct Geom {
   int gpad;          // G rounded up to 16 (router GEMM N, dense dlogit width)
   int esize;         // bytes per act element
   float lbw;         // load-balancing loss weight lambda (desc->balance_weight; 0 = off)
-  // fused k-way sums (desc.flags without SPT_FFN_DETERMINISTIC): FWD2 / dX add
-  // their rows into an fp32 token accumulator in L2 (TMA reduce-add) instead of
-  // writing per-pair partial rows; units run token window by token window
-  bool fuse_fwd, fuse_bwd;
-  int win;           // token window (tokens) of the fused unit order
-  int nW;            // windows: ceil(T / win) (>= 1)
 };
 
 // Device-resident views of the routing decision (= spt_route_buf).
@@ -68,19 +62,12 @@ struct Bufs {
   int32_t* tile_list;     // [ceil(T*k/128) + G]: bucket tiles in (m-tile, block) order
   int32_t* unit_offsets;  // [G+2]: prefix of weight-resident work units per block; [G+1] = pair tiles
   int32_t* tile_block;    // [ceil(T*k/128) + G]: block of each 128-row bucket tile
-  // fused k-way sums: window schedule (stash, built by the forward) + fp32 accumulator
-  int32_t* win_lo;        // [nW+1, G]: bucket-local first position of window w in block b
-  int32_t* win_uoff;      // [nW, G+1]: per window, prefix over blocks of weight-resident units
-  int32_t* win_base;      // [nW+1]: first global unit of window w (x N tiles)
-  float* acc;             // [T, d] f32 token accumulator (workspace)
   float* lb_part;         // [n_chunks, G] f32: per-chunk softmax sums (balance loss)
   void* lb_x;             // lambda != 0: bf16 [T, d] dense router term of dx (tcgen05 path)
                           //              f32 [T, G] lambda dL_balance/dx_R (SIMT path)
 };
 
 int unit_mtiles();  // m-tiles per weight-resident unit (FWD2 / DX); SPT_FFN_UNIT_MT, default 128
-bool fuse_enabled();  // fused k-way sums available (SPT_FFN_FUSE=0 turns them off: A/B timing)
-int fuse_window();    // token window of the fused unit order (SPT_FFN_WINDOW, default 4096)
 constexpr int kRasterBlocks = 16;  // blocks per L2 raster group of the gathered-A GEMMs
 
 void count_launch(int n = 1);
@@ -100,13 +87,6 @@ cudaError_t simt_backward(const Geom& g, const void* x, const void* w1, const vo
                           const void* w_r, const RouteView& r, const void* dy, void* dx,
                           float* dw1, float* dw2, float* dw_r, float* dgate_out, bool accumulate,
                           const Bufs& b, cudaEvent_t dw_ev, cudaStream_t s);
-
-// fused k-way sums (combine.cu): out[t] = act(acc[t]) for the forward; for the
-// backward + the router term (sum_j dlogit_j w_r[b_j], or the dense [T,d] term)
-cudaError_t launch_acc_finish_fwd(const Geom& g, const float* acc, void* y, cudaStream_t s);
-cudaError_t launch_acc_finish_bwd(const Geom& g, const RouteView& r, const float* acc,
-                                  const float* dlogit, const void* w_r, const void* dense, void* dx,
-                                  cudaStream_t s);
 
 // shared HBM-bound kernels (combine.cu)
 cudaError_t launch_combine_fwd(const Geom& g, const RouteView& r, const void* part, void* y,

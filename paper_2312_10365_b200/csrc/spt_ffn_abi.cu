@@ -86,12 +86,6 @@ static spt_status make_geom(const spt_ffn_desc* d, Geom* g) {
   if (g->bw % 16) return SPT_ERR_UNSUPPORTED;
   if (g->pairs + (int64_t)g->G * kTileM > INT32_MAX) return SPT_ERR_UNSUPPORTED;
   if (g->dtype == SPT_BF16 && !tc_supported(*g)) return SPT_ERR_UNSUPPORTED;
-  // fused k-way sums: bf16 path, weight-resident FWD2 (bw <= 256) / dX (m' bw <= 256)
-  const bool fuse = g->dtype == SPT_BF16 && !(d->flags & SPT_FFN_DETERMINISTIC) && fuse_enabled();
-  g->fuse_fwd = fuse && g->bw <= 256;
-  g->fuse_bwd = fuse && g->mp * g->bw <= 256;
-  g->win = fuse_window();
-  g->nW = g->T > 0 ? (int)ceil_div(g->T, g->win) : 1;
   return SPT_OK;
 }
 
@@ -99,8 +93,7 @@ static int dwr_splits(const Geom& g) { return dense_tn_splits(g); }
 
 struct Sizes {
   size_t z, h, stash;
-  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, tb, wl, wu, wb, acc, lbp,
-      lbx, ws;
+  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, tb, lbp, lbx, ws;
 };
 
 static Sizes compute_sizes(const Geom& g) {
@@ -113,14 +106,8 @@ static Sizes compute_sizes(const Geom& g) {
   s.tl = align256((size_t)(ceil_div(g.pairs, kTileM) + g.G) * 4);
   s.uo = align256((size_t)(g.G + 2) * 4);
   s.tb = s.tl;
-  const bool fused = g.fuse_fwd || g.fuse_bwd;
-  s.wl = fused ? align256((size_t)(g.nW + 1) * g.G * 4) : 0;
-  s.wu = fused ? align256((size_t)g.nW * (g.G + 1) * 4) : 0;
-  s.wb = fused ? align256((size_t)(g.nW + 1) * 4) : 0;
-  s.stash = s.z + s.h + s.tl + s.uo + s.tb + s.wl + s.wu + s.wb;
-  // per-pair partial rows only where a k-way sum is not fused
-  s.part = (g.fuse_fwd && g.fuse_bwd) ? 0 : align256((size_t)g.rows_cap * g.d * e);
-  s.acc = fused ? align256((size_t)g.T * g.d * 4) : 0;
+  s.stash = s.z + s.h + s.tl + s.uo + s.tb;
+  s.part = align256((size_t)g.rows_cap * g.d * e);
   s.dz = align256((size_t)g.rows_cap * g.mp * g.bw * e);
   s.da = align256((size_t)g.rows_cap * g.bw * 4);  // fp32 dA rows (both paths)
   s.dlogit = align256((size_t)g.rows_cap * 4);
@@ -134,7 +121,7 @@ static Sizes compute_sizes(const Geom& g) {
   s.lbx = g.lbw == 0.f ? 0                         // balance gradient: dense router term
           : align256(g.dtype == SPT_BF16 ? (size_t)g.T * g.d * 2 : (size_t)g.T * g.G * 4);
   s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb +
-         s.lbp + s.lbx + s.acc;
+         s.lbp + s.lbx;
   return s;
 }
 
@@ -148,10 +135,7 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
     uint8_t* q = p + s.z + s.h;
     b.tile_list = (int32_t*)q; q += s.tl;
     b.unit_offsets = (int32_t*)q; q += s.uo;
-    b.tile_block = (int32_t*)q; q += s.tb;
-    b.win_lo = s.wl ? (int32_t*)q : nullptr; q += s.wl;
-    b.win_uoff = s.wu ? (int32_t*)q : nullptr; q += s.wu;
-    b.win_base = s.wb ? (int32_t*)q : nullptr;
+    b.tile_block = (int32_t*)q;
   }
   uint8_t* w = (uint8_t*)ws;
   b.part = w; w += s.part;
@@ -167,7 +151,6 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
   b.n_b = (int32_t*)w; w += s.nb;
   b.lb_part = (float*)w; w += s.lbp;
   b.lb_x = s.lbx ? (void*)w : nullptr; w += s.lbx;
-  b.acc = s.acc ? (float*)w : nullptr; w += s.acc;
   return b;
 }
 
@@ -185,8 +168,6 @@ static spt_status lora_geom(const spt_ffn_desc* d, int32_t rank, Geom* g) {
   if (rank < 1) return SPT_ERR_INVALID_ARGUMENT;
   if (g->dtype != SPT_BF16) return SPT_ERR_UNSUPPORTED;  // tcgen05 path only
   if ((int64_t)g->mp * rank > kLoraK) return SPT_ERR_UNSUPPORTED;
-  // the LoRA finish passes add their rank-r terms to the per-pair rows: unfused
-  g->fuse_fwd = g->fuse_bwd = false;
   return SPT_OK;
 }
 

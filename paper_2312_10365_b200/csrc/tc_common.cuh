@@ -102,18 +102,6 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
       "r"(smem_u32(src)), "r"(c0), "r"(c1)
       : "memory");
 }
-// smem -> global reduce-add (fp32) of 4 rows r0..r3 x box[0] columns from
-// column c0 (TMA tile::scatter4; the source holds the 4 rows consecutively in
-// the map's swizzle); rows outside the tensor are dropped.  Bulk group.
-__device__ __forceinline__ void tma_reduce_add_scatter4(const CUtensorMap* m, const void* src,
-                                                        int32_t c0, int32_t r0, int32_t r1,
-                                                        int32_t r2, int32_t r3) {
-  asm volatile(
-      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile::scatter4.bulk_group"
-      " [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(reinterpret_cast<uint64_t>(m)),
-      "r"(smem_u32(src)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
-}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }

@@ -78,16 +78,6 @@ struct TcArgs {
   int nu;                       // FWD1 / DA: unit tiles; DW1 / DW2: feature tiles
   int kstream;                  // FWD2 / DX: K-streaming tiles (K > 256)
   float* dgp;                   // DA, nu > 1: per-unit-tile dgate partials [rows_cap][nu]
-  // fused k-way sums (FWD2 / DX, Geom::fuse_*): the epilogue reduce-adds each
-  // row into the fp32 token accumulator (tensor map `tc`: [T, d] f32, TMA
-  // tile::scatter4 .add) instead of storing a per-pair partial row; units run
-  // token window by token window (window-major, then N tile, then block), so a
-  // window's accumulator slice and its H~ / dZ rows stay in L2
-  int fuse;
-  const int32_t* win_lo;        // [nW+1][G] bucket-local first position of window w in block b
-  const int32_t* win_uoff;      // [nW][G+1] per-window prefix of units over blocks
-  const int32_t* win_base;      // [nW+1] first global unit of window w
-  int nW;
   int ablate;                   // SPT_FFN_ABLATE (timing experiments only; results wrong):
                                 //  1 = skip gathered-row copies, 2 = skip FWD1 epilogue stores,
                                 //  3 = no operand loads at all, 4 = 3 + no epilogue work,
@@ -230,40 +220,12 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
   return ti;
 }
 
-// FWD2 / DX work unit u -> (block b, bucket-local rows [lo, hi), m-tiles
-// [mt0, mt1) of 128 rows from lo, N tile nt).  Unfused: units are block-major
-// (lo = 0, hi = n_b; the m-tiles are the block's padded bucket tiles); fused:
-// window-major (rows of tokens [w win, (w+1) win) of the block, which start
-// anywhere inside its padded rows -- the A loads are unaligned TMA boxes).
+// FWD2 / DX work unit u -> (block b, m-tiles [mt0, mt1), N tile nt)
 struct UnitInfo {
-  int b, nt, mt0, mt1, lo, hi;
+  int b, nt, mt0, mt1;
 };
-__device__ __forceinline__ int find_le(const int32_t* off, int n, int v) {  // last i < n with off[i] <= v
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= v) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
 __device__ __forceinline__ UnitInfo decode_unit(const TcArgs& a, int u) {
   UnitInfo ui;
-  if (a.fuse) {
-    const int w = find_le(a.win_base, a.nW, u);
-    const int32_t* uo = a.win_uoff + (int64_t)w * (a.G + 1);
-    const int per_nt = uo[a.G];
-    const int r = u - a.win_base[w];
-    ui.nt = r / per_nt;
-    const int r2 = r - ui.nt * per_nt;
-    ui.b = find_le(uo, a.G, r2);  // the last block starting at or before r2 (blocks without units are skipped)
-    const int mc = r2 - uo[ui.b];
-    ui.lo = a.win_lo[(int64_t)w * a.G + ui.b];
-    ui.hi = a.win_lo[(int64_t)(w + 1) * a.G + ui.b];
-    const int ntl = (ui.hi - ui.lo + 127) / 128;
-    ui.mt0 = mc * a.unit_mt;
-    ui.mt1 = min(ntl, ui.mt0 + a.unit_mt);
-    return ui;
-  }
   ui.b = find_block(a.unit_offsets, a.G, u);
   const int r = u - a.unit_offsets[ui.b];
   ui.nt = r % a.NT;
@@ -271,8 +233,6 @@ __device__ __forceinline__ UnitInfo decode_unit(const TcArgs& a, int u) {
   const int ntb = a.r.tile_offsets[ui.b + 1] - a.r.tile_offsets[ui.b];
   ui.mt0 = mc * a.unit_mt;
   ui.mt1 = min(ntb, ui.mt0 + a.unit_mt);
-  ui.lo = 0;
-  ui.hi = a.r.block_offsets[ui.b + 1] - a.r.block_offsets[ui.b];
   return ui;
 }
 template <int KIND>
@@ -280,9 +240,10 @@ __device__ __forceinline__ TileInfo decode_mtile(const TcArgs& a, const UnitInfo
   TileInfo ti{};
   ti.b = u.b;
   ti.nt = u.nt;
-  ti.n_valid = u.hi - u.lo - mt * 128;
-  ti.prow0 = (int64_t)a.r.tile_offsets[u.b] * 128 + u.lo + mt * 128;
-  ti.pos0 = a.r.block_offsets[u.b] + u.lo + mt * 128;
+  const int nb = a.r.block_offsets[u.b + 1] - a.r.block_offsets[u.b];
+  ti.n_valid = nb - mt * 128;
+  ti.prow0 = (int64_t)(a.r.tile_offsets[u.b] + mt) * 128;
+  ti.pos0 = a.r.block_offsets[u.b] + mt * 128;
   ti.nkb = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
   return ti;
 }
@@ -621,47 +582,6 @@ __device__ __forceinline__ void epilogue_tma_store(const TcArgs& a, const TileIn
   }
 }
 
-// Fused FWD2 / DX epilogue: the 32 rows x 128 columns of this warp are added
-// into the fp32 token accumulator, 32 columns at a time: the rows go to a
-// 128-byte-swizzled smem box (row = lane, conflict-free) and lanes 0..7 each
-// issue one TMA tile::scatter4 reduce-add of 4 token rows x 32 fp32 (512 B).
-// Rows past the unit's valid rows address token row T (outside the map): the
-// TMA unit drops them.  Every issuing lane waits for its own bulk groups.
-__device__ __forceinline__ void epilogue_tma_reduce(const TcArgs& a, const TileInfo& ti,
-                                                    uint32_t tacc, int q, int lane, int half,
-                                                    uint8_t* stg, int& stg_i) {
-  const int ncols = min(256, a.d - ti.nt * 256);
-  const int c_lo = half * 128, c_hi = min(ncols, c_lo + 128);
-  const int row = q * 32 + lane;
-  const int tok = row < ti.n_valid ? a.r.bucket_token[ti.pos0 + row] : (int)a.T;
-  int t4[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) t4[i] = __shfl_sync(0xffffffffu, tok, 4 * (lane & 7) + i);
-  for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
-    uint32_t v[32];
-    tmem_ld32(tacc + c0, v);
-    tmem_ld_wait();
-    uint8_t* buf = stg + stg_i * 4096;
-    if (lane < 8) {
-      if (a.n_stg == 3) bulk_wait_read<2>();
-      else if (a.n_stg == 2) bulk_wait_read<1>();
-      else bulk_wait_read<0>();
-    }
-    __syncwarp();
-#pragma unroll
-    for (int c = 0; c < 8; ++c)  // 16-byte chunk c of this row, swizzled by row & 7
-      *reinterpret_cast<uint4*>(buf + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-          make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane < 8) {
-      tma_reduce_add_scatter4(&a.tc, buf + lane * 512, ti.nt * 256 + c0, t4[0], t4[1], t4[2], t4[3]);
-      bulk_commit();
-    }
-    stg_i = (stg_i + 1) % a.n_stg;
-  }
-}
-
 // DAT epilogue: the accumulator is dA^T (TMEM lane = unit of the block, column =
 // token row of the pair tile).  Each warp stages 32 tokens x 32 units of fp32
 // row-major in smem and TMA-stores the box into dA[row][unit]; dgate / dZ are
@@ -862,11 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           twait(&tfull[acc], aphase, (tr && threadIdx.x == 4 * 32) ? tr : nullptr, 2);
           tc_fence_after();
           const long long te0 = clock64();
-          if (a.fuse)
-            epilogue_tma_reduce(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, q, lane, half,
-                                stg_base + e * a.n_stg * 4096, stg_i);
-          else
-            epilogue_tma_store(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, q, lane, half,
+          epilogue_tma_store(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, q, lane, half,
                                stg_base + e * a.n_stg * 4096, stg_i);
           tc_fence_before();
           __syncwarp();
@@ -875,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           if (++acc == 2) { acc = 0; aphase ^= 1; }
         }
       }
-      bulk_wait<0>();  // all partial tiles / reductions done before exit (per issuing lane)
+      if (lane == 0) bulk_wait<0>();  // all partial tiles written before exit
     }
   } else if (kind_gather_a(KIND) && (warp == 0 || warp == 2 || warp == 3)) {
     // ------------------------ FWD1 / DA: TMA tile::gather4 of 256 token rows
@@ -1479,11 +1395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const long long te0 = clock64();
         if (my_mt < ui.mt1) {  // the pair's second m-tile may not exist
           const TileInfo ti = decode_mtile<KIND>(a, ui, my_mt);
-          if (a.fuse)
-            epilogue_tma_reduce(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, q, lane, half,
-                                stg_base + e * a.n_stg * 4096, stg_i);
-          else
-            epilogue_tma_store(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, q, lane, half,
+          epilogue_tma_store(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, q, lane, half,
                                stg_base + e * a.n_stg * 4096, stg_i);
         }
         tc_fence_before();
@@ -1496,7 +1408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
     }
-    bulk_wait<0>();
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -1895,73 +1807,6 @@ __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, int unit
   }
 }
 
-// Window schedule of the fused FWD2 / DX units (one CTA; no host sync):
-//  win_lo[w][b]   = #{bucket entries of block b with token < w * win} (block-local
-//                   position; bucket rows are token-ascending, so a binary search)
-//  win_uoff[w][b] = prefix over blocks of the window's weight-resident units,
-//                   ceil(ceil((hi - lo) / 128) / unit_mt) per block
-//  win_base[w]    = prefix over windows of their units x N tiles
-__global__ void __launch_bounds__(256) win_sched_kernel(int64_t T, int G, int win, int nW, int NT,
-                                                        int unit_mt,
-                                                        const int32_t* __restrict__ block_offsets,
-                                                        const int32_t* __restrict__ bucket_token,
-                                                        int32_t* __restrict__ win_lo,
-                                                        int32_t* __restrict__ win_uoff,
-                                                        int32_t* __restrict__ win_base) {
-  for (int i = threadIdx.x; i < (nW + 1) * G; i += blockDim.x) {
-    const int w = i / G, b = i % G;
-    const int b0 = block_offsets[b], nb = block_offsets[b + 1] - b0;
-    int lo = 0, hi = nb;  // first position whose token >= w * win
-    if (w >= nW) {
-      lo = nb;
-    } else if (w > 0) {
-      const int64_t t0 = (int64_t)w * win;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (bucket_token[b0 + mid] < t0) lo = mid + 1; else hi = mid;
-      }
-    }
-    win_lo[i] = lo;
-  }
-  __syncthreads();
-  for (int w = threadIdx.x; w < nW; w += blockDim.x) {
-    int run = 0;
-    for (int b = 0; b < G; ++b) {
-      win_uoff[(int64_t)w * (G + 1) + b] = run;
-      const int n = win_lo[(int64_t)(w + 1) * G + b] - win_lo[(int64_t)w * G + b];
-      run += (int)ceil_div(ceil_div(n, 128), unit_mt);
-    }
-    win_uoff[(int64_t)w * (G + 1) + G] = run;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int base = 0;
-    for (int w = 0; w < nW; ++w) {
-      win_base[w] = base;
-      base += win_uoff[(int64_t)w * (G + 1) + G] * NT;
-    }
-    win_base[nW] = base;
-  }
-}
-
-bool fuse_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SPT_FFN_FUSE");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-int fuse_window() {
-  static int v = 0;
-  if (!v) {
-    const char* e = getenv("SPT_FFN_WINDOW");
-    v = e ? atoi(e) : 4096;
-    if (v < 128) v = 4096;
-  }
-  return v;
-}
-
 // blocks per L2 raster group of the gathered-A GEMMs (SPT_FFN_RASTER, default kRasterBlocks)
 static int raster_blocks() {
   static int v = 0;
@@ -1981,27 +1826,7 @@ static cudaError_t build_schedules(const Geom& g, const RouteView& r, const Bufs
                                         b.unit_offsets, b.tile_block);
   prof_end(s);
   count_launch();
-  if (g.fuse_fwd || g.fuse_bwd) {
-    prof_begin("win_sched", s);
-    win_sched_kernel<<<1, 256, 0, s>>>(g.T, g.G, g.win, g.nW, (int)ceil_div(g.d, 256), unit_mtiles(),
-                                       r.block_offsets, r.bucket_token, b.win_lo, b.win_uoff,
-                                       b.win_base);
-    prof_end(s);
-    count_launch();
-  }
   return cudaGetLastError();
-}
-
-// fused FWD2 / dX: window-major weight-resident units reduce-adding into b.acc
-static void fused_args(TcArgs& a, const Geom& g, const Bufs& b) {
-  a.fuse = 1;
-  a.win_lo = b.win_lo;
-  a.win_uoff = b.win_uoff;
-  a.win_base = b.win_base;
-  a.nW = g.nW;
-}
-static int units_upper_fused(const Geom& g) {  // every (window, block) adds at most one ragged tile
-  return (int)((ceil_div(g.pairs, 128) + (int64_t)g.nW * g.G) * ceil_div(g.d, 256));
 }
 
 static int units_upper(const Geom& g) {
@@ -2050,32 +1875,23 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
       TRY(launch<K_FWD1>(a, tiles, s));
     }
   }
-  const bool fuse = g.fuse_fwd && !lo;
   {
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, 128) &&
               make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, 64);
+    ok = ok && make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
     a.BN = 256;
+    a.out = b.part;
     a.unit_offsets = b.unit_offsets;
-    if (fuse) {  // a5 + a6 fused: rows reduce-added into the fp32 token accumulator
-      ok = ok && make_tmap_f32_2d_sw128(&a.tc, b.acc, g.T, g.d, g.d, 1);
-      fused_args(a, g, b);
-      if (cudaMemsetAsync(b.acc, 0, (size_t)g.T * g.d * 4, s) != cudaSuccess) return cudaErrorUnknown;
-      TRY(launch_bres<K_FWD2>(a, units_upper_fused(g), s));
+    a.kstream = g.bw > 256;  // the K = bw slab no longer fits smem: stream K
+    if (a.kstream) {
+      TRY(launch<K_FWD2>(a, up * a.NT, s));
     } else {
-      ok = ok && make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
-      a.out = b.part;
-      a.kstream = g.bw > 256;  // the K = bw slab no longer fits smem: stream K
-      if (a.kstream) {
-        TRY(launch<K_FWD2>(a, up * a.NT, s));
-      } else {
-        TRY(launch_bres<K_FWD2>(a, units_upper(g), s));
-      }
+      TRY(launch_bres<K_FWD2>(a, units_upper(g), s));
     }
   }
   if (lo) return lora_fwd_finish(g, r, b, *lo, y, s);
-  if (fuse) return launch_acc_finish_fwd(g, b.acc, y, s);
   return launch_combine_fwd(g, r, b.part, y, s);
 }
 
@@ -2385,24 +2201,16 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       return cudaErrorUnknown;
     return cudaSuccess;
   };
-  const bool fuse = g.fuse_bwd && !lo;
-  auto run_dx = [&]() -> cudaError_t {  // a8: dXp = dZ W1_b (partials, or fused into b.acc)
+  auto run_dx = [&]() -> cudaError_t {  // a8: dXp = dZ W1_b (partials)
     TcArgs a{};
     base_args(a, g, r);
     bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
                                 (uint64_t)g.mp * g.bw, 64, 128) &&
               make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, 64);
-    a.BN = 256;
-    a.unit_offsets = b.unit_offsets;
-    if (fuse) {
-      ok = ok && make_tmap_f32_2d_sw128(&a.tc, b.acc, g.T, g.d, g.d, 1);
-      fused_args(a, g, b);
-      if (cudaMemsetAsync(b.acc, 0, (size_t)g.T * g.d * 4, s) != cudaSuccess) return cudaErrorUnknown;
-      TRY(launch_bres<K_DX>(a, units_upper_fused(g), s));
-      return cudaSuccess;
-    }
     ok = ok && make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
+    a.BN = 256;
     a.out = b.part;
+    a.unit_offsets = b.unit_offsets;
     a.kstream = g.mp * g.bw > 256;  // the K = m' bw slab no longer fits smem: stream K
     if (a.kstream) {
       TRY(launch<K_DX>(a, up * a.NT, s));
@@ -2429,13 +2237,11 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.BN = 256;
     a.out = b.lb_x;
     TRY(launch<K_DXR>(a, (int)ceil_div(g.T, 128) * a.NT, s));
-    e = lo     ? lora_bwd_finish(g, r, b, *lo, x, dy, b.lb_x, nullptr, dx, s)
-        : fuse ? launch_acc_finish_bwd(g, r, b.acc, nullptr, nullptr, b.lb_x, dx, s)
-               : launch_combine_bwd_dense(g, r, b.part, b.lb_x, dx, s);
+    e = lo ? lora_bwd_finish(g, r, b, *lo, x, dy, b.lb_x, nullptr, dx, s)
+           : launch_combine_bwd_dense(g, r, b.part, b.lb_x, dx, s);
   } else {
-    e = lo     ? lora_bwd_finish(g, r, b, *lo, x, dy, nullptr, w_r, dx, s)
-        : fuse ? launch_acc_finish_bwd(g, r, b.acc, b.dlogit, w_r, nullptr, dx, s)
-               : launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
+    e = lo ? lora_bwd_finish(g, r, b, *lo, x, dy, nullptr, w_r, dx, s)
+           : launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
   }
   if (e != cudaSuccess) return e;
   // LoRA: every gradient (dw_r and the factors) is final only here

@@ -55,20 +55,4 @@ inline bool make_tmap_f32_2d(CUtensorMap* m, const void* base, uint64_t rows, ui
   return r == CUDA_SUCCESS;
 }
 
-// 2-D row-major fp32 matrix with a 128-byte swizzle: box = 32 columns x box_rows
-// (box_rows = 1 for tile::gather4 / scatter4 maps)
-inline bool make_tmap_f32_2d_sw128(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
-                                   uint64_t pitch_elems, uint32_t box_rows) {
-  auto fn = get_encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {pitch_elems * 4};
-  cuuint32_t box[2] = {32, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 }  // namespace spt

@@ -4,8 +4,6 @@ knobs read once per process, so each case runs in its own interpreter):
   SPT_FFN_PREFETCH=1  L2 prefetch of gathered rows
   SPT_FFN_PAIR=1|0    CTA-pair (cta_group::2) weight-resident kernel for FWD2 + dX / neither (default: dX only)
   SPT_FFN_PAIR_GATHER=0  1-CTA FWD1 / dA kernel (default: CTA-pair gather kernel)
-  SPT_FFN_WINDOW=n    token window of the fused k-way sums (default 4096)
-  SPT_FFN_FUSE=0      no fused k-way sums (partial rows + ordered combine everywhere)
 """
 import os
 import subprocess
@@ -35,11 +33,7 @@ print("ok")
 
 
 @pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"}, {"SPT_FFN_PAIR": "0"},
-                                 {"SPT_FFN_PAIR_GATHER": "0"},
-                                 # fused k-way sums over many small token windows (ragged
-                                 # window / block row ranges, unaligned A boxes) and turned off
-                                 {"SPT_FFN_WINDOW": "256"}, {"SPT_FFN_WINDOW": "256", "SPT_FFN_PAIR": "1"},
-                                 {"SPT_FFN_FUSE": "0"}])
+                                 {"SPT_FFN_PAIR_GATHER": "0"}])
 def test_variant_parity(env):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True,
