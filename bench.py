@@ -69,6 +69,10 @@ def kernel_work(cfg, T):
         "combine_bwd": ("hbm", P * d * e + 12.0 * P + T * d * e),
         "topk_hist": ("hbm", 4.0 * T * G + 8.0 * T * cfg.k),
         "bucket_scatter": ("hbm", 20.0 * P),
+        # fp32 on tensor cores (reading c13'): fp32 -> bf16 hi | lo copies of x (route,
+        # forward, backward), dy, w1, w2 (forward, backward) and w_r (route); 4 bytes read
+        # + 4 written per element, averaged over the step's 9 launches
+        "split_bf16": ("hbm", 8.0 * (3 * T * d + T * d + 2 * (mp * cfg.D * d + cfg.D * d) + G * d) / 9),
         # fp32 path (tiny config): CUDA-core FFMA kernels, no tensor cores (reading c13)
         "simt_f1": ("alu", 2.0 * P * mp * bw * d),
         "simt_f2": ("alu", 2.0 * P * bw * d),
@@ -661,7 +665,9 @@ def main():
         kind, amt = work.get(dom, ("tensor", 0.0))
         traffic = None
         tp = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
-        if os.path.exists(tp) and cfg.name == "llama_scale" and T == 32768:
+        # the capture is of the plain bf16 step: never attach it to a LoRA / other line
+        if os.path.exists(tp) and cfg.name == "llama_scale" and T == 32768 and not args.lora \
+                and not args.balance_weight:
             kt = json.load(open(tp))["kernels"].get(dom)
             if kt:
                 traffic = kt["dram_read_bytes"] + kt["dram_write_bytes"]
@@ -675,10 +681,15 @@ def main():
                         "share_of_step": tot / args.steps / step_ms_prof}
         elif kind == "tensor":
             ach = amt / (per / 1e3) / 1e12
-            roofline = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk["bf16_sustained"],
-                        "unit": "TFLOP/s", "frac": ach / pk["bf16_sustained"], "traffic": traffic,
+            # fp32 (split path, reading c13'): every fp32 product is three bf16 tensor-core
+            # products, so the fp32 roof is the measured bf16 rate / 3
+            f32 = cfg.dtype == "f32"
+            peak = pk["bf16_sustained"] / 3 if f32 else pk["bf16_sustained"]
+            roofline = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": peak,
+                        "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
                         "traffic_src": "profiles/r01_ncu_traffic.json (dram read+write bytes per launch)",
-                        "peak_src": pk["src"] + " bf16 sustained",
+                        "peak_src": pk["src"] + " bf16 sustained" +
+                                    (" / 3 (fp32 as hi*hi + hi*lo + lo*hi bf16 products)" if f32 else ""),
                         "algorithmic_per_launch": amt, "ms_per_launch": per,
                         "share_of_step": tot / args.steps / step_ms_prof}
         else:

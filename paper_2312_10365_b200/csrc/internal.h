@@ -27,6 +27,12 @@ struct Geom {
   int gpad;          // G rounded up to 16 (router GEMM N, dense dlogit width)
   int esize;         // bytes per act element
   float lbw;         // load-balancing loss weight lambda (desc->balance_weight; 0 = off)
+  // fp32 path on the bf16 tensor cores (reading c13'): every fp32 operand is
+  // split into bf16 hi + lo and each GEMM sums the hi*hi, hi*lo and lo*hi
+  // products in fp32.  Intermediates (Z, H~, dZ) are stored as bf16 hi / lo
+  // halves (esize 4 = both halves, hi first), per-pair partials as fp32.
+  bool split;
+  bool tc() const { return dtype == SPT_BF16 || split; }  // tcgen05 kernels (else SIMT)
 };
 
 // Device-resident views of the routing decision (= spt_route_buf).
@@ -65,7 +71,18 @@ struct Bufs {
   float* lb_part;         // [n_chunks, G] f32: per-chunk softmax sums (balance loss)
   void* lb_x;             // lambda != 0: bf16 [T, d] dense router term of dx (tcgen05 path)
                           //              f32 [T, G] lambda dL_balance/dx_R (SIMT path)
+  // split (fp32 on tensor cores): bf16 hi | lo copies of the fp32 operands
+  void* xs;               // [2][T, d]
+  void* dys;              // [2][T, d]
+  void* w1s;              // [2][m' D, d]
+  void* w2s;              // [2][D, d]
+  void* wrs;              // [2][G, d]
 };
+
+// split: the lo half of a hi | lo pair of bf16 tensors of n elements each
+inline const void* lo_half(const void* hi, int64_t n) { return (const uint8_t*)hi + n * 2; }
+inline void* lo_half(void* hi, int64_t n) { return (uint8_t*)hi + n * 2; }
+bool simt_forced();  // SPT_FFN_SIMT=1: fp32 runs on the SIMT kernels (A/B of the split path)
 
 int unit_mtiles();  // m-tiles per weight-resident unit (FWD2 / DX); SPT_FFN_UNIT_MT, default 128
 constexpr int kRasterBlocks = 16;  // blocks per L2 raster group of the gathered-A GEMMs
@@ -171,12 +188,15 @@ cudaError_t launch_topl(int H, int nq, int nk, int M, int E, int L, int causal,
 
 // tcgen05 path (tc_ffn.cu), bf16 only
 bool tc_supported(const Geom& g);
+// split (g.split): x / w_r are fp32 and the hi | lo copies go to b.xs / b.wrs
 cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logits,
-                      cudaStream_t s);
+                      cudaStream_t s, const Bufs* b = nullptr);
+// fp32 -> bf16 hi | lo halves (hi at dst, lo at lo_half(dst, n)), RNE both
+cudaError_t launch_split_bf16(const float* src, void* dst, int64_t n, cudaStream_t s);
 // dense split-K  out[G, d] (=|+=) A^T B  with A given as bf16 hi|lo halves [2, T, gpad]
 // and B [T, d] bf16 (the dW_R GEMM; also dB_I / dC_O of the LoRA path)
 cudaError_t tc_dense_tn(const Geom& g, const void* ahl, const void* bmat, float* part, int n_split,
-                        float* out, bool accumulate, cudaStream_t s);
+                        float* out, bool accumulate, cudaStream_t s, const void* bmat_lo = nullptr);
 int dense_tn_splits(const Geom& g);
 // dense  out[T, d] (bf16) = A B  with A given as bf16 hi|lo halves [2, T, gpad] and
 // B [G, d] bf16 (the dx router term of the balance loss; the du B_I^T term of LoRA)

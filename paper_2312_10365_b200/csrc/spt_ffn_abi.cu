@@ -86,6 +86,10 @@ static spt_status make_geom(const spt_ffn_desc* d, Geom* g) {
   if (g->bw % 16) return SPT_ERR_UNSUPPORTED;
   if (g->pairs + (int64_t)g->G * kTileM > INT32_MAX) return SPT_ERR_UNSUPPORTED;
   if (g->dtype == SPT_BF16 && !tc_supported(*g)) return SPT_ERR_UNSUPPORTED;
+  // fp32: the split tensor-core path wherever the tcgen05 kernels support the
+  // shape; the SIMT kernels otherwise (G > 128) and for the load-balancing
+  // gradient (its dense dX term has no split kernel)
+  g->split = g->dtype == SPT_F32 && tc_supported(*g) && g->lbw == 0.f && !simt_forced();
   return SPT_OK;
 }
 
@@ -93,7 +97,7 @@ static int dwr_splits(const Geom& g) { return dense_tn_splits(g); }
 
 struct Sizes {
   size_t z, h, stash;
-  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, tb, lbp, lbx, ws;
+  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, tb, lbp, lbx, xs, ws_w, ws;
 };
 
 static Sizes compute_sizes(const Geom& g) {
@@ -112,8 +116,13 @@ static Sizes compute_sizes(const Geom& g) {
   s.da = align256((size_t)g.rows_cap * g.bw * 4);  // fp32 dA rows (both paths)
   s.dlogit = align256((size_t)g.rows_cap * 4);
   s.dgate = align256((size_t)g.rows_cap * 4);
-  s.dlg = g.dtype == SPT_BF16 ? align256((size_t)2 * g.T * g.gpad * 2) : 0;
-  s.dwr = g.dtype == SPT_BF16 ? align256((size_t)dwr_splits(g) * g.G * g.d * 4) : 0;
+  s.dlg = g.tc() ? align256((size_t)2 * g.T * g.gpad * 2) : 0;
+  s.dwr = g.tc() ? align256((size_t)dwr_splits(g) * g.G * g.d * 4) : 0;
+  // split: bf16 hi | lo copies of x, dy and the weights (4 bytes per element)
+  s.xs = g.split ? align256((size_t)g.T * g.d * 4) : 0;
+  s.ws_w = g.split ? align256((size_t)g.mp * g.D * g.d * 4) + align256((size_t)g.D * g.d * 4) +
+                         align256((size_t)g.G * g.d * 4)
+                   : 0;
   s.counts = align256((size_t)g.n_sub * g.G * 4);
   s.base = s.counts;
   s.nb = align256((size_t)g.G * 4);
@@ -121,7 +130,7 @@ static Sizes compute_sizes(const Geom& g) {
   s.lbx = g.lbw == 0.f ? 0                         // balance gradient: dense router term
           : align256(g.dtype == SPT_BF16 ? (size_t)g.T * g.d * 2 : (size_t)g.T * g.G * 4);
   s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb +
-         s.lbp + s.lbx;
+         s.lbp + s.lbx + 2 * s.xs + s.ws_w;
   return s;
 }
 
@@ -145,12 +154,19 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
   b.dgate = (float*)w; w += s.dgate;
   b.dlg = s.dlg ? (void*)w : nullptr; w += s.dlg;
   b.dwr_part = s.dwr ? (float*)w : nullptr; w += s.dwr;
-  b.n_split = g.dtype == SPT_BF16 ? dwr_splits(g) : 0;
+  b.n_split = g.tc() ? dwr_splits(g) : 0;
   b.chunk_counts = (int32_t*)w; w += s.counts;
   b.chunk_base = (int32_t*)w; w += s.base;
   b.n_b = (int32_t*)w; w += s.nb;
   b.lb_part = (float*)w; w += s.lbp;
   b.lb_x = s.lbx ? (void*)w : nullptr; w += s.lbx;
+  if (g.split) {
+    b.xs = w; w += s.xs;
+    b.dys = w; w += s.xs;
+    b.w1s = w; w += align256((size_t)g.mp * g.D * g.d * 4);
+    b.w2s = w; w += align256((size_t)g.D * g.d * 4);
+    b.wrs = w; w += align256((size_t)g.G * g.d * 4);
+  }
   return b;
 }
 
@@ -362,8 +378,8 @@ spt_status spt_ffn_route(const spt_ffn_desc* desc, const void* x, const void* w_
   }
   cudaError_t e = cudaSuccess;
   if (!logits_in) {
-    e = g.dtype == SPT_BF16 ? tc_router(g, x, w_r, r->logits, s)
-                            : launch_router_simt(g, x, w_r, r->logits, s);
+    e = g.tc() ? tc_router(g, x, w_r, r->logits, s, &b)
+               : launch_router_simt(g, x, w_r, r->logits, s);
     if (e != cudaSuccess) return SPT_ERR_CUDA;
   }
   return to_status(launch_topk_bucket(g, rv, b, s));
@@ -395,8 +411,8 @@ spt_status spt_ffn_forward(const spt_ffn_desc* desc, const void* x, const void* 
   cudaStream_t s = (cudaStream_t)stream;
   Bufs b = carve(g, stash, ws);
   RouteView rv = view(r);
-  cudaError_t e = g.dtype == SPT_BF16 ? tc_forward(g, x, w1, w2, rv, y, b, s)
-                                      : simt_forward(g, x, w1, w2, rv, y, b, s);
+  cudaError_t e = g.tc() ? tc_forward(g, x, w1, w2, rv, y, b, s)
+                         : simt_forward(g, x, w1, w2, rv, y, b, s);
   return to_status(e);
 }
 
@@ -431,7 +447,7 @@ spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void*
   Bufs b = carve(g, const_cast<void*>(stash), ws);
   RouteView rv = view(r);
   cudaEvent_t ev = (cudaEvent_t)dw_event;
-  cudaError_t e = g.dtype == SPT_BF16
+  cudaError_t e = g.tc()
                       ? tc_backward(g, x, w1, w2, w_r, rv, dy, dx, dw1, dw2, dw_r, dgate, acc, b, ev, s)
                       : simt_backward(g, x, w1, w2, w_r, rv, dy, dx, dw1, dw2, dw_r, dgate, acc, b,
                                       ev, s);

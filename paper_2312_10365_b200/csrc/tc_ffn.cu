@@ -48,6 +48,12 @@ struct TcArgs {
   CUtensorMap ta;  // A operand
   CUtensorMap tb;  // B operand
   CUtensorMap tc;  // FWD2/DX: partials [rows, d] bf16, box 64 cols x 32 rows (TMA store)
+  // fp32 path on the bf16 tensor cores (Geom::split, reading c13'): every fp32
+  // operand is carried as two bf16 tensors, x = hi + lo + O(2^-17 |x|), and each
+  // GEMM runs its K loop three times -- hi*hi, hi*lo, lo*hi -- into the same
+  // fp32 TMEM accumulator (the dropped lo*lo term is <= 2^-18 of each product).
+  CUtensorMap ta2;  // lo half of the A operand (geometry of ta)
+  CUtensorMap tb2;  // lo half of the B operand (geometry of tb)
   RouteView r;
   int64_t T;
   int G, d, D, bw, mp, act, gate, gpad;
@@ -78,6 +84,11 @@ struct TcArgs {
   int nu;                       // FWD1 / DA: unit tiles; DW1 / DW2: feature tiles
   int kstream;                  // FWD2 / DX: K-streaming tiles (K > 256)
   float* dgp;                   // DA, nu > 1: per-unit-tile dgate partials [rows_cap][nu]
+  int split;                    // 1: fp32 path, three K passes (see ta2 / tb2 above)
+  const void* aux2_lo;          // split: lo half of the gathered rows (aux2)
+  const void* aux_lo;           // split, DA: lo half of the Z stash (aux)
+  void* out_lo;                 // split, FWD1: lo half of the Z stash (out)
+  void* out2_lo;                // split: FWD1 lo half of H~ (out2); DA lo half of dZ (out2)
   int ablate;                   // SPT_FFN_ABLATE (timing experiments only; results wrong):
                                 //  1 = skip gathered-row copies, 2 = skip FWD1 epilogue stores,
                                 //  3 = no operand loads at all, 4 = 3 + no epilogue work,
@@ -136,11 +147,20 @@ struct TileInfo {
   int n_valid;      // valid rows of the M tile (bucket-row kinds) / bucket size n_b (DW*)
   int64_t prow0;    // first padded bucket row of the M tile (bucket-row kinds)
   int64_t pos0;     // bucket position of row 0 (bucket-row kinds) / of block start (DW*)
-  int nkb;          // K stages
+  int nkb;          // K stages (split: 3 passes of kb1 stages)
+  int kb1;          // K stages of one pass
   int64_t kbase;    // DW*: first padded row of the block; DWR: first token of the split
   int rows_pad;     // bucket-row kinds: padded rows of the block from prow0 on (write limit)
   int ut;           // FWD1 / DA: unit tile; DW1 / DW2: feature tile (wide blocks)
 };
+
+// split K loop: stage kb of pass p = kb / kb1 reads stage kk = kb % kb1 of
+// (A, B) = (hi, hi) for p = 0, (hi, lo) for p = 1, (lo, hi) for p = 2
+__device__ __forceinline__ int kpass(const TileInfo& ti, int kb, int& kk) {
+  const int p = kb >= ti.kb1 ? (kb >= 2 * ti.kb1 ? 2 : 1) : 0;
+  kk = kb - p * ti.kb1;
+  return p;
+}
 
 // TMEM columns: accumulator buffer `acc`, M half `h` (each half holds BN <= 256
 // columns at a stride of 128 or 256); two buffers alternate between tiles when
@@ -217,6 +237,15 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
     const int nk = t1 > ti.kbase ? (int)ceil_div(t1 - ti.kbase, 64) : 0;
     ti.nkb = 2 * nk;  // hi part then lo part
   }
+  ti.kb1 = ti.nkb;
+  if (a.split) {
+    if (KIND == K_DWR) {  // parts: dlogit hi x X hi, dlogit lo x X hi, dlogit hi x X lo
+      ti.kb1 = ti.nkb / 2;
+      ti.nkb = 3 * ti.kb1;
+    } else {
+      ti.nkb *= 3;
+    }
+  }
   return ti;
 }
 
@@ -264,40 +293,45 @@ __device__ __forceinline__ uint32_t tile_tx_bytes(const TcArgs& a) {
 template <int KIND>
 __device__ __forceinline__ void produce_tiles(const TcArgs& a, const TileInfo& ti, int kb,
                                               uint8_t* sA, uint8_t* sB, uint64_t* bar) {
+  int kk = kb;
+  const int p = kpass(ti, kb, kk);
+  const CUtensorMap* ma = p == 2 ? &a.ta2 : &a.ta;  // split passes (p = 0 without split)
+  const CUtensorMap* mb = p == 1 ? &a.tb2 : &a.tb;
   if (KIND == K_ROUTER) {
-    tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
-    tma_load_2d(sB, &a.tb, bar, kb * 64, 0);
+    tma_load_2d(sA, ma, bar, kk * 64, (int)ti.prow0);
+    tma_load_2d(sB, mb, bar, kk * 64, 0);
   } else if (KIND == K_DAT) {  // A = the block's W2 rows (units) x 64 columns
     tma_load_2d(sA, &a.tb, bar, kb * 64, ti.b * a.bw);
   } else if (KIND == K_FWD1 || KIND == K_DA) {  // B: the tile's bn_u units (+ up rows)
     const int u0 = ti.b * a.bw + ti.ut * a.bn_u;
-    tma_load_2d(sB, &a.tb, bar, kb * 64, u0);
-    if (KIND == K_FWD1 && a.mp == 2) tma_load_2d(sB + a.bn_u * 128, &a.tb, bar, kb * 64, a.D + u0);
+    tma_load_2d(sB, mb, bar, kk * 64, u0);
+    if (KIND == K_FWD1 && a.mp == 2) tma_load_2d(sB + a.bn_u * 128, mb, bar, kk * 64, a.D + u0);
   } else if (KIND == K_FWD2 || KIND == K_DX) {
-    tma_load_2d(sA, &a.ta, bar, kb * 64, (int)ti.prow0);
+    tma_load_2d(sA, ma, bar, kk * 64, (int)ti.prow0);
     int krow;
-    if (KIND == K_FWD2) krow = ti.b * a.bw + kb * 64;
-    else krow = kb * 64 < a.bw ? ti.b * a.bw + kb * 64 : a.D + ti.b * a.bw + (kb * 64 - a.bw);
+    if (KIND == K_FWD2) krow = ti.b * a.bw + kk * 64;
+    else krow = kk * 64 < a.bw ? ti.b * a.bw + kk * 64 : a.D + ti.b * a.bw + (kk * 64 - a.bw);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, krow);
+    for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, mb, bar, ti.nt * 256 + j * 64, krow);
   } else if (KIND == K_DXR) {  // A = dense dlogits (hi rows, then lo rows), B = w_r (MN-major)
-    const int nkh = ti.nkb / 2, kk = kb % nkh;
-    tma_load_2d(sA, &a.ta, bar, kk * 64, (int)((kb < nkh ? 0 : a.T) + ti.prow0));
+    const int nkh = ti.nkb / 2, kh = kb % nkh;
+    tma_load_2d(sA, &a.ta, bar, kh * 64, (int)((kb < nkh ? 0 : a.T) + ti.prow0));
 #pragma unroll
-    for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, kk * 64);
+    for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, kh * 64);
   } else if (KIND == K_DW1 || KIND == K_DW2) {
     constexpr int BK = kind_bk(KIND);  // MN-major A: 64-feature chunks x BK bucket rows
     for (int j = 0; j < 2 * a.MH; ++j)  // features [256 ut + 64 j, +64)
-      tma_load_2d(sA + j * (BK * 128), &a.ta, bar, ti.ut * 256 + j * 64, (int)(ti.kbase + kb * BK));
-  } else {  // DWR
-    const int nk = ti.nkb / 2;
-    const int part = kb >= nk;
-    const int kk = part ? kb - nk : kb;
-    const int trow = (int)(ti.kbase + kk * 64);
+      tma_load_2d(sA + j * (BK * 128), ma, bar, ti.ut * 256 + j * 64, (int)(ti.kbase + kk * BK));
+  } else {  // DWR: part 0 = (dlogit hi, X), 1 = (dlogit lo, X), split: 2 = (dlogit hi, X lo)
+    const int nk = a.split ? ti.kb1 : ti.nkb / 2;
+    const int part = kb / nk;
+    const int kd = kb - part * nk;
+    const int trow = (int)(ti.kbase + kd * 64);
+    const CUtensorMap* mx = part == 2 ? &a.tb2 : &a.tb;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) tma_load_2d(sA + j * 8192, &a.ta, bar, j * 64, (int)(part * a.T) + trow);
+    for (int j = 0; j < 2; ++j) tma_load_2d(sA + j * 8192, &a.ta, bar, j * 64, (int)((part & 1) * a.T) + trow);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, &a.tb, bar, ti.nt * 256 + j * 64, trow);
+    for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, mx, bar, ti.nt * 256 + j * 64, trow);
   }
 }
 
@@ -323,10 +357,19 @@ __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* dst, const uint32_
   }
 }
 
+// split: the lo halves of a packed bf16 pair, x - bf16(x) (exact in fp32), rounded to bf16
+__device__ __forceinline__ uint32_t pack_bf16_lo(float x0, float x1, uint32_t hi) {
+  return pack_bf16(x0 - __uint_as_float(hi << 16), x1 - __uint_as_float(hi & 0xffff0000u));
+}
+// value of the bf16 at half (i & 1) of word w, plus (split) its lo half from word wl
+__device__ __forceinline__ float bf16_at(uint32_t w, int i) {
+  return __uint_as_float((i & 1) ? (w & 0xffff0000u) : (w << 16));
+}
+
 // Row `row` of the tile is TMEM lane `row`; columns [c_lo, c_hi) of it belong
 // to this thread (the other warp of the same lane quarter owns the rest).
 // tacc: TMEM address of (this warp's lane quarter, column 0) of the accumulator.
-template <int KIND>
+template <int KIND, bool kSplit = false>
 __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, uint32_t tacc,
                                          int row, int half, float* dg_xchg) {
   const bool valid = row < ti.n_valid;
@@ -360,6 +403,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
       if (a.mp == 2) tmem_ld16(tacc + a.bn_u + u0, vu);
       tmem_ld_wait();
       uint32_t pz[8], pu[8], ph[8];
+      uint32_t lz[8], lu[8], lh[8];  // split: lo halves
 #pragma unroll
       for (int i = 0; i < 16; i += 2) {
         const float z0 = valid ? __uint_as_float(vg[i]) : 0.f;
@@ -369,11 +413,31 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
           u0f = valid ? __uint_as_float(vu[i]) : 0.f;
           u1f = valid ? __uint_as_float(vu[i + 1]) : 0.f;
           pu[i / 2] = pack_bf16(u0f, u1f);
+          if (kSplit) lu[i / 2] = pack_bf16_lo(u0f, u1f, pu[i / 2]);
         }
         pz[i / 2] = pack_bf16(z0, z1);
-        ph[i / 2] = pack_bf16(g * act_fwd<true>(a.act, z0, u0f), g * act_fwd<true>(a.act, z1, u1f));
+        const float h0 = g * act_fwd<true>(a.act, z0, u0f), h1 = g * act_fwd<true>(a.act, z1, u1f);
+        ph[i / 2] = pack_bf16(h0, h1);
+        if (kSplit) {
+          lz[i / 2] = pack_bf16_lo(z0, z1, pz[i / 2]);
+          lh[i / 2] = pack_bf16_lo(h0, h1, ph[i / 2]);
+        }
       }
       if (a.ablate == 2) continue;
+      if (kSplit) {  // lo halves: same row layout, separate tensors
+        uint4* zd = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out_lo + prow * (int64_t)(a.mp * a.bw) + ub + u0);
+        uint4* hd = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out2_lo + prow * (int64_t)a.bw + ub + u0);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          zd[q] = make_uint4(lz[4 * q], lz[4 * q + 1], lz[4 * q + 2], lz[4 * q + 3]);
+          hd[q] = make_uint4(lh[4 * q], lh[4 * q + 1], lh[4 * q + 2], lh[4 * q + 3]);
+        }
+        if (a.mp == 2) {
+          uint4* ud = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out_lo + prow * (int64_t)(a.mp * a.bw) + ub + a.bw + u0);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) ud[q] = make_uint4(lu[4 * q], lu[4 * q + 1], lu[4 * q + 2], lu[4 * q + 3]);
+        }
+      }
       uint4* zd = reinterpret_cast<uint4*>(zr + u0);
       uint4* hd = reinterpret_cast<uint4*>(hr + u0);
 #pragma unroll
@@ -390,13 +454,24 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
   } else if (KIND == K_FWD2 || KIND == K_DX || KIND == K_DXR) {
     const int64_t prow = ti.prow0 + row;
     __nv_bfloat16* dst = (__nv_bfloat16*)a.out + prow * (int64_t)a.d + ti.nt * 256;
+    float* dstf = (float*)a.out + prow * (int64_t)a.d + ti.nt * 256;  // split: fp32 rows
     const int ncols = min(256, a.d - ti.nt * 256);
     const int c_lo = half * 128, c_hi = min(ncols, c_lo + 128);
     for (int c0 = c_lo; c0 < c_hi; c0 += 64) {
       uint32_t v[64];
       const bool two = c0 + 32 < c_hi;
       tmem_ld64(tacc + c0, v, two);
-      if (valid) store_bf16_row(dst + c0, v, two ? 64 : 32);
+      if (!valid) continue;
+      if (kSplit) {
+        uint4* d4 = reinterpret_cast<uint4*>(dstf + c0);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          if (q >= (two ? 16 : 8)) break;
+          d4[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+      } else {
+        store_bf16_row(dst + c0, v, two ? 64 : 32);
+      }
     }
   } else if (KIND == K_DA) {
     const int64_t prow = ti.prow0 + row;
@@ -404,6 +479,9 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     const int ub = ti.ut * a.bn_u, nut = min(a.bn_u, a.bw - ub);  // this tile's units
     const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + prow * (int64_t)(a.mp * a.bw) + ub;
     __nv_bfloat16* dzr = (__nv_bfloat16*)a.out2 + prow * (int64_t)(a.mp * a.bw) + ub;
+    // split: lo halves of the Z stash / dZ rows (same layout)
+    const __nv_bfloat16* zrl = (const __nv_bfloat16*)a.aux_lo + prow * (int64_t)(a.mp * a.bw) + ub;
+    __nv_bfloat16* dzrl = (__nv_bfloat16*)a.out2_lo + prow * (int64_t)(a.mp * a.bw) + ub;
     const int hw = ((a.bn_u / 2) + 15) & ~15;
     const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? nut : min(nut, u_lo + hw);
     float dgate = 0.f;
@@ -411,34 +489,34 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
       uint32_t v[16];
       tmem_ld16(tacc + u0, v);
       tmem_ld_wait();
-      uint32_t zg4[8], zu4[8];
+      uint32_t zg4[8], zu4[8], zgl[8], zul[8];
       if (valid) {
-        const uint4* zs = reinterpret_cast<const uint4*>(zr + u0);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const uint4 w = zs[q];
-          zg4[4 * q] = w.x; zg4[4 * q + 1] = w.y; zg4[4 * q + 2] = w.z; zg4[4 * q + 3] = w.w;
-        }
-        if (a.mp == 2) {
-          const uint4* us = reinterpret_cast<const uint4*>(zr + a.bw + u0);
+        auto ld8 = [](const __nv_bfloat16* src, uint32_t (&w8)[8]) {
+          const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const uint4 w = us[q];
-            zu4[4 * q] = w.x; zu4[4 * q + 1] = w.y; zu4[4 * q + 2] = w.z; zu4[4 * q + 3] = w.w;
+            const uint4 w = s4[q];
+            w8[4 * q] = w.x; w8[4 * q + 1] = w.y; w8[4 * q + 2] = w.z; w8[4 * q + 3] = w.w;
           }
+        };
+        ld8(zr + u0, zg4);
+        if (a.mp == 2) ld8(zr + a.bw + u0, zu4);
+        if (kSplit) {
+          ld8(zrl + u0, zgl);
+          if (a.mp == 2) ld8(zrl + a.bw + u0, zul);
         }
       }
-      uint32_t pg[8], pu[8];
+      uint32_t pg[8], pu[8], lg[8], lu[8];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         float dA = 0.f, zg = 0.f, zu = 0.f;
         if (valid) {
           dA = __uint_as_float(v[i]);
-          const uint32_t wg = zg4[i / 2];
-          zg = __uint_as_float((i & 1) ? (wg & 0xffff0000u) : (wg << 16));
+          zg = bf16_at(zg4[i / 2], i);
+          if (kSplit) zg += bf16_at(zgl[i / 2], i);
           if (a.mp == 2) {
-            const uint32_t wu = zu4[i / 2];
-            zu = __uint_as_float((i & 1) ? (wu & 0xffff0000u) : (wu << 16));
+            zu = bf16_at(zu4[i / 2], i);
+            if (kSplit) zu += bf16_at(zul[i / 2], i);
           }
         }
         float av, dg, du;
@@ -449,6 +527,12 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         const uint32_t bu = __bfloat16_as_ushort(__float2bfloat16(dzu));
         if (i & 1) { pg[i / 2] |= bg << 16; pu[i / 2] |= bu << 16; }
         else { pg[i / 2] = bg; pu[i / 2] = bu; }
+        if (kSplit) {
+          const uint32_t cg = __bfloat16_as_ushort(__float2bfloat16(dzg - __uint_as_float(bg << 16)));
+          const uint32_t cu = __bfloat16_as_ushort(__float2bfloat16(dzu - __uint_as_float(bu << 16)));
+          if (i & 1) { lg[i / 2] |= cg << 16; lu[i / 2] |= cu << 16; }
+          else { lg[i / 2] = cg; lu[i / 2] = cu; }
+        }
       }
       uint4* d4 = reinterpret_cast<uint4*>(dzr + u0);
 #pragma unroll
@@ -457,6 +541,16 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         uint4* u4 = reinterpret_cast<uint4*>(dzr + a.bw + u0);
 #pragma unroll
         for (int q = 0; q < 2; ++q) u4[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
+      }
+      if (kSplit) {
+        uint4* l4 = reinterpret_cast<uint4*>(dzrl + u0);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) l4[q] = make_uint4(lg[4 * q], lg[4 * q + 1], lg[4 * q + 2], lg[4 * q + 3]);
+        if (a.mp == 2) {
+          uint4* m4 = reinterpret_cast<uint4*>(dzrl + a.bw + u0);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) m4[q] = make_uint4(lu[4 * q], lu[4 * q + 1], lu[4 * q + 2], lu[4 * q + 3]);
+        }
       }
     }
     // column-split epilogue: combine the two halves' partial dgate (half 1 ->
@@ -639,7 +733,7 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, unsigned l
 constexpr int kTraceSlots = 8;
 
 // ------------------------------------------------------------------ kernel
-template <int KIND>
+template <int KIND, bool kSplit = false>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcArgs a,
                                                                int n_stages) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -829,8 +923,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         if (p == 0 && lane == 0 && a.ablate < 3)
           produce_tiles<KIND>(a, ti, kb, sA, sA + astride, &full[stage]);
         if (has_call && a.ablate != 1 && a.ablate < 3) {
-          tma_gather4((kind_rows_on_b(KIND) ? sA + astride : sA) + c * 512, &a.ta, &full[stage],
-                      kb * 64, rr[0], rr[1], rr[2], rr[3]);
+          int kk = kb;
+          const int ps = kpass(ti, kb, kk);
+          tma_gather4((kind_rows_on_b(KIND) ? sA + astride : sA) + c * 512, ps == 2 ? &a.ta2 : &a.ta,
+                      &full[stage], kk * 64, rr[0], rr[1], rr[2], rr[3]);
           // warm L2 with the next 256 columns of these rows in one 512-byte run per
           // row (DRAM-friendly), 4..7 stages ahead of their gathers
           if (a.prefetch && !kind_rows_on_b(KIND) && (kb & 3) == 0 && kb + 4 < ti.nkb)
@@ -877,12 +973,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
         __syncwarp();
         const uint32_t sA = smem_u32(smem + stage * sstride + (kind_rows_on_b(KIND) ? astride : 0));
+        int kk = kb;
+        const __nv_bfloat16* srcp = kpass(ti, kb, kk) == 2 ? (const __nv_bfloat16*)a.aux2_lo : src;
 #pragma unroll
         for (int i = 0; i < kRowsPer; ++i) {
           if (a.ablate == 1 || a.ablate >= 3) break;
           const int r = kTmaRows + (t >> 3) + 16 * i;
           const uint32_t dst = sA + (r >> 7) * 16384 + (r & 127) * 128 + ((ch ^ (r & 7)) << 4);
-          const __nv_bfloat16* g = src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kb * 64 + ch * 8;
+          const __nv_bfloat16* g = srcp + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kk * 64 + ch * 8;
           cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
         }
         cp_async_arrive_noinc(&full[stage]);
@@ -905,10 +1003,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       const TileInfo ti = decode<KIND>(a, tile);
       int tok[kRowsG];
       auto load_idx = [&](int kb) {
+        int kk = kb;
+        kpass(ti, kb, kk);
 #pragma unroll
         for (int i = 0; i < kRowsG; ++i) {
           const int r = (gt >> 5) + 6 * i;
-          const int e = kb * BK + r;
+          const int e = kk * BK + r;
           tok[i] = (r < BK && e < ti.n_valid) ? a.r.bucket_token[ti.pos0 + e] : -1;
         }
       };
@@ -926,13 +1026,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
         __syncwarp();
         const uint32_t sB = smem_u32(smem + stage * sstride + astride);
+        int kk = kb;
+        const __nv_bfloat16* srcp = kpass(ti, kb, kk) == 1 ? (const __nv_bfloat16*)a.aux2_lo : src;
 #pragma unroll
         for (int i = 0; i < kRowsG; ++i) {
           const int r = (gt >> 5) + 6 * i;
           if (r < BK) {
             const uint32_t dst = sB + j * (BK * 128) + r * 128 + ((pc ^ (r & 7)) << 4);
             const __nv_bfloat16* g =
-                src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + ti.nt * 256 + j * 64 + pc * 8;
+                srcp + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + ti.nt * 256 + j * 64 + pc * 8;
             cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
           }
         }
@@ -1016,13 +1118,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         th.prow0 += half * 128;
         th.pos0 += half * 128;
         if (half * 128 < ti.rows_pad)  // the second m-tile may not exist: write nothing
-          epilogue<KIND>(a, th, tmem + lanes + tm_col(a.BN, a.MH, acc, half), row, -1, dg_xchg);
+          epilogue<KIND, kSplit>(a, th, tmem + lanes + tm_col(a.BN, a.MH, acc, half), row, -1, dg_xchg);
       } else if (KIND == K_DAT) {
         epilogue_dat(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, 0), q, lane, half,
                      stg_base + e * 4096);
       } else {
         const uint32_t col0 = tm_col(a.BN, a.MH, acc, a.MH == 2 ? half : 0);
-        epilogue<KIND>(a, ti, tmem + lanes + col0, row, half, dg_xchg);
+        epilogue<KIND, kSplit>(a, ti, tmem + lanes + col0, row, half, dg_xchg);
       }
       tc_fence_before();
       __syncwarp();
@@ -1552,15 +1654,18 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
   int stages = std::min(kind_bres(KIND) || kind_bk(KIND) < 64 ? 8 : 6,
                         (227 * 1024 - extra - slab - stg) / sst);
   const int smem = slab + stages * sst + extra + stg;
-  static std::atomic<bool> attr_set[kMaxDev];
-  if (cudaError_t e = set_smem_attr_once(tc_gemm_kernel<KIND>, attr_set)) return e;
+  // split (fp32 on tensor cores): its own instantiation, so the hi / lo epilogue
+  // code costs the bf16 kernels no registers
+  static std::atomic<bool> attr_set[2][kMaxDev];
+  auto* kern = a.split ? tc_gemm_kernel<KIND, true> : tc_gemm_kernel<KIND, false>;
+  if (cudaError_t e = set_smem_attr_once(kern, attr_set[a.split ? 1 : 0])) return e;
   const int grid = std::max(1, std::min(tiles_upper, gemm_sms()));
   static const char* kNames[] = {"tc_router", "tc_fwd1_gate_up", "tc_fwd2_down", "tc_bwd_dA",
                                  "tc_bwd_dX", "tc_bwd_dW1", "tc_bwd_dW2", "tc_bwd_dWR",
                                  "tc_bwd_dAT", "tc_bwd_dXR"};
   const bool trace_on = trace_begin(a, s);
   prof_begin(kNames[KIND], s);
-  tc_gemm_kernel<KIND><<<grid, kThreads, smem, s>>>(a, stages);
+  kern<<<grid, kThreads, smem, s>>>(a, stages);
   prof_end(s);
   if (trace_on) trace_report(a, kNames[KIND], grid, s);
   count_launch();
@@ -1688,6 +1793,7 @@ static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
   a.nu = 1;
   a.bn_u = g.bw;
   a.kstream = 0;
+  a.split = g.split ? 1 : 0;
   a.unit_mt = unit_mtiles();
   static int pf = -1;  // SPT_FFN_PREFETCH=1 enables the L2 prefetch of gathered rows
   if (pf < 0) {
@@ -1750,12 +1856,63 @@ bool tc_supported(const Geom& g) {
     if (e_ != cudaSuccess) return e_;                                             \
   } while (0)
 
+// fp32 -> bf16 hi | lo (reading c13': hi = RNE(x), lo = RNE(x - hi), x - hi exact)
+__global__ void __launch_bounds__(256) split_bf16_kernel(const float* __restrict__ src,
+                                                         __nv_bfloat16* __restrict__ hi,
+                                                         __nv_bfloat16* __restrict__ lo, int64_t n) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(src) + i);
+    const uint32_t h0 = pack_bf16(v.x, v.y), h1 = pack_bf16(v.z, v.w);
+    reinterpret_cast<uint2*>(hi)[i] = make_uint2(h0, h1);
+    reinterpret_cast<uint2*>(lo)[i] = make_uint2(pack_bf16_lo(v.x, v.y, h0), pack_bf16_lo(v.z, v.w, h1));
+  }
+  for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const __nv_bfloat16 h = __float2bfloat16(src[i]);
+    hi[i] = h;
+    lo[i] = __float2bfloat16(src[i] - __bfloat162float(h));
+  }
+}
+
+cudaError_t launch_split_bf16(const float* src, void* dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>(ceil_div(n / 4 + 1, 256), (int64_t)num_sms() * 8);
+  prof_begin("split_bf16", s);
+  split_bf16_kernel<<<grid, 256, 0, s>>>(src, (__nv_bfloat16*)dst,
+                                         (__nv_bfloat16*)lo_half(dst, n), n);
+  prof_end(s);
+  count_launch();
+  return cudaGetLastError();
+}
+
+bool simt_forced() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_SIMT");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 cudaError_t tc_router(const Geom& g, const void* x, const void* w_r, float* logits,
-                      cudaStream_t s) {
+                      cudaStream_t s, const Bufs* b) {
   TcArgs a{};
   base_args(a, g, RouteView{});
-  bool ok = make_tmap_bf16_2d(&a.ta, x, g.T, g.d, g.d, 64, 128) &&
-            make_tmap_bf16_2d(&a.tb, w_r, g.G, g.d, g.d, 64, g.gpad);
+  bool ok = true;
+  if (g.split) {  // fp32 operands -> hi | lo copies in the workspace
+    if (!b) return cudaErrorInvalidValue;
+    cudaError_t e = launch_split_bf16((const float*)x, b->xs, g.T * g.d, s);
+    if (e == cudaSuccess) e = launch_split_bf16((const float*)w_r, b->wrs, (int64_t)g.G * g.d, s);
+    if (e != cudaSuccess) return e;
+    x = b->xs;
+    w_r = b->wrs;
+    ok = make_tmap_bf16_2d(&a.ta2, lo_half(x, g.T * g.d), g.T, g.d, g.d, 64, 128) &&
+         make_tmap_bf16_2d(&a.tb2, lo_half(w_r, (int64_t)g.G * g.d), g.G, g.d, g.d, 64, g.gpad);
+  }
+  ok = ok && make_tmap_bf16_2d(&a.ta, x, g.T, g.d, g.d, 64, 128) &&
+       make_tmap_bf16_2d(&a.tb, w_r, g.G, g.d, g.d, 64, g.gpad);
   a.BN = g.gpad;
   a.out = logits;
   TRY(launch<K_ROUTER>(a, (int)ceil_div(g.T, 128), s));
@@ -1839,6 +1996,16 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
   const int up = bucket_tiles_upper(g);
   cudaError_t e0 = build_schedules(g, r, b, s);
   if (e0 != cudaSuccess) return e0;
+  const int64_t nz = g.rows_cap * g.mp * g.bw, nh = g.rows_cap * g.bw;  // split: lo offsets
+  if (g.split) {  // fp32 operands -> bf16 hi | lo copies (reading c13')
+    if ((e0 = launch_split_bf16((const float*)x, b.xs, g.T * g.d, s)) != cudaSuccess ||
+        (e0 = launch_split_bf16((const float*)w1, b.w1s, (int64_t)g.mp * g.D * g.d, s)) != cudaSuccess ||
+        (e0 = launch_split_bf16((const float*)w2, b.w2s, (int64_t)g.D * g.d, s)) != cudaSuccess)
+      return e0;
+    x = b.xs;
+    w1 = b.w1s;
+    w2 = b.w2s;
+  }
   {
     // LoRA: FWD1 runs on X_aug / W1_aug (K = d + 64: the u C_I term is one more K stage)
     Geom g1 = g;
@@ -1865,8 +2032,16 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
     a.out = b.z;
     a.out2 = b.h;
     a.unit_offsets = b.unit_offsets;
+    if (g.split) {
+      ok = ok && make_tmap_bf16_2d(&a.ta2, lo_half(x, g.T * g.d), g.T, g.d, g.d, 64, 1) &&
+           make_tmap_bf16_2d(&a.tb2, lo_half(w1, (int64_t)g.mp * g.D * g.d), (uint64_t)g.mp * g.D,
+                             g.d, g.d, 64, a.bn_u);
+      a.aux2_lo = lo_half(x, g.T * g.d);
+      a.out_lo = lo_half(b.z, nz);
+      a.out2_lo = lo_half(b.h, nh);
+    }
     const int tiles = (up / 2 + g.G) * a.nu;
-    if (use_pair_gather() && pair_gather_ok(a.BN)) {
+    if (use_pair_gather() && pair_gather_ok(a.BN) && !g.split) {
       // CTA r holds B rows of its N half: the gate (r = 0) / up (r = 1) rows
       // for SwiGLU (a box of bn_u rows), else rows [r BN/2, (r+1) BN/2) of the tile
       if (g.mp != 2) ok = ok && make_tmap_bf16_2d(&a.tb, w1, g.D, g.d, g.d, 64, a.BN / 2);
@@ -1881,10 +2056,13 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
     bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, 128) &&
               make_tmap_bf16_2d(&a.tb, w2, g.D, g.d, g.d, 64, 64);
     ok = ok && make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
+    if (g.split)  // fp32 partial rows (generic epilogue), K streamed in three passes
+      ok = ok && make_tmap_bf16_2d(&a.ta2, lo_half(b.h, nh), g.rows_cap, g.bw, g.bw, 64, 128) &&
+           make_tmap_bf16_2d(&a.tb2, lo_half(w2, (int64_t)g.D * g.d), g.D, g.d, g.d, 64, 64);
     a.BN = 256;
     a.out = b.part;
     a.unit_offsets = b.unit_offsets;
-    a.kstream = g.bw > 256;  // the K = bw slab no longer fits smem: stream K
+    a.kstream = g.bw > 256 || g.split;  // the K = bw slab no longer fits smem: stream K
     if (a.kstream) {
       TRY(launch<K_FWD2>(a, up * a.NT, s));
     } else {
@@ -2046,11 +2224,13 @@ int dense_tn_splits(const Geom& g) {
 }
 
 cudaError_t tc_dense_tn(const Geom& g, const void* ahl, const void* bmat, float* part, int n_split,
-                        float* out, bool accumulate, cudaStream_t s) {
+                        float* out, bool accumulate, cudaStream_t s, const void* bmat_lo) {
   TcArgs a{};
   base_args(a, g, RouteView{});
+  a.split = bmat_lo ? 1 : 0;  // third part: dlogit hi x B lo
   bool ok = make_tmap_bf16_2d(&a.ta, ahl, (uint64_t)2 * g.T, g.gpad, g.gpad, 64, 64) &&
-            make_tmap_bf16_2d(&a.tb, bmat, g.T, g.d, g.d, 64, 64);
+            make_tmap_bf16_2d(&a.tb, bmat, g.T, g.d, g.d, 64, 64) &&
+            (!bmat_lo || make_tmap_bf16_2d(&a.tb2, bmat_lo, g.T, g.d, g.d, 64, 64));
   a.BN = 256;
   a.n_split = n_split;
   a.ksplit = (int)(ceil_div(ceil_div(g.T, n_split), 64) * 64);
@@ -2088,6 +2268,18 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   cudaError_t e0 = cudaSuccess;
   if ((sig || lb) && cudaMemsetAsync(b.dlg, 0, (size_t)2 * g.T * g.gpad * 2, s) != cudaSuccess)
     return cudaErrorUnknown;
+  const int64_t nz = g.rows_cap * g.mp * g.bw, nh = g.rows_cap * g.bw, ntd = g.T * g.d;
+  if (g.split) {  // fp32 operands -> bf16 hi | lo copies (reading c13'); w_r stays fp32 (combine)
+    if ((e0 = launch_split_bf16((const float*)dy, b.dys, ntd, s)) != cudaSuccess ||
+        (e0 = launch_split_bf16((const float*)x, b.xs, ntd, s)) != cudaSuccess ||
+        (e0 = launch_split_bf16((const float*)w1, b.w1s, (int64_t)g.mp * g.D * g.d, s)) != cudaSuccess ||
+        (e0 = launch_split_bf16((const float*)w2, b.w2s, (int64_t)g.D * g.d, s)) != cudaSuccess)
+      return e0;
+    dy = b.dys;
+    x = b.xs;
+    w1 = b.w1s;
+    w2 = b.w2s;
+  }
   // LoRA: dA runs on dY_aug / W2_aug (K = d + 64: the (dy C_O^T) B_O^T term)
   Geom gda = g;
   const void* dy_da = dy;
@@ -2098,7 +2290,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     dy_da = lo->xaug;
     w2_da = lo->waug;
   }
-  if (!use_fused_da() && g.bw <= 128) {  // a7: dA^T = W2_b dY[bucket]^T (tokens on N), then dgate/dZ
+  if (!use_fused_da() && g.bw <= 128 && !g.split) {  // a7: dA^T = W2_b dY[bucket]^T (tokens on N), then dgate/dZ
     TcArgs a{};
     base_args(a, gda, r);
     bool ok = make_tmap_bf16_2d(&a.ta, dy_da, g.T, gda.d, gda.d, 64, 1) &&
@@ -2138,8 +2330,15 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.MH = 2;
     a.aux2 = dy_da;
     a.unit_offsets = b.unit_offsets;
+    if (g.split) {
+      ok = ok && make_tmap_bf16_2d(&a.ta2, lo_half(dy, ntd), g.T, g.d, g.d, 64, 1) &&
+           make_tmap_bf16_2d(&a.tb2, lo_half(w2, (int64_t)g.D * g.d), g.D, g.d, g.d, 64, a.bn_u);
+      a.aux2_lo = lo_half(dy, ntd);
+      a.aux_lo = lo_half(b.z, nz);
+      a.out2_lo = lo_half(b.dz, nz);
+    }
     const int tiles = (up / 2 + g.G) * a.nu;
-    if (use_pair_gather() && pair_gather_ok(a.BN)) {
+    if (use_pair_gather() && pair_gather_ok(a.BN) && !g.split) {
       ok = ok && make_tmap_bf16_2d(&a.tb, w2_da, g.D, gda.d, gda.d, 64, a.BN / 2);
       TRY(launch_pair_gather<K_DA>(a, tiles, s));
     } else {
@@ -2166,6 +2365,11 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
                                   (uint64_t)g.mp * g.bw, 64, kind_bk(K_DW1)) &&
                 make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 1);
+      if (g.split) {
+        ok = ok && make_tmap_bf16_2d(&a.ta2, lo_half(b.dz, nz), g.rows_cap, (uint64_t)g.mp * g.bw,
+                                     (uint64_t)g.mp * g.bw, 64, kind_bk(K_DW1));
+        a.aux2_lo = lo_half(x, ntd);
+      }
       a.BN = 256;
       a.MH = (int)std::min<int64_t>(2, ceil_div(g.mp * g.bw, 128));
       a.nu = (int)ceil_div(g.mp * g.bw, 256);
@@ -2179,6 +2383,11 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       base_args(a, g, r);
       bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, kind_bk(K_DW2)) &&
                 make_tmap_bf16_2d(&a.tb, dy, g.T, g.d, g.d, 64, 1);
+      if (g.split) {
+        ok = ok && make_tmap_bf16_2d(&a.ta2, lo_half(b.h, nh), g.rows_cap, g.bw, g.bw, 64,
+                                     kind_bk(K_DW2));
+        a.aux2_lo = lo_half(dy, ntd);
+      }
       a.BN = 256;
       a.MH = (int)std::min<int64_t>(2, ceil_div(g.bw, 128));
       a.nu = (int)ceil_div(g.bw, 256);
@@ -2196,7 +2405,9 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       if (e != cudaSuccess) return e;
     }
     // a10: dW_R = dLogits^T X  (split-K, hi + lo bf16 halves of dlogit)
-    if (sig || lb) return tc_dense_tn(g, b.dlg, x, b.dwr_part, b.n_split, dw_r, accumulate, s);
+    if (sig || lb)
+      return tc_dense_tn(g, b.dlg, x, b.dwr_part, b.n_split, dw_r, accumulate, s,
+                         g.split ? lo_half(x, ntd) : nullptr);
     if (!accumulate && cudaMemsetAsync(dw_r, 0, (size_t)g.G * g.d * 4, s) != cudaSuccess)
       return cudaErrorUnknown;
     return cudaSuccess;
@@ -2208,10 +2419,15 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
                                 (uint64_t)g.mp * g.bw, 64, 128) &&
               make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, 64);
     ok = ok && make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
+    if (g.split)  // fp32 partial rows (generic epilogue), K streamed in three passes
+      ok = ok && make_tmap_bf16_2d(&a.ta2, lo_half(b.dz, nz), g.rows_cap, (uint64_t)g.mp * g.bw,
+                                   (uint64_t)g.mp * g.bw, 64, 128) &&
+           make_tmap_bf16_2d(&a.tb2, lo_half(w1, (int64_t)g.mp * g.D * g.d), (uint64_t)g.mp * g.D,
+                             g.d, g.d, 64, 64);
     a.BN = 256;
     a.out = b.part;
     a.unit_offsets = b.unit_offsets;
-    a.kstream = g.mp * g.bw > 256;  // the K = m' bw slab no longer fits smem: stream K
+    a.kstream = g.mp * g.bw > 256 || g.split;  // the K = m' bw slab no longer fits smem: stream K
     if (a.kstream) {
       TRY(launch<K_DX>(a, up * a.NT, s));
     } else {

@@ -99,6 +99,17 @@ PAPER_CONFIGS = {
                                 cfg_index=21),
     "llama4096_g4_b34": FfnConfig("llama4096_g4_b34", 4096, 11008, 4, 3, 16 * 512, "bf16", ACT_GELU,
                                   cfg_index=22),
+    # Table 5's own precision: fp32 ("single-precision") at beta = 1/2
+    # and 3/4, G = 8 -- the configurations the paper quotes 54.9 / 84.6 ms (OPT-2048)
+    # and 150.8 / 228.9 ms (LLaMA-4096) for
+    "opt2048_g8_f32": FfnConfig("opt2048_g8_f32", 2048, 8192, 8, 4, 16 * 512, "f32", ACT_RELU,
+                                cfg_index=23),
+    "llama4096_g8_f32": FfnConfig("llama4096_g8_f32", 4096, 11008, 8, 4, 16 * 512, "f32", ACT_GELU,
+                                  cfg_index=24),
+    "opt2048_g8_b34_f32": FfnConfig("opt2048_g8_b34_f32", 2048, 8192, 8, 6, 16 * 512, "f32",
+                                    ACT_RELU, cfg_index=25),
+    "llama4096_g8_b34_f32": FfnConfig("llama4096_g8_b34_f32", 4096, 11008, 8, 6, 16 * 512, "f32",
+                                      ACT_GELU, cfg_index=26),
 }
 ALL_CONFIGS = {**CONFIGS, **PAPER_CONFIGS}
 

@@ -122,3 +122,70 @@ def oracle_run(orc, cfg: S.FfnConfig, inputs: dict, logits, topk_idx, tokens=Non
                                 topk_idx, inputs["dy"], cfg.act, cfg.gate, tokens=tokens, blocks=blocks,
                                 lb_weight=lb_weight))
     return out
+
+
+def relu_kink_fixup(cfg, inp, logits, topk_idx, got, ref, tokens=None, blocks=None, tau=1e-3):
+    """ReLU's derivative is a decision taken in floating point: relu'(z) = [z > 0].
+    Where |z| < tau (z from the inputs in fp64 here, independent of both sides)
+    the GPU's fp32 z and the oracle's fp64 z may fall on different sides of the
+    kink, and both derivatives are valid within rounding (DESIGN reading c24).
+    For every such (token, block, unit) the flip changes dx[t] by
+    g dA[t,u] w1[u] and dw1[u] by g dA[t,u] x[t]; per dx row / dw1 row this
+    adds to ref the flips the GPU took (least squares of the residual on the
+    row's flip terms, nearly orthogonal vectors: coefficient ~1 for a taken flip,
+    ~0 otherwise), so the standard bound then checks everything else.  tau covers
+    the split fp32 path's z error (~1e-4 absolute at d = 4096).
+    Returns the number of ambiguous elements.  ReLU only; y and dgate are
+    continuous at the kink and are not touched."""
+    if cfg.act != S.ACT_RELU:
+        return 0
+    x = inp["x"].astype(np.float64)
+    w1 = inp["w1"].astype(np.float64)
+    w2 = inp["w2"].astype(np.float64)
+    dy = inp["dy"].astype(np.float64)
+    lg = np.asarray(logits, np.float64)
+    T, k, bw = topk_idx.shape[0], topk_idx.shape[1], cfg.bw
+    amb = []  # (t, unit, delta sign, g dA)
+    tok_set = None if tokens is None else set(int(t) for t in tokens)
+    blk_set = None if blocks is None else set(int(b) for b in blocks)
+    for t in range(T):
+        for j in range(k):
+            b = int(topk_idx[t, j])
+            if tok_set is not None and t not in tok_set and (blk_set is None or b not in blk_set):
+                continue  # a pair no compared quantity depends on
+            rows = slice(b * bw, (b + 1) * bw)
+            z = w1[rows] @ x[t]
+            near = np.nonzero(np.abs(z) < tau)[0]
+            if not len(near):
+                continue
+            g = 1.0 / (1.0 + np.exp(-lg[t, b])) if cfg.gate == S.GATE_SIGMOID else 1.0
+            da = w2[b * bw + near] @ dy[t]
+            for u, a, zz in zip(near, da, z[near]):
+                # the oracle used [z > 0]; the alternative removes / adds the term
+                amb.append((t, b * bw + int(u), -1.0 if zz > 0 else 1.0, g * a))
+    if not amb:
+        return 0
+
+    def best(gv, rv, terms):
+        # least squares of the residual on the row's flip terms (a few nearly
+        # orthogonal vectors): coefficient ~1 where the GPU took a flip, ~0 where not
+        r = gv - rv
+        V = np.stack([sgn * vec for sgn, vec in terms], axis=1)
+        c = np.linalg.lstsq(V, r, rcond=None)[0]
+        return rv + V @ (c > 0.5).astype(np.float64)
+
+    if "dx" in ref:
+        by_t = {}
+        for t, u, sgn, gda in amb:
+            if tok_set is None or t in tok_set:
+                by_t.setdefault(t, []).append((sgn, gda * w1[u]))
+        for t, terms in by_t.items():
+            ref["dx"][t] = best(np.asarray(got["dx"][t], np.float64), ref["dx"][t], terms)
+    if "dw1" in ref:
+        by_u = {}
+        for t, u, sgn, gda in amb:
+            if blk_set is None or u // bw in blk_set:
+                by_u.setdefault(u, []).append((sgn, gda * x[t]))
+        for u, terms in by_u.items():
+            ref["dw1"][u] = best(np.asarray(got["dw1"][u], np.float64), ref["dw1"][u], terms)
+    return len(amb)

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import synthetic as S
-from helpers import TOL, gpu_run, oracle_run, relerr
+from helpers import TOL, gpu_run, oracle_run, relerr, relu_kink_fixup
 
 pytestmark = pytest.mark.gpu
 
@@ -40,6 +40,8 @@ def _parity(orc, cfg, T, kind=None, names=NAMES):
     # the GPU's selection (checked bit-exact against the oracle's top-k in test_gpu_route)
     assert np.array_equal(got["topk_idx"], orc.topk(got["logits"], cfg.k))
     ref = oracle_run(orc, cfg, inp, lg, got["topk_idx"])
+    if cfg.dtype == "f32":  # fp32 bound: ReLU kink decisions taken in each side's precision
+        relu_kink_fixup(cfg, inp, lg, got["topk_idx"], got, ref)
     return _check(cfg, got, ref, names)
 
 
@@ -109,6 +111,22 @@ def test_paper_g4_g8_beta(orc, name):
     PAPER.md:1023-1026, 1043-1046; "G (e.g., 4 or 8)"), full shapes
     (bw 1024-2752) at a T the oracle's full backward covers in seconds."""
     _parity(orc, S.PAPER_CONFIGS[name], 300)
+
+
+@pytest.mark.parametrize("name", ["opt2048_g8_f32", "llama4096_g8_f32", "opt2048_g8_b34_f32",
+                                  "llama4096_g8_b34_f32"])
+def test_paper_fp32(orc, name):
+    """SURVEY §8(f) f1 at the paper's own precision (fp32; Table 5):
+    fp32 tensors on the bf16 tensor cores as hi + lo halves (three products per
+    GEMM, reading c13'), held to the fp32 bound 1e-4 at the full G = 8 shapes."""
+    _parity(orc, S.PAPER_CONFIGS[name], 300)
+
+
+@pytest.mark.parametrize("name,T", [("bert", 600), ("opt", 300), ("llama", 257)])
+def test_fp32_tensor_core_shapes(orc, name, T):
+    """The split fp32 path at the BASELINE block shapes (bw 96 / 128, GELU, ReLU,
+    SwiGLU; K streamed in three passes for FWD2 / dX) against the 1e-4 bound."""
+    _parity(orc, S.CONFIGS[name].with_(dtype="f32", name=f"{name}-f32"), T)
 
 
 def test_k1_bf16(orc):

@@ -25,7 +25,7 @@ import numpy as np
 import pytest
 
 import synthetic as S
-from helpers import TOL, elemerr, gpu_run, relerr, relerr_rows
+from helpers import TOL, elemerr, gpu_run, relerr, relerr_rows, relu_kink_fixup
 
 pytestmark = pytest.mark.gpu
 
@@ -38,13 +38,18 @@ CASES = [("tiny", 2), ("bert", 2), ("opt", 2), ("llama", 1), ("llama_scale", 1),
          # dx, dgate and the full-size Euler identities (their blocks hold 4-6k tokens
          # of 1024-2752 units: the oracle's per-block dW sum would take minutes)
          ("opt2048_g8_b34", 0), ("llama4096_g8_b34", 0), ("opt2048_g4", 0), ("llama4096_g4", 0),
-         ("opt2048_g4_b34", 0), ("llama4096_g4_b34", 0)]
+         ("opt2048_g4_b34", 0), ("llama4096_g4_b34", 0),
+         # the paper's fp32 Table 5 workloads on the split tensor-core path
+         ("opt2048_g8_f32", 1), ("llama4096_g8_f32", 0), ("opt2048_g8_b34_f32", 0),
+         ("llama4096_g8_b34_f32", 0)]
 
 
 def _router_parity(orc, cfg, got, x, w_r):
     """a1 at full T against the oracle; returns the oracle's fp64 logits."""
     lg = orc.router(x, w_r)
-    lim = 1e-5 if cfg.dtype == "f32" else 1e-4   # fp32 accumulation of exact bf16 / fp32 products
+    # bf16: fp32 accumulation of exact bf16 products; fp32 (split path): the
+    # north_star's fp32 bound (measured ~2e-5: tensor-core accumulation, reading c13')
+    lim = 1e-4
     assert relerr(got["logits"], lg) <= lim
     # every 128-token router tile on its own (a wrong tile cannot hide under the rest)
     T = lg.shape[0]
@@ -78,6 +83,8 @@ def _sampled_ffn_parity(orc, cfg, inp, got, lg, ti, tokens, blocks):
     bw_ = orc.backward(inp["x"], inp["w1"], inp["w2"], inp["w_r"], lg, ti, inp["dy"], cfg.act,
                        cfg.gate, tokens=tokens, blocks=blocks if len(blocks) else None,
                        want_blocks=len(blocks) > 0)
+    if cfg.dtype == "f32":  # fp32 bound: ReLU kink decisions taken in each side's precision
+        relu_kink_fixup(cfg, inp, lg, ti, got, bw_, tokens=tokens, blocks=blocks)
     assert relerr(got["dx"][tokens], bw_["dx"][tokens]) <= tol
     assert relerr(got["dgate"][tokens], bw_["dgate"][tokens]) <= tol
     elem = {"y": elemerr(got["y"][tokens], y[tokens]), "dx": elemerr(got["dx"][tokens], bw_["dx"][tokens])}
