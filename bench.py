@@ -190,9 +190,12 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    t0, _ = oracle_sample(cfg, 8, args.lora)
+    # calibrate the sample like cpu_baseline (a probe large enough that the oracle's
+    # per-call fixed costs do not dominate), then fit steps + warmup into ~150 s
     budget = 150.0 / max(1, args.steps + args.warmup)          # seconds per step
-    n = int(max(8, min(2048, 8 * budget / max(t0, 1e-3))))
+    n0 = 64
+    t0, _ = oracle_sample(cfg, n0, args.lora)
+    n = int(max(8, min(2048, n0 * budget / max(t0, 1e-3))))
     for _ in range(args.warmup):
         oracle_sample(cfg, n, args.lora)
     tot, cores = 0.0, 1

@@ -55,8 +55,8 @@ extern "C" {
 typedef enum {
   SPT_OK = 0,
   SPT_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, T < 0, k < 1, k > G, D % G != 0, dims <= 0 */
-  SPT_ERR_UNSUPPORTED = 2,      /* G > 256, d % 64, bw % 16, fp32 with bw % 4, non-sm_100 device;
-                                   bf16: G > 128, SwiGLU with bw % 64.  Any block width
+  SPT_ERR_UNSUPPORTED = 2,      /* G > 256, d % 64, bw % 16, non-sm_100 device; bf16: SwiGLU
+                                   with bw % 64 (fp32 then runs its SIMT kernels).  Any block width
                                    otherwise (m' bw > 256 -- the paper's G = 4 / 8 blocks,
                                    PAPER.md:436 -- runs unit / feature-tiled GEMMs) */
   SPT_ERR_WORKSPACE_TOO_SMALL = 3,

@@ -153,18 +153,22 @@ def backward(x, w1, w2, w_r, logits, topk_idx, dy, act, gate, tokens=None, block
     k = ti.shape[1]
     mp = 2 if act == ACT_SWIGLU else 1
     out = {}
+    # entries the oracle does not compute (a token / block subset) are NaN; a full
+    # call writes every entry, so it skips the (single-threaded) NaN fill
+    fill = np.full if tokens is not None else (lambda shape, v: np.empty(shape))
     if want_tokens:
-        dx = np.full((T, d), np.nan)
-        dg = np.full((T, k), np.nan)
+        dx = fill((T, d), np.nan)
+        dg = fill((T, k), np.nan)
         tk = None if tokens is None else np.ascontiguousarray(tokens, dtype=np.int64)
         lib().spt_oracle_backward_tokens(T, d, D, G, k, act, gate, _ptr(x), _ptr(w1), _ptr(w2),
                                          _ptr(w_r), _ptr(lg), _ptr(ti), _ptr(dy), _ptr(tk),
                                          0 if tk is None else len(tk), _ptr(dx), _ptr(dg))
         out["dx"], out["dgate"] = dx, dg
     if want_blocks:
-        dw1 = np.full((mp, D, d) if mp == 2 else (D, d), np.nan)
-        dw2 = np.full((D, d), np.nan)
-        dwr = np.full((G, d), np.nan)
+        fill = np.full if blocks is not None else (lambda shape, v: np.empty(shape))
+        dw1 = fill((mp, D, d) if mp == 2 else (D, d), np.nan)
+        dw2 = fill((D, d), np.nan)
+        dwr = fill((G, d), np.nan)
         bl = None if blocks is None else np.ascontiguousarray(blocks, dtype=np.int32)
         lib().spt_oracle_backward_blocks(T, d, D, G, k, act, gate, _ptr(x), _ptr(w1), _ptr(w2),
                                          _ptr(lg), _ptr(ti), _ptr(dy), _ptr(bl),

@@ -285,7 +285,8 @@ __device__ __forceinline__ uint32_t tile_tx_bytes(const TcArgs& a) {
   if (KIND == K_DAT) return 128 * 128;  // the W2 box is always 128 unit rows (rows >= bw unused)
   if (KIND == K_ROUTER) return kABytes + a.gpad * 128;
   if (KIND == K_DW1 || KIND == K_DW2) return 128 * kind_bk(KIND) * 2 * a.MH;
-  return kABytes + 32768;  // FWD2, DX, DWR
+  if (KIND == K_DWR) return kABytes * a.MH + 32768;
+  return kABytes + 32768;  // FWD2, DX
 }
 
 // ---------------------------------------------------------------- producer
@@ -328,8 +329,8 @@ __device__ __forceinline__ void produce_tiles(const TcArgs& a, const TileInfo& t
     const int kd = kb - part * nk;
     const int trow = (int)(ti.kbase + kd * 64);
     const CUtensorMap* mx = part == 2 ? &a.tb2 : &a.tb;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) tma_load_2d(sA + j * 8192, &a.ta, bar, j * 64, (int)((part & 1) * a.T) + trow);
+    for (int j = 0; j < 2 * a.MH; ++j)  // blocks [64 j, 64 j + 64); MH = 2 when G > 128
+      tma_load_2d(sA + j * 8192, &a.ta, bar, j * 64, (int)((part & 1) * a.T) + trow);
 #pragma unroll
     for (int j = 0; j < 4; ++j) tma_load_2d(sB + j * 8192, mx, bar, ti.nt * 256 + j * 64, trow);
   }
@@ -591,11 +592,12 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     bool live;
     int c_lo, c_hi;
     const int ncols = min(256, a.d - ti.nt * 256);
-    if (KIND == K_DWR) {  // split-K partial [split][G][d]
-      live = row < a.G;
-      orow = (int64_t)ti.b * a.G + row;
-      c_lo = half * 128;
-      c_hi = min(ncols, c_lo + 128);
+    if (KIND == K_DWR) {  // split-K partial [split][G][d]; MH == 2 (G > 128): half = block half
+      const int f = (a.MH == 2 ? half * 128 : 0) + row;
+      live = f < a.G;
+      orow = (int64_t)ti.b * a.G + f;
+      if (a.MH == 2) { c_lo = 0; c_hi = ncols; }
+      else { c_lo = half * 128; c_hi = min(ncols, c_lo + 128); }
     } else {
       // MH == 2: this warp's half owns accumulator `half` (features half*128 + row);
       // MH == 1: one accumulator, columns split between the halves
@@ -1840,7 +1842,7 @@ bool tc_supported(const Geom& g) {
   // m' bw > 256 (wide blocks): FWD1 / DA tile the units, DW* the features,
   // FWD2 / DX stream K (no limit on bw beyond the ABI's bw % 16 == 0)
   if (g.mp == 2 && g.bw % 64) return false;     // DX K stages must not straddle gate/up
-  if (g.gpad > 128) return false;               // DWR: one 128-row M tile of blocks
+  if (g.gpad > 256) return false;               // router N / DWR M (two 128-block halves) <= 256
   return true;
 }
 
@@ -2216,7 +2218,7 @@ __global__ void __launch_bounds__(256) dgate_reduce_kernel(int64_t T, int G, int
 
 int dense_tn_splits(const Geom& g) {
   // one wave: (N tiles) x (splits) <= #SMs (ceil gave 160 CTAs on 148 SMs at d = 4096)
-  const int tiles = (int)(ceil_div(g.G, 128) * ceil_div(g.d, 256));
+  const int tiles = (int)ceil_div(g.d, 256);  // one M tile of blocks (two halves when G > 128)
   int s = std::max(1, num_sms() / tiles);
   const int max_s = (int)ceil_div(g.T, 64);
   if (s > max_s) s = max_s;
@@ -2232,6 +2234,7 @@ cudaError_t tc_dense_tn(const Geom& g, const void* ahl, const void* bmat, float*
             make_tmap_bf16_2d(&a.tb, bmat, g.T, g.d, g.d, 64, 64) &&
             (!bmat_lo || make_tmap_bf16_2d(&a.tb2, bmat_lo, g.T, g.d, g.d, 64, 64));
   a.BN = 256;
+  a.MH = g.gpad > 128 ? 2 : 1;  // G in 129..256: two 128-block M halves
   a.n_split = n_split;
   a.ksplit = (int)(ceil_div(ceil_div(g.T, n_split), 64) * 64);
   a.out = part;

@@ -40,6 +40,17 @@ def _desc(**kw):
     return make_desc(**a)
 
 
+@pytest.mark.parametrize("G", [129, 200, 256])
+def test_bf16_wide_router_supported(G):
+    """Reading c25: G up to 256 on the bf16 path (router N = G padded to 16,
+    dW_R in two 128-block M halves); sizes grow with G."""
+    import torch
+    from paper_2312_10365_b200 import spt_ffn_sizes
+    s, w = spt_ffn_sizes(_desc(dtype=torch.bfloat16, d=256, G=G, D=G * 64, k=8))
+    s1, w1 = spt_ffn_sizes(_desc(dtype=torch.bfloat16, d=256, G=128, D=128 * 64, k=8))
+    assert s > s1 > 0 and w > w1 > 0
+
+
 def test_sizes_valid_and_monotone():
     from paper_2312_10365_b200 import spt_ffn_sizes
     s1, w1 = spt_ffn_sizes(_desc())

@@ -129,6 +129,13 @@ def test_fp32_tensor_core_shapes(orc, name, T):
     _parity(orc, S.CONFIGS[name].with_(dtype="f32", name=f"{name}-f32"), T)
 
 
+@pytest.mark.parametrize("G,k", [(129, 8), (256, 16)])
+def test_bf16_many_blocks(orc, G, k):
+    """Reading c25: G in 129..256 on the tcgen05 path (router N = 144 / 256, dW_R
+    as two 128-block M halves), bit-exact routing and the bf16 bound."""
+    _parity(orc, S.FfnConfig(f"G{G}", 256, G * 64, G, k, 900, "bf16", S.ACT_GELU), 900)
+
+
 def test_k1_bf16(orc):
     cfg = S.FfnConfig("k1", 256, 2048, 16, 1, 400, "bf16", S.ACT_GELU)
     _parity(orc, cfg, 400)
