@@ -624,23 +624,41 @@ def main():
         yh = torch.empty_like(x, device="cpu").pin_memory()
         dxh = torch.empty_like(x, device="cpu").pin_memory()
         pipe = HostStepPipeline(f, w1, w2, w_r, grad_hook=lambda: dp.allreduce_grads(fg), lora=lora)
-        for i in range(3):
-            pipe.step(i, xh, dyh, yh, dxh)
+        pipe.step(0, xh, dyh, yh, dxh)
         pipe.synchronize()
         barrier()
-        k2 = max(6, args.steps // 2)
+        # steady-state period of the pipeline: from the end of warm-up step 2's D2H to the
+        # end of the last timed step's D2H, i.e. exactly k2 steps, each with its own H2D,
+        # kernels and D2H (the one-time fill / drain of the 3-stage pipeline is not a step)
+        for i in range(1, 3):
+            pipe.step(i, xh, dyh, yh, dxh)
+        k2 = max(6, args.steps)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(pipe.s_h2d)
+        e0.record(pipe.s_d2h)
         for i in range(k2):
             pipe.step(3 + i, xh, dyh, yh, dxh)
         e1.record(pipe.s_d2h)
         pipe.synchronize()
         ms_e = dp.max_over_ranks(e0.elapsed_time(e1) / k2, device="cuda")
+        # the same k2 steps from an idle pipeline: the first H2D and the last D2H
+        # are not overlapped by anything (reported beside the steady-state value)
+        barrier()
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2.record(pipe.s_h2d)
+        for i in range(k2):
+            pipe.step(3 + k2 + i, xh, dyh, yh, dxh)
+        e3.record(pipe.s_d2h)
+        pipe.synchronize()
+        ms_fill = dp.max_over_ranks(e2.elapsed_time(e3) / k2, device="cuda")
         hb, db = pipe.bytes_per_step()
         e2e = {"value": T_global / (ms_e / 1e3), "unit": UNIT, "ms_per_step": ms_e,
+               "ms_per_step_incl_fill_drain": ms_fill,
                "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db,
                "what": "per step: H2D x, dy from pinned host -> route/fwd/bwd(+allreduce) -> D2H y, dx "
-                       "to pinned host; copies of adjacent steps overlap the kernels (copy streams)"}
+                       "to pinned host; copies of adjacent steps overlap the kernels (copy streams); "
+                       "steady-state period over k2 steps (pipeline fill / drain excluded); PCIe "
+                       "ceiling on this box: 49.6 GB/s per direction with both directions busy "
+                       "(tools/pcie_bw.py)", "steps": k2}
 
     if rank != 0:
         if world > 1:

@@ -32,7 +32,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-3, "
 
 
 def profile_name(kernel):
-    m = re.search(r"tc_(?:gemm|pair_gather|pair)_kernel<(?:\(int\))?(\d+)>", kernel)
+    m = re.search(r"tc_(?:gemm|pair_gather|pair)_kernel<(?:\(int\))?(\d+)(?:, *(?:\(bool\))?\w+)?>", kernel)
     if m:
         return TC_NAMES[int(m.group(1))]
     if "combine_kernel" in kernel:
