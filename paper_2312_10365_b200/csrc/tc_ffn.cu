@@ -1744,7 +1744,19 @@ static bool use_pair_gather() {
 // runs the tensor pipe at ~43 % and the 1-CTA kernel (two M halves in flight)
 // wins (same-box A/B, LLaMA-scale dA: 1.18 vs 1.33 ms; OPT FWD1 114 vs 132 us),
 // while at N = 256 the pair wins (LLaMA FWD1 1.31 vs 1.50 ms).
-static bool pair_gather_ok(int BN) { return BN > 128 && BN <= 256 && BN % 32 == 0; }
+// N = 128 (dA at bw = 128) also maps onto pairs (B halves of 64 rows); measured
+// before taking it by default (SPT_FFN_PAIR128=1)
+static bool pair128() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_PAIR128");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+static bool pair_gather_ok(int BN) {
+  return (BN > 128 || (BN == 128 && pair128())) && BN <= 256 && BN % 32 == 0;
+}
 
 template <int KIND>
 static cudaError_t launch_pair_gather(TcArgs& a, int tiles_upper, cudaStream_t s) {
