@@ -56,6 +56,8 @@ __global__ void __launch_bounds__(128) combine_kernel(int64_t T, int d, int k, R
                                                       const TIn* __restrict__ w_r,
                                                       const TIn* __restrict__ dense,
                                                       TIn* __restrict__ out) {
+  pdl_wait();  // PDL: predecessor grid complete, its writes visible
+  pdl_trigger();
   constexpr int V = Vec<TIn>::N;
   __shared__ int64_t rows[kMaxBlocks];
   __shared__ int blk[kMaxBlocks];
@@ -110,11 +112,11 @@ cudaError_t launch_combine_fwd(const Geom& g, const RouteView& r, const void* pa
                                cudaStream_t s) {
   prof_begin("combine_fwd", s);
   if (g.dtype == SPT_BF16)
-    combine_kernel<__nv_bfloat16, false><<<(unsigned)g.T, 128, 0, s>>>(
+    (void)launch_pdl(combine_kernel<__nv_bfloat16, false>, dim3((unsigned)g.T), dim3(128), 0, s, 
         g.T, g.d, g.k, r, (const __nv_bfloat16*)part, nullptr, nullptr, nullptr,
         (__nv_bfloat16*)y);
   else
-    combine_kernel<float, false><<<(unsigned)g.T, 128, 0, s>>>(g.T, g.d, g.k, r, (const float*)part,
+    (void)launch_pdl(combine_kernel<float, false>, dim3((unsigned)g.T), dim3(128), 0, s, g.T, g.d, g.k, r, (const float*)part,
                                                                nullptr, nullptr, nullptr, (float*)y);
   prof_end(s);
   count_launch();
@@ -127,11 +129,11 @@ cudaError_t launch_combine_bwd(const Geom& g, const RouteView& r, const void* pa
   const void* wr = g.gate == SPT_GATE_SIGMOID ? w_r : nullptr;
   prof_begin("combine_bwd", s);
   if (g.dtype == SPT_BF16)
-    combine_kernel<__nv_bfloat16, true><<<(unsigned)g.T, 128, 0, s>>>(
+    (void)launch_pdl(combine_kernel<__nv_bfloat16, true>, dim3((unsigned)g.T), dim3(128), 0, s, 
         g.T, g.d, g.k, r, (const __nv_bfloat16*)part, dlogit, (const __nv_bfloat16*)wr, nullptr,
         (__nv_bfloat16*)dx);
   else
-    combine_kernel<float, true><<<(unsigned)g.T, 128, 0, s>>>(
+    (void)launch_pdl(combine_kernel<float, true>, dim3((unsigned)g.T), dim3(128), 0, s, 
         g.T, g.d, g.k, r, (const float*)part, dlogit, (const float*)wr, nullptr, (float*)dx);
   prof_end(s);
   count_launch();
@@ -142,11 +144,11 @@ cudaError_t launch_combine_bwd_dense(const Geom& g, const RouteView& r, const vo
                                      const void* dxr, void* dx, cudaStream_t s) {
   prof_begin("combine_bwd", s);
   if (g.dtype == SPT_BF16)
-    combine_kernel<__nv_bfloat16, true><<<(unsigned)g.T, 128, 0, s>>>(
+    (void)launch_pdl(combine_kernel<__nv_bfloat16, true>, dim3((unsigned)g.T), dim3(128), 0, s, 
         g.T, g.d, g.k, r, (const __nv_bfloat16*)part, nullptr, nullptr,
         (const __nv_bfloat16*)dxr, (__nv_bfloat16*)dx);
   else
-    combine_kernel<float, true><<<(unsigned)g.T, 128, 0, s>>>(
+    (void)launch_pdl(combine_kernel<float, true>, dim3((unsigned)g.T), dim3(128), 0, s, 
         g.T, g.d, g.k, r, (const float*)part, nullptr, nullptr, (const float*)dxr, (float*)dx);
   prof_end(s);
   count_launch();
@@ -155,6 +157,8 @@ cudaError_t launch_combine_bwd_dense(const Geom& g, const RouteView& r, const vo
 
 __global__ void gather_dgate_kernel(int64_t T, int k, RouteView r, const float* __restrict__ rows,
                                     float* __restrict__ out) {
+  pdl_wait();  // PDL: predecessor grid complete, its writes visible
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= T * k) return;
   out[i] = rows[pair_row(r, i / k, k, (int)(i % k))];
@@ -163,7 +167,7 @@ __global__ void gather_dgate_kernel(int64_t T, int k, RouteView r, const float* 
 cudaError_t launch_gather_dgate(const Geom& g, const RouteView& r, const float* dgate_rows,
                                 float* dgate_out, cudaStream_t s) {
   prof_begin("gather_dgate", s);
-  gather_dgate_kernel<<<(unsigned)ceil_div(g.pairs, 256), 256, 0, s>>>(g.T, g.k, r, dgate_rows,
+  (void)launch_pdl(gather_dgate_kernel, dim3((unsigned)ceil_div(g.pairs, 256)), dim3(256), 0, s, g.T, g.k, r, dgate_rows,
                                                                        dgate_out);
   prof_end(s);
   count_launch();

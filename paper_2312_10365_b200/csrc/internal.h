@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/spt_ffn.h"
 
 namespace spt {
@@ -88,6 +90,36 @@ int unit_mtiles();  // m-tiles per weight-resident unit (FWD2 / DX); SPT_FFN_UNI
 constexpr int kRasterBlocks = 16;  // blocks per L2 raster group of the gathered-A GEMMs
 
 void count_launch(int n = 1);
+
+// Programmatic dependent launch (PDL): hot-path kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's grid is
+// scheduled while its predecessor drains (its CTAs take SMs as the
+// predecessor's exit and run their prologue -- barrier init, TMEM alloc,
+// tensor-map prefetch).  Every such kernel executes pdl_wait() before its
+// first access to global memory another kernel wrote or reads (it returns once
+// the predecessor grid has completed and its writes are visible; a no-op when
+// launched without the attribute), then pdl_trigger() lets its own successor
+// launch.  SPT_FFN_PDL=0 turns the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 // optional per-kernel CUDA-event profiling (spt_ffn_profile_enable / _read)
 void prof_begin(const char* name, cudaStream_t s);
 void prof_end(cudaStream_t s);

@@ -73,6 +73,8 @@ __global__ void __launch_bounds__(256) topk_hist_kernel(int64_t T, int G, int k,
                                                         int32_t* __restrict__ topk_idx,
                                                         float* __restrict__ topk_gate,
                                                         int32_t* __restrict__ chunk_counts) {
+  pdl_wait();  // PDL: predecessor grid complete, its writes visible
+  pdl_trigger();
   __shared__ int hist[kMaxBlocks];
   for (int b = threadIdx.x; b < G; b += blockDim.x) hist[b] = 0;
   __syncthreads();
@@ -138,6 +140,8 @@ __global__ void __launch_bounds__(256) bucket_scan_kernel(int64_t n_chunks, int 
                                                           const int32_t* __restrict__ counts,
                                                           int32_t* __restrict__ chunk_base,
                                                           int32_t* __restrict__ n_b) {
+  pdl_wait();  // PDL: predecessor grid complete, its writes visible
+  pdl_trigger();
   __shared__ int wsum[8];
   const int b = blockIdx.x;
   const int per = (int)ceil_div(n_chunks, blockDim.x);
@@ -173,6 +177,8 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
     int32_t* __restrict__ block_offsets, int32_t* __restrict__ tile_offsets,
     int32_t* __restrict__ bucket_token, float* __restrict__ bucket_gate,
     int32_t* __restrict__ pair_slot) {
+  pdl_wait();  // PDL: predecessor grid complete, its writes visible
+  pdl_trigger();
   __shared__ int boff[kMaxBlocks + 1];
   __shared__ int toff[kMaxBlocks + 1];
   __shared__ unsigned mask[8][kMaxBlocks];
@@ -237,12 +243,13 @@ cudaError_t launch_topk_bucket(const Geom& g, const RouteView& r, const Bufs& b,
   const unsigned nch = (unsigned)g.n_chunks;
   prof_begin("topk_hist", s);
   const int nslot = (g.G + 31) / 32;
+  cudaError_t e;
   // one CTA of 8 warps per kTopkChunk tokens (4 per warp): T / 32 CTAs, so even
   // 8 K-token batches spread over every SM (the selection is a serial 32-step
   // search per token)
-#define SPT_TOPK(NS)                                                                         \
-  topk_hist_kernel<NS><<<(unsigned)g.n_sub, 256, 0, s>>>(g.T, g.G, g.k, g.gate, r.logits, \
-                                                         r.topk_idx, r.topk_gate, b.chunk_counts)
+#define SPT_TOPK(NS)                                                                        \
+  e = launch_pdl(topk_hist_kernel<NS>, dim3((unsigned)g.n_sub), dim3(256), 0, s, g.T, g.G, g.k, \
+                 g.gate, r.logits, r.topk_idx, r.topk_gate, b.chunk_counts)
   if (nslot <= 1) SPT_TOPK(1);
   else if (nslot == 2) SPT_TOPK(2);
   else if (nslot == 3) SPT_TOPK(3);
@@ -250,16 +257,20 @@ cudaError_t launch_topk_bucket(const Geom& g, const RouteView& r, const Bufs& b,
   else SPT_TOPK(8);
 #undef SPT_TOPK
   prof_end(s);
+  if (e != cudaSuccess) return e;
   prof_begin("bucket_scan", s);
-  bucket_scan_kernel<<<g.G, 256, 0, s>>>(g.n_sub, g.G, b.chunk_counts, b.chunk_base, b.n_b);
+  e = launch_pdl(bucket_scan_kernel, dim3(g.G), dim3(256), 0, s, (int64_t)g.n_sub, g.G,
+                 b.chunk_counts, b.chunk_base, b.n_b);
   prof_end(s);
+  if (e != cudaSuccess) return e;
   prof_begin("bucket_scatter", s);
-  bucket_scatter_kernel<<<nch, 256, 0, s>>>(g.T, g.G, g.k, b.n_b, b.chunk_base, r.topk_idx,
-                                            r.topk_gate, r.block_offsets, r.tile_offsets,
-                                            r.bucket_token, r.bucket_gate, r.pair_slot);
+  e = launch_pdl(bucket_scatter_kernel, dim3(nch), dim3(256), 0, s, g.T, g.G, g.k,
+                 (const int32_t*)b.n_b, (const int32_t*)b.chunk_base, (const int32_t*)r.topk_idx,
+                 (const float*)r.topk_gate, r.block_offsets, r.tile_offsets, r.bucket_token,
+                 r.bucket_gate, r.pair_slot);
   prof_end(s);
   count_launch(3);
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace spt

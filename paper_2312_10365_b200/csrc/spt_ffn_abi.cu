@@ -9,12 +9,23 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace spt {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 // ---- per-kernel profiling: a pair of CUDA events around every launch, on the
 // launch stream; aggregated on read.  Off by default (zero overhead).

@@ -792,6 +792,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // PDL: barriers / TMEM set up; now the predecessor's outputs are visible
+  pdl_trigger();
   const int ntiles = num_tiles<KIND>(a);
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   const long long t_start = clock64();
@@ -1196,6 +1198,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  pdl_wait();  // PDL: barriers / TMEM set up; now the predecessor's outputs are visible
+  pdl_trigger();
   const uint32_t tmem = *tmem_slot;
   const int ntiles = a.unit_offsets[a.G + 1] * a.nu;  // pair tiles x unit tiles
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -1411,6 +1415,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync();  // barriers of both CTAs initialised before any cross-CTA traffic
   tc_fence_after();
+  pdl_wait();  // PDL: barriers / TMEM set up; now the predecessor's outputs are visible
+  pdl_trigger();
   const uint32_t tmem = *tmem_slot;
   const int nunits = a.unit_offsets[a.G];
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -1667,11 +1673,11 @@ static cudaError_t launch(TcArgs& a, int tiles_upper, cudaStream_t s) {
                                  "tc_bwd_dAT", "tc_bwd_dXR"};
   const bool trace_on = trace_begin(a, s);
   prof_begin(kNames[KIND], s);
-  kern<<<grid, kThreads, smem, s>>>(a, stages);
+  cudaError_t le = launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, a, stages);
   prof_end(s);
   if (trace_on) trace_report(a, kNames[KIND], grid, s);
   count_launch();
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = le != cudaSuccess ? le : cudaGetLastError();
   if (debug_sync()) {
     e = cudaStreamSynchronize(s);
     fprintf(stderr, "[spt] tc kind %d grid %d stages %d smem %d BN %d MH %d: %s\n", KIND, grid,
@@ -1717,11 +1723,11 @@ static cudaError_t launch_pair(TcArgs& a, int units_upper, cudaStream_t s) {
   const bool trace_on = trace_begin(a, s);
   const char* name = KIND == K_FWD2 ? "tc_fwd2_down" : "tc_bwd_dX";
   prof_begin(name, s);
-  tc_pair_kernel<KIND><<<2 * clusters, kThreads, smem, s>>>(a, stages);
+  cudaError_t le = launch_pdl(tc_pair_kernel<KIND>, dim3(2 * clusters), dim3(kThreads), smem, s, a, stages);
   prof_end(s);
   if (trace_on) trace_report(a, name, 2 * clusters, s);
   count_launch();
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = le != cudaSuccess ? le : cudaGetLastError();
   if (debug_sync()) {
     e = cudaStreamSynchronize(s);
     fprintf(stderr, "[spt] tc pair kind %d clusters %d stages %d smem %d: %s\n", KIND, clusters,
@@ -1770,11 +1776,11 @@ static cudaError_t launch_pair_gather(TcArgs& a, int tiles_upper, cudaStream_t s
   const bool trace_on = trace_begin(a, s);
   const char* name = KIND == K_FWD1 ? "tc_fwd1_gate_up" : "tc_bwd_dA";
   prof_begin(name, s);
-  tc_pair_gather_kernel<KIND><<<2 * clusters, kThreads, smem, s>>>(a, stages);
+  cudaError_t le = launch_pdl(tc_pair_gather_kernel<KIND>, dim3(2 * clusters), dim3(kThreads), smem, s, a, stages);
   prof_end(s);
   if (trace_on) trace_report(a, name, 2 * clusters, s);
   count_launch();
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = le != cudaSuccess ? le : cudaGetLastError();
   if (debug_sync()) {
     e = cudaStreamSynchronize(s);
     fprintf(stderr, "[spt] tc pair-gather kind %d clusters %d stages %d smem %d BN %d: %s\n", KIND,
@@ -1874,6 +1880,8 @@ bool tc_supported(const Geom& g) {
 __global__ void __launch_bounds__(256) split_bf16_kernel(const float* __restrict__ src,
                                                          __nv_bfloat16* __restrict__ hi,
                                                          __nv_bfloat16* __restrict__ lo, int64_t n) {
+  pdl_wait();  // PDL: predecessor grid complete, its writes visible
+  pdl_trigger();
   const int64_t n4 = n / 4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -1894,11 +1902,11 @@ cudaError_t launch_split_bf16(const float* src, void* dst, int64_t n, cudaStream
   if (n <= 0) return cudaSuccess;
   const int grid = (int)std::min<int64_t>(ceil_div(n / 4 + 1, 256), (int64_t)num_sms() * 8);
   prof_begin("split_bf16", s);
-  split_bf16_kernel<<<grid, 256, 0, s>>>(src, (__nv_bfloat16*)dst,
-                                         (__nv_bfloat16*)lo_half(dst, n), n);
+  cudaError_t le = launch_pdl(split_bf16_kernel, dim3(grid), dim3(256), 0, s, src,
+                              (__nv_bfloat16*)dst, (__nv_bfloat16*)lo_half(dst, n), n);
   prof_end(s);
   count_launch();
-  return cudaGetLastError();
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 bool simt_forced() {
@@ -1942,6 +1950,8 @@ __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, int unit
                                                          int32_t* __restrict__ tile_list,
                                                          int32_t* __restrict__ unit_offsets,
                                                          int32_t* __restrict__ tile_block) {
+  pdl_wait();  // PDL: predecessor grid complete, its writes visible
+  pdl_trigger();
   __shared__ int ntb[kMaxBlocks];
   __shared__ int ntu[kMaxBlocks];  // 128-row tiles per block (units) ...
   for (int i = threadIdx.x; i < G; i += blockDim.x) {
@@ -1991,7 +2001,7 @@ static int raster_blocks() {
 
 static cudaError_t build_schedules(const Geom& g, const RouteView& r, const Bufs& b, cudaStream_t s) {
   prof_begin("tile_sched", s);
-  tile_sched_kernel<<<g.G, 256, 0, s>>>(g.G, (int)ceil_div(g.d, 256), unit_mtiles(),
+  (void)launch_pdl(tile_sched_kernel, dim3(g.G), dim3(256), 0, s, g.G, (int)ceil_div(g.d, 256), unit_mtiles(),
                                         raster_blocks(), r.tile_offsets,
                                         b.tile_list,
                                         b.unit_offsets, b.tile_block);
@@ -2190,6 +2200,8 @@ __global__ void __launch_bounds__(256, 4) da_post_kernel(int64_t T, int G, int b
 
 __global__ void dwr_reduce_kernel(int n_split, int64_t n, const float* __restrict__ part,
                                   float* __restrict__ out, int acc) {
+  pdl_wait();  // PDL: predecessor grid complete, its writes visible
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float s = acc ? out[i] : 0.f;
@@ -2208,6 +2220,8 @@ __global__ void __launch_bounds__(256) dgate_reduce_kernel(int64_t T, int G, int
                                                            float* __restrict__ rows_f,
                                                            float* __restrict__ rows_g,
                                                            __nv_bfloat16* __restrict__ dlg) {
+  pdl_wait();  // PDL: predecessor grid complete, its writes visible
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= T * k) return;
   const int64_t t = i / k;
@@ -2253,7 +2267,7 @@ cudaError_t tc_dense_tn(const Geom& g, const void* ahl, const void* bmat, float*
   TRY(launch<K_DWR>(a, a.NT * a.n_split, s));
   const int64_t n = (int64_t)g.G * g.d;
   prof_begin("dwr_reduce", s);
-  dwr_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(n_split, n, part, out,
+  (void)launch_pdl(dwr_reduce_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, s, n_split, n, part, out,
                                                                accumulate ? 1 : 0);
   prof_end(s);
   count_launch();
@@ -2362,7 +2376,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     if (a.nu > 1) {  // sum the unit tiles' dgate partials; dlogit, dense dlogits
       const int64_t n = g.T * g.k;
       prof_begin("dgate_reduce", s);
-      dgate_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(
+      (void)launch_pdl(dgate_reduce_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, s, 
           g.T, g.G, g.k, a.nu, g.gate, g.gpad, r, b.da, b.dgate, b.dlogit, (__nv_bfloat16*)b.dlg);
       prof_end(s);
       count_launch();
