@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(128) combine_kernel(int64_t T, int d, int k, R
                                                       const TIn* __restrict__ dense,
                                                       TIn* __restrict__ out) {
   pdl_wait();  // PDL: predecessor grid complete, its writes visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   constexpr int V = Vec<TIn>::N;
   __shared__ int64_t rows[kMaxBlocks];
   __shared__ int blk[kMaxBlocks];
@@ -158,7 +158,7 @@ cudaError_t launch_combine_bwd_dense(const Geom& g, const RouteView& r, const vo
 __global__ void gather_dgate_kernel(int64_t T, int k, RouteView r, const float* __restrict__ rows,
                                     float* __restrict__ out) {
   pdl_wait();  // PDL: predecessor grid complete, its writes visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= T * k) return;
   out[i] = rows[pair_row(r, i / k, k, (int)(i % k))];

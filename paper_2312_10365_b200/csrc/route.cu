@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) topk_hist_kernel(int64_t T, int G, int k,
                                                         float* __restrict__ topk_gate,
                                                         int32_t* __restrict__ chunk_counts) {
   pdl_wait();  // PDL: predecessor grid complete, its writes visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   __shared__ int hist[kMaxBlocks];
   for (int b = threadIdx.x; b < G; b += blockDim.x) hist[b] = 0;
   __syncthreads();
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) bucket_scan_kernel(int64_t n_chunks, int 
                                                           int32_t* __restrict__ chunk_base,
                                                           int32_t* __restrict__ n_b) {
   pdl_wait();  // PDL: predecessor grid complete, its writes visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   __shared__ int wsum[8];
   const int b = blockIdx.x;
   const int per = (int)ceil_div(n_chunks, blockDim.x);
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(256) bucket_scatter_kernel(
     int32_t* __restrict__ bucket_token, float* __restrict__ bucket_gate,
     int32_t* __restrict__ pair_slot) {
   pdl_wait();  // PDL: predecessor grid complete, its writes visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   __shared__ int boff[kMaxBlocks + 1];
   __shared__ int toff[kMaxBlocks + 1];
   __shared__ unsigned mask[8][kMaxBlocks];

@@ -21,8 +21,8 @@ void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_r
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("SPT_FFN_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
+    const char* e = getenv("SPT_FFN_PDL");  // measured neutral on B200 (round 2): opt-in
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }

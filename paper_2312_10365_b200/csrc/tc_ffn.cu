@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // PDL: barriers / TMEM set up; now the predecessor's outputs are visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   const int ntiles = num_tiles<KIND>(a);
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
   const long long t_start = clock64();
@@ -1199,7 +1199,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   pdl_wait();  // PDL: barriers / TMEM set up; now the predecessor's outputs are visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   const uint32_t tmem = *tmem_slot;
   const int ntiles = a.unit_offsets[a.G + 1] * a.nu;  // pair tiles x unit tiles
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -1416,7 +1416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();  // barriers of both CTAs initialised before any cross-CTA traffic
   tc_fence_after();
   pdl_wait();  // PDL: barriers / TMEM set up; now the predecessor's outputs are visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   const uint32_t tmem = *tmem_slot;
   const int nunits = a.unit_offsets[a.G];
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
@@ -1881,7 +1881,7 @@ __global__ void __launch_bounds__(256) split_bf16_kernel(const float* __restrict
                                                          __nv_bfloat16* __restrict__ hi,
                                                          __nv_bfloat16* __restrict__ lo, int64_t n) {
   pdl_wait();  // PDL: predecessor grid complete, its writes visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   const int64_t n4 = n / 4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -1951,7 +1951,7 @@ __global__ void __launch_bounds__(256) tile_sched_kernel(int G, int NT, int unit
                                                          int32_t* __restrict__ unit_offsets,
                                                          int32_t* __restrict__ tile_block) {
   pdl_wait();  // PDL: predecessor grid complete, its writes visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   __shared__ int ntb[kMaxBlocks];
   __shared__ int ntu[kMaxBlocks];  // 128-row tiles per block (units) ...
   for (int i = threadIdx.x; i < G; i += blockDim.x) {
@@ -2201,7 +2201,7 @@ __global__ void __launch_bounds__(256, 4) da_post_kernel(int64_t T, int G, int b
 __global__ void dwr_reduce_kernel(int n_split, int64_t n, const float* __restrict__ part,
                                   float* __restrict__ out, int acc) {
   pdl_wait();  // PDL: predecessor grid complete, its writes visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float s = acc ? out[i] : 0.f;
@@ -2221,7 +2221,7 @@ __global__ void __launch_bounds__(256) dgate_reduce_kernel(int64_t T, int G, int
                                                            float* __restrict__ rows_g,
                                                            __nv_bfloat16* __restrict__ dlg) {
   pdl_wait();  // PDL: predecessor grid complete, its writes visible
-  pdl_trigger();
+  // successor launches as this grid's CTAs exit (an early trigger measured slower)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= T * k) return;
   const int64_t t = i / k;

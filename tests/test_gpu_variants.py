@@ -5,6 +5,7 @@ knobs read once per process, so each case runs in its own interpreter):
   SPT_FFN_PAIR=1|0    CTA-pair (cta_group::2) weight-resident kernel for FWD2 + dX / neither (default: dX only)
   SPT_FFN_PAIR_GATHER=0  1-CTA FWD1 / dA kernel (default: CTA-pair gather kernel)
   SPT_FFN_SIMT=1      fp32 on the SIMT (FFMA) kernels instead of the split tensor-core path
+  SPT_FFN_PDL=1       programmatic dependent launch of the hot-path kernels
 """
 import os
 import subprocess
@@ -34,7 +35,7 @@ print("ok")
 
 
 @pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"}, {"SPT_FFN_PAIR": "0"},
-                                 {"SPT_FFN_PAIR_GATHER": "0"}, {"SPT_FFN_SIMT": "1"}])
+                                 {"SPT_FFN_PAIR_GATHER": "0"}, {"SPT_FFN_SIMT": "1"}, {"SPT_FFN_PDL": "1"}])
 def test_variant_parity(env):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True,
