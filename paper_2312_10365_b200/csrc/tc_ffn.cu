@@ -54,6 +54,7 @@ struct TcArgs {
   // fp32 TMEM accumulator (the dropped lo*lo term is <= 2^-18 of each product).
   CUtensorMap ta2;  // lo half of the A operand (geometry of ta)
   CUtensorMap tb2;  // lo half of the B operand (geometry of tb)
+  CUtensorMap tw2;  // fused FWD1 -> FWD2 kernel: W2 (the second GEMM's MN-major B), box 64 x 64
   RouteView r;
   int64_t T;
   int G, d, D, bw, mp, act, gate, gpad;
@@ -370,9 +371,12 @@ __device__ __forceinline__ float bf16_at(uint32_t w, int i) {
 // Row `row` of the tile is TMEM lane `row`; columns [c_lo, c_hi) of it belong
 // to this thread (the other warp of the same lane quarter owns the rest).
 // tacc: TMEM address of (this warp's lane quarter, column 0) of the accumulator.
+// sh (FWD1 of the fused FWD1 -> FWD2 kernel): also write this row's H~ units
+// into the K-major, 128-byte-swizzled smem A tile of the second GEMM
+// (k-block u / 64 at +16 KB, row at +128 B, 16-byte chunk ((u % 64) / 8) ^ (row & 7)).
 template <int KIND, bool kSplit = false>
 __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, uint32_t tacc,
-                                         int row, int half, float* dg_xchg) {
+                                         int row, int half, float* dg_xchg, uint8_t* sh = nullptr) {
   const bool valid = row < ti.n_valid;
   if (KIND == K_ROUTER) {
     const int64_t t = ti.prow0 + row;
@@ -425,6 +429,15 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         }
       }
       if (a.ablate == 2) continue;
+      if (sh) {  // fused FWD2's A operand (this CTA's 128 rows x bw units)
+        const int u = ub + u0;
+        uint8_t* rowp = sh + (u >> 6) * 16384 + row * 128;
+        const int c0 = (u & 63) >> 3;
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          *reinterpret_cast<uint4*>(rowp + (((c0 + q) ^ (row & 7)) << 4)) =
+              make_uint4(ph[4 * q], ph[4 * q + 1], ph[4 * q + 2], ph[4 * q + 3]);
+      }
       if (kSplit) {  // lo halves: same row layout, separate tensors
         uint4* zd = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out_lo + prow * (int64_t)(a.mp * a.bw) + ub + u0);
         uint4* hd = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out2_lo + prow * (int64_t)a.bw + ub + u0);
@@ -1368,6 +1381,363 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// ================================== fused FWD1 -> FWD2 on CTA pairs (a4 + a5)
+// One pair tile (256 bucket rows of block b; CTA r owns rows [128r, 128r+128))
+// runs FWD1 exactly as tc_pair_gather_kernel<FWD1> (gathered X rows, W1_b gate /
+// up halves, M = 256 cta_group::2 MMAs into TMEM columns [0, 256)), then its
+// epilogue writes the Z / H~ stash AND the tile's H~ rows into smem (sH, the
+// K-major A operand of the second GEMM).  The second GEMM P = H~ W2_b runs in
+// 128-column chunks (M = 256, N = 128, K = bw <= 128) into two alternating
+// TMEM accumulators (columns [256, 384) / [384, 512)) whose bf16 rows the
+// epilogue TMA-stores as the per-pair partial rows (Alg. 4 line 5; the combine
+// sums them).  The leader interleaves the chunks of tile i with the FWD1
+// stages of tile i+1, so the partial-row writes (the HBM-bound half of the
+// separate FWD2 kernel) overlap the gather-bound FWD1 mainloop.
+// Warps: 0, 2 TMA gather4 of rows [0, 64) (warp 0 lane 0 also W1_b); 3 lane 0
+// W2_b chunk producer (both CTAs; bytes land on the leader's barrier); 1 MMA
+// issuer (leader) / stage relay (peer); 4-11 epilogue; 12-15 cp.async rows
+// [64, 128).  Epilogue order per tile: FWD1 epilogue, then its chunk drains --
+// so tile i+1's FWD1 epilogue (which overwrites sH) starts only after every
+// chunk MMA of tile i has completed (their t2full commits).
+constexpr int kMlpGatherWarps = 2;  // warps 0, 2
+constexpr int kMlpW2Slots = 2;      // W2_b chunk ring (16 KB per CTA each)
+constexpr int kMlpChunkN = 128;     // N of one second-GEMM chunk (64 columns per CTA)
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_pair_mlp_kernel(const __grid_constant__ TcArgs a, int n_stages) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sH = smem + n_stages * kPairStage;                 // 2 k-blocks x 16 KB
+  uint8_t* sW2 = sH + 32768;                                   // kMlpW2Slots x 16 KB
+  uint8_t* stg_base = sW2 + kMlpW2Slots * 16384;               // kEpiWarps x 4 KB (TMA-store staging)
+  uint64_t* full = (uint64_t*)(stg_base + kEpiWarps * 4096);
+  uint64_t* empty = full + n_stages;
+  uint64_t* w2full = empty + n_stages;
+  uint64_t* w2empty = w2full + kMlpW2Slots;
+  // TMEM: two 256-column buffers used in turn by the tiles of this cluster (tile
+  // n -> buffer n & 1): FWD1 accumulates there, and after its epilogue the same
+  // buffer's halves [0, 128) / [128, 256) take the tile's second-GEMM chunks
+  // (chunk c -> half c & 1) -- so the FWD1 of tile n+1 (other buffer) overlaps
+  // the FWD1 epilogue of tile n.
+  uint64_t* t1full = w2empty + kMlpW2Slots;   // [2] FWD1 accumulator of buffer x complete
+  uint64_t* hready = t1full + 2;              // FWD1 epilogue done (sH written, buffer read)
+  uint64_t* t2full = hready + 1;              // [2][2] chunk accumulator (buffer, half) complete
+  uint64_t* t2empty = t2full + 4;             // [2][2] chunk accumulator drained
+  uint32_t* tmem_slot = (uint32_t*)(t2empty + 4);
+  float* dg_xchg = (float*)(tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nh = a.BN / 2;                         // FWD1 B rows held by this CTA
+  const int nchunks = (a.d + kMlpChunkN - 1) / kMlpChunkN;
+  const int kb2 = (a.bw + 63) / 64;                // K blocks of the second GEMM (<= 2)
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(&full[s], kMlpGatherWarps + kCpThreadsA + (leader ? 1 : 0));
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < kMlpW2Slots; ++i) {
+      mbar_init(&w2full[i], 1);
+      mbar_init(&w2empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) mbar_init(&t1full[i], 1);
+    mbar_init(hready, 2 * kEpiWarps);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&t2full[i], 1);
+      mbar_init(&t2empty[i], 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&a.ta);
+    tma_prefetch_desc(&a.tb);
+    tma_prefetch_desc(&a.tw2);
+    tma_prefetch_desc(&a.tc);
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  pdl_wait();
+  const uint32_t tmem = *tmem_slot;
+  const int ntiles = a.unit_offsets[a.G + 1];  // pair tiles (nu == 1)
+  // SPT_FFN_TRACE slots: 0 MMA wait stage, 1 MMA wait acc1 / H~, 2 epi wait acc1,
+  // 3 epi wait chunk, 4 MMA wait W2 chunk, 5 MMA wait acc2, 6 total, 7 epi drain busy
+  unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+  const long long t_start = clock64();
+
+  auto my_half = [&](int tile) {
+    TileInfo ti = decode<K_FWD1>(a, tile);
+    ti.n_valid -= (int)rank * 128;
+    ti.prow0 += rank * 128;
+    ti.pos0 += rank * 128;
+    ti.rows_pad -= (int)rank * 128;
+    return ti;
+  };
+
+  if (warp == 0 || warp == 2) {
+    // --------- TMA gather4 of rows [0, kPairRows); warp 0 lane 0 also loads W1_b
+    const int p = warp == 0 ? 0 : 1;
+    const int c = lane * kMlpGatherWarps + p;
+    constexpr int n_calls = kPairRows / 4;
+    const bool has_call = c < n_calls;
+    const int my_calls = n_calls > p ? (n_calls - p + kMlpGatherWarps - 1) / kMlpGatherWarps : 0;
+    const uint32_t tx = (uint32_t)my_calls * 512u + (p == 0 ? (uint32_t)nh * 128u : 0u);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = cid; tile < ntiles; tile += ncl) {
+      const TileInfo ti = my_half(tile);
+      int rr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * c + i;
+        rr[i] = (has_call && r < ti.n_valid) ? a.r.bucket_token[ti.pos0 + r] : (int)a.T;
+      }
+      const int u0 = ti.b * a.bw;
+      const int brow = a.mp == 2 ? (int)rank * a.D + u0 : u0 + (int)rank * nh;
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        if (lane == 0) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], tx);
+        }
+        __syncwarp();
+        uint8_t* sA = smem + stage * kPairStage;
+        if (p == 0 && lane == 0) tma_load_2d(sA + kABytes, &a.tb, &full[stage], kb * 64, brow);
+        if (has_call) tma_gather4(sA + c * 512, &a.ta, &full[stage], kb * 64, rr[0], rr[1], rr[2], rr[3]);
+        if (++stage == n_stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 3) {
+    // ------------- W2_b chunk producer (both CTAs): this CTA's 64 columns
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t wph = 0;
+      for (int tile = cid; tile < ntiles; tile += ncl) {
+        const TileInfo ti = decode<K_FWD1>(a, tile);
+        for (int ch = 0; ch < nchunks; ++ch) {
+          mbar_wait(&w2empty[slot], wph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&w2full[slot], 2u * (uint32_t)kb2 * 8192u);
+          for (int k2 = 0; k2 < kb2; ++k2)
+            tma_load_2d_pair(sW2 + slot * 16384 + k2 * 8192, &a.tw2, &w2full[slot],
+                             ch * kMlpChunkN + (int)rank * 64, ti.b * a.bw + k2 * 64);
+          if (++slot == kMlpW2Slots) { slot = 0; wph ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 12) {
+    // ------------------------------- cp.async of rows [kPairRows, 128)
+    const int t = threadIdx.x - 12 * 32;  // 0..127
+    const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
+    const int ch = t & 7;
+    constexpr int kRowsPer = (128 - kPairRows) * 8 / kCpThreadsA;  // 4
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = cid; tile < ntiles; tile += ncl) {
+      const TileInfo ti = my_half(tile);
+      int tok[kRowsPer];
+#pragma unroll
+      for (int i = 0; i < kRowsPer; ++i) {
+        const int r = kPairRows + (t >> 3) + 16 * i;
+        tok[i] = r < ti.n_valid ? a.r.bucket_token[ti.pos0 + r] : -1;
+      }
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
+        __syncwarp();
+        const uint32_t sA = smem_u32(smem + stage * kPairStage);
+#pragma unroll
+        for (int i = 0; i < kRowsPer; ++i) {
+          const int r = kPairRows + (t >> 3) + 16 * i;
+          const uint32_t dst = sA + r * 128 + ((ch ^ (r & 7)) << 4);
+          const __nv_bfloat16* g = src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kb * 64 + ch * 8;
+          cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
+        }
+        cp_async_arrive_noinc(&full[stage]);
+        if (++stage == n_stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ------------------------------------------- MMA issuer (leader)
+      const uint32_t idesc1 = idesc_bf16(256, a.BN, false, false);
+      const uint32_t idesc2 = idesc_bf16(256, kMlpChunkN, false, true);
+      const uint64_t adesc0 = sdesc_sw128(smem_u32(smem), 16, 1024);
+      const uint64_t bdesc0 = sdesc_sw128(smem_u32(smem) + kABytes, 16, 1024);
+      const uint64_t hdesc0 = sdesc_sw128(smem_u32(sH), 16, 1024);
+      const uint64_t wdesc0 = sdesc_sw128(smem_u32(sW2), 8192, 1024);
+      unsigned long long* trl = lane == 0 ? tr : nullptr;
+      int stage = 0, slot = 0;
+      uint32_t phase = 0, wph = 0, hph = 0;
+      int chunk = 0, px = 0;  // next chunk of the previous tile (buffer px)
+      // chunk `chunk` of the previous tile into buffer px, half chunk & 1: waits its
+      // W2_b chunk and the drain of chunk - 2 (the same half; its completion index
+      // on that barrier is chunk / 2 - 1 within the tile, 16 per tile -> parity)
+      auto issue_chunk = [&]() {
+        const int h = chunk & 1;
+        twait(&w2full[slot], wph, trl, 4);
+        if (chunk >= 2) twait(&t2empty[px * 2 + h], ((chunk >> 1) - 1) & 1, trl, 5);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t dtm = tmem + px * 256 + h * kMlpChunkN;
+          const uint64_t wd = wdesc0 + (uint64_t)((slot * 16384) >> 4);
+          for (int k2 = 0; k2 < kb2; ++k2) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16_pair(dtm, hdesc0 + (uint64_t)((k2 * 16384) >> 4) + k * 2,
+                            wd + (uint64_t)((k2 * 8192) >> 4) + k * 128, idesc2,
+                            (k2 != 0 || k != 0) ? 1u : 0u);
+          }
+          mma_commit_pair(&w2empty[slot]);
+          mma_commit_pair(&t2full[px * 2 + h]);
+        }
+        __syncwarp();
+        if (++slot == kMlpW2Slots) { slot = 0; wph ^= 1; }
+        ++chunk;
+      };
+      bool prev = false;
+      int n = 0;  // this cluster's tile sequence number (buffer n & 1)
+      for (int tile = cid;; tile += ncl, ++n) {
+        const bool cur = tile < ntiles;
+        if (!cur && !prev) break;
+        const int x = n & 1;
+        bool started = false;  // the previous tile's FWD1 epilogue is done (hready)
+        int kb0 = 0;           // the stage at which it was seen
+        chunk = 0;
+        px = x ^ 1;
+        if (cur) {
+          const TileInfo ti = decode<K_FWD1>(a, tile);
+          if (n >= 2) {  // buffer x: every chunk drain of tile n - 2 (the last of each half)
+            twait(&t2empty[x * 2 + 0], 1u, trl, 1);
+            twait(&t2empty[x * 2 + 1], 1u, trl, 1);
+          }
+          tc_fence_after();
+          for (int kb = 0; kb < ti.nkb; ++kb) {
+            if (prev && chunk < nchunks) {
+              if (!started && mbar_test(hready, hph)) {
+                started = true;
+                kb0 = kb;
+                hph ^= 1;
+                tc_fence_after();
+              }
+              // spread the chunks evenly over the stages left once started
+              if (started && chunk * (ti.nkb - kb0) <= (kb - kb0) * nchunks) issue_chunk();
+            }
+            twait(&full[stage], phase, trl, 0);
+            fence_proxy_async_smem();  // this CTA's cp.async rows -> async proxy
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t soff = (uint64_t)((stage * kPairStage) >> 4);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_pair(tmem + x * 256, adesc0 + soff + k * 2, bdesc0 + soff + k * 2, idesc1,
+                              (kb != 0 || k != 0) ? 1u : 0u);
+              mma_commit_pair(&empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == n_stages) { stage = 0; phase ^= 1; }
+          }
+          if (elect_one()) mma_commit_pair(&t1full[x]);
+          __syncwarp();
+        }
+        if (prev && chunk < nchunks) {
+          if (!started) {
+            twait(hready, hph, trl, 1);
+            hph ^= 1;
+            tc_fence_after();
+          }
+          while (chunk < nchunks) issue_chunk();
+        }
+        prev = cur;
+      }
+    } else if (lane == 0) {
+      // ------------- relay (peer): this CTA's stage complete -> leader
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < ntiles; tile += ncl) {
+        const TileInfo ti = decode<K_FWD1>(a, tile);
+        for (int kb = 0; kb < ti.nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_proxy_async_smem();
+          mbar_arrive_remote_relaxed(&full[stage], 0);
+          if (++stage == n_stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 4 + kEpiWarps) {
+    // ------------------------------------------- epilogue (both CTAs)
+    const int e = warp - 4;
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int half = e >> 2;  // FWD1: unit half (= k-block of sH); chunks: 64-column half
+    uint8_t* stg = stg_base + e * 4096;
+    int n = 0;
+    for (int tile = cid; tile < ntiles; tile += ncl, ++n) {
+      const TileInfo ti = my_half(tile);
+      const int x = n & 1;
+      // FWD1: Z / H~ stash + the smem H~ tile (sH is free: every chunk MMA of the
+      // previous tile completed before this warp drained its last chunk)
+      unsigned long long* tre = (tr && threadIdx.x == 4 * 32) ? tr : nullptr;
+      twait(&t1full[x], (n >> 1) & 1, tre, 2);
+      tc_fence_after();
+      if (ti.rows_pad > 0)
+        epilogue<K_FWD1>(a, ti, tmem + ((uint32_t)(q * 32) << 16) + x * 256, row, half, dg_xchg, sH);
+      fence_proxy_async_smem();  // sH (generic writes) -> the async proxy of the chunk MMAs
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(hready);
+        else mbar_arrive_remote_relaxed(hready, 0);
+      }
+      // second GEMM: this tile's partial rows, chunk by chunk
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int h = ch & 1;
+        twait(&t2full[x * 2 + h], (ch >> 1) & 1, tre, 3);
+        const long long td0 = tre ? clock64() : 0;
+        tc_fence_after();
+        const int col0 = ch * kMlpChunkN + half * 64;
+        uint32_t v[64];
+        tmem_ld64(tmem + ((uint32_t)(q * 32) << 16) + x * 256 + h * kMlpChunkN + half * 64, v, true);
+        if (ti.rows_pad > 0 && col0 < a.d) {
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 w = make_uint4(pack_bf16(__uint_as_float(v[8 * c + 0]), __uint_as_float(v[8 * c + 1])),
+                                       pack_bf16(__uint_as_float(v[8 * c + 2]), __uint_as_float(v[8 * c + 3])),
+                                       pack_bf16(__uint_as_float(v[8 * c + 4]), __uint_as_float(v[8 * c + 5])),
+                                       pack_bf16(__uint_as_float(v[8 * c + 6]), __uint_as_float(v[8 * c + 7])));
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) = w;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&a.tc, stg, col0, (int)(ti.prow0 + q * 32));
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&t2empty[x * 2 + h]);
+          else mbar_arrive_remote_relaxed(&t2empty[x * 2 + h], 0);
+        }
+        if (tre) tre[7] += (unsigned long long)(clock64() - td0);
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[6] = (unsigned long long)(clock64() - t_start);
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem);
+  }
+}
+
 // ============================================= CTA-pair weight-resident GEMMs
 // FWD2 / DX on CTA pairs (cta_group::2): a unit (block b, 256 output columns,
 // its m-tiles) runs on a 2-CTA cluster; CTA r computes m-tiles 2p + r, keeps
@@ -1789,6 +2159,62 @@ static cudaError_t launch_pair_gather(TcArgs& a, int tiles_upper, cudaStream_t s
   return e;
 }
 
+// fused FWD1 -> FWD2 (tc_pair_mlp_kernel): SwiGLU blocks of 128 units on the
+// CTA-pair gather path; SPT_FFN_MLP=0 runs the two GEMMs as separate kernels
+// Measured on B200 (round 2), LLaMA shapes: parity-clean and 2-4 % slower than the
+// two kernels (1.42 vs 1.38 ms at 16 K tokens, 2.84 vs 2.72 ms at 32 K): sH, the
+// W2 ring and the store staging leave FWD1 a 4-stage (128 KB) operand ring instead
+// of 7, and the gathered mainloop loses what the overlap gains -> opt-in
+static bool mlp_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_MLP");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+static bool mlp_ok(const Geom& g) { return g.mp == 2 && g.bw == 128 && !g.split && mlp_enabled(); }
+
+static cudaError_t launch_pair_mlp(TcArgs& a, int tiles_upper, cudaStream_t s) {
+  // sH, W2 ring, TMA-store staging, barriers
+  const int fixed = 32768 + kMlpW2Slots * 16384 + kEpiWarps * 4096 + 2048;
+  const int stages = std::min(6, (227 * 1024 - fixed) / kPairStage);
+  const int smem = stages * kPairStage + fixed;
+  static std::atomic<bool> attr_set[kMaxDev];
+  static std::atomic<int> mc_cache[kMaxDev];
+  if (cudaError_t e = set_smem_attr_once(tc_pair_mlp_kernel, attr_set)) return e;
+  const int max_clusters = max_pair_clusters(tc_pair_mlp_kernel, smem, mc_cache);
+  const int clusters = std::max(1, std::min(tiles_upper, max_clusters));
+  const bool trace_on = trace_begin(a, s);
+  prof_begin("tc_fwd1_fwd2", s);
+  cudaError_t le = launch_pdl(tc_pair_mlp_kernel, dim3(2 * clusters), dim3(kThreads), smem, s, a, stages);
+  prof_end(s);
+  if (trace_on) {
+    unsigned long long h[1024 * kTraceSlots];
+    cudaMemcpyAsync(h, g_trace_buf, sizeof(unsigned long long) * 2 * clusters * kTraceSlots,
+                    cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double sum[kTraceSlots] = {0};
+    for (int b = 0; b < 2 * clusters; b += 2)  // leaders (MMA) and their epilogue
+      for (int i = 0; i < kTraceSlots; ++i) sum[i] += (double)h[b * kTraceSlots + i];
+    const double tot = sum[6] > 0 ? sum[6] : 1;
+    fprintf(stderr,
+            "[spt-trace] fused fwd1->fwd2 (leaders) | MMA wait stage %.0f%% acc1/H %.0f%% W2 %.0f%% "
+            "acc2 %.0f%% | epi wait acc1 %.0f%% chunk %.0f%% drain busy %.0f%% | cta cycles %.0f\n",
+            100 * sum[0] / tot, 100 * sum[1] / tot, 100 * sum[4] / tot, 100 * sum[5] / tot,
+            100 * sum[2] / tot, 100 * sum[3] / tot, 100 * sum[7] / tot, tot / clusters);
+    a.trace = nullptr;
+  }
+  count_launch();
+  cudaError_t e = le != cudaSuccess ? le : cudaGetLastError();
+  if (debug_sync()) {
+    e = cudaStreamSynchronize(s);
+    fprintf(stderr, "[spt] fused fwd1->fwd2 clusters %d stages %d smem %d: %s\n", clusters, stages,
+            smem, cudaGetErrorString(e));
+  }
+  return e;
+}
+
 template <int KIND>
 static cudaError_t launch_bres(TcArgs& a, int units_upper, cudaStream_t s) {
   const int kbu = KIND == K_FWD2 ? (a.bw + 63) / 64 : (a.mp * a.bw + 63) / 64;
@@ -2029,6 +2455,25 @@ cudaError_t tc_forward(const Geom& g, const void* x, const void* w1, const void*
     x = b.xs;
     w1 = b.w1s;
     w2 = b.w2s;
+  }
+  if (!lo && mlp_ok(g) && use_pair_gather()) {  // a4 + a5 in one kernel, then the combine
+    TcArgs a{};
+    base_args(a, g, r);
+    a.tile_list = b.tile_list;
+    a.bn_u = g.bw;
+    a.nu = 1;
+    bool ok = make_tmap_bf16_2d(&a.ta, x, g.T, g.d, g.d, 64, 1) &&
+              make_tmap_bf16_2d(&a.tb, w1, (uint64_t)g.mp * g.D, g.d, g.d, 64, a.bn_u) &&
+              make_tmap_bf16_2d(&a.tw2, w2, g.D, g.d, g.d, 64, 64) &&
+              make_tmap_bf16_2d(&a.tc, b.part, g.rows_cap, g.d, g.d, 64, 32);
+    a.BN = g.mp * a.bn_u;
+    a.MH = 2;
+    a.aux2 = x;
+    a.out = b.z;
+    a.out2 = b.h;
+    a.unit_offsets = b.unit_offsets;
+    TRY(launch_pair_mlp(a, up / 2 + g.G, s));
+    return launch_combine_fwd(g, r, b.part, y, s);
   }
   {
     // LoRA: FWD1 runs on X_aug / W1_aug (K = d + 64: the u C_I term is one more K stage)

@@ -6,6 +6,7 @@ knobs read once per process, so each case runs in its own interpreter):
   SPT_FFN_PAIR_GATHER=0  1-CTA FWD1 / dA kernel (default: CTA-pair gather kernel)
   SPT_FFN_SIMT=1      fp32 on the SIMT (FFMA) kernels instead of the split tensor-core path
   SPT_FFN_PDL=1       programmatic dependent launch of the hot-path kernels
+  SPT_FFN_MLP=1       fused FWD1 -> FWD2 CTA-pair kernel (SwiGLU, bw = 128)
 """
 import os
 import subprocess
@@ -35,9 +36,20 @@ print("ok")
 
 
 @pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"}, {"SPT_FFN_PAIR": "0"},
-                                 {"SPT_FFN_PAIR_GATHER": "0"}, {"SPT_FFN_SIMT": "1"}, {"SPT_FFN_PDL": "1"}])
+                                 {"SPT_FFN_PAIR_GATHER": "0"}, {"SPT_FFN_SIMT": "1"}, {"SPT_FFN_PDL": "1"}, {"SPT_FFN_MLP": "1"}])
 def test_variant_parity(env):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True,
                        text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_fused_fwd1_fwd2_many_tiles():
+    """SPT_FFN_MLP=1 at a T where every cluster runs several pair tiles (both TMEM
+    buffers in turn, chunk drains of tile n-2 gating FWD1 of tile n) and buckets
+    end in ragged tiles."""
+    code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests")).replace(
+        'for name, T in (("bert", 700), ("llama", 300), ("tiny", 333)):', 'for name, T in (("llama", 3001),):')
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "SPT_FFN_MLP": "1"},
+                       capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
