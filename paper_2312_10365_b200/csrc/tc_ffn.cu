@@ -110,7 +110,12 @@ constexpr int kEpiWarps = 8;                  // warps 4..11
 constexpr int kTmaGatherWarps = 3;            // FWD1 / DA: warps 0, 2, 3
 constexpr int kTmaRows = 128;                 // FWD1 / DA: rows per stage gathered by TMA
 constexpr int kCpThreadsA = 128;              // FWD1 / DA: cp.async warps 12..15
-constexpr int kCpThreadsB = 192;              // DW*: cp.async warps 2, 3, 12..15
+// DW*: cp.async warps 2, 3, 8..15 (10 warps).  The dW tiles run ~130 K stages per
+// epilogue, so warps 8..11 gather instead of waiting as epilogue warps: the B rows
+// (32 KB gathered per 512-1024 MMA clocks) are what bounds dW2 / dW1
+constexpr int kGatherWarpsB = 10;
+constexpr int kCpThreadsB = kGatherWarpsB * 32;
+constexpr int kEpiWarpsDW = 4;                // DW*: epilogue warps 4..7 (one per TMEM lane quarter)
 constexpr int kABytes = 16384;                // 128 rows x 64 bf16
 
 // kinds whose 256 gathered token rows per stage come from the pair-tile list:
@@ -779,7 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   // two accumulators alternate between tiles when both fit in TMEM
   const int n_acc = tm_nacc(a.BN, a.MH);
   constexpr bool kGather = kind_gather_a(KIND) || kind_gather_b(KIND);  // uses cp.async
-  const int n_epi = kEpiWarps;
+  const int n_epi = kind_gather_b(KIND) ? kEpiWarpsDW : kEpiWarps;
   if (threadIdx.x == 0) {
     // stage barrier: warp 0's TMA arm (+ expected bytes); FWD1 / DA: one arm
     // per gather4 warp; DW*: one cp.async completion arrival per gather thread
@@ -1004,42 +1009,38 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         if (++stage == n_stages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (kind_gather_b(KIND) && (warp == 2 || warp == 3 || warp >= 12)) {
-    // -------------------------- DW*: cp.async row gathers of B (6 warps)
+  } else if (kind_gather_b(KIND) && (warp == 2 || warp == 3 || warp >= 8)) {
+    // ------------------------- DW*: cp.async row gathers of B (10 warps)
     // B: BK bucket rows (K) x 256 columns (N) per stage, MN-major: 64-column
     // chunk j at +BK*128 B*j, K row r at +128 B*r, 16-byte piece p swizzled
-    // by r.  This thread: piece (gt & 31) of rows r_i = (gt >> 5) + 6 i.  Its
+    // by r.  This thread: piece (gt & 31) of rows r_i = (gt >> 5) + 10 i.  Its
     // arrival on the stage barrier fires when its copies have landed.
-    constexpr int kRowsG = (BK + 5) / 6;  // rows per thread (upper bound)
-    const int gt = (warp < 4 ? warp - 2 : warp - 10) * 32 + lane;  // 0..191
+    constexpr int kRowsG = (BK + kGatherWarpsB - 1) / kGatherWarpsB;  // rows per thread (upper bound)
+    const int gt = (warp < 4 ? warp - 2 : warp - 6) * 32 + lane;  // 0..319
     const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
     const int j = (gt & 31) >> 3, pc = gt & 7;
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo ti = decode<KIND>(a, tile);
-      int tok[kRowsG];
-      auto load_idx = [&](int kb) {
+      int tk[kRowsG];  // this stage's token rows (loaded one stage ahead)
+      auto load_idx = [&](int kb, int (&t)[kRowsG]) {
         int kk = kb;
         kpass(ti, kb, kk);
 #pragma unroll
         for (int i = 0; i < kRowsG; ++i) {
-          const int r = (gt >> 5) + 6 * i;
+          const int r = (gt >> 5) + kGatherWarpsB * i;
           const int e = kk * BK + r;
-          tok[i] = (r < BK && e < ti.n_valid) ? a.r.bucket_token[ti.pos0 + e] : -1;
+          t[i] = (r < BK && e < ti.n_valid) ? a.r.bucket_token[ti.pos0 + e] : -1;
         }
       };
-      if (ti.nkb > 0) load_idx(0);
-      // one thread per row warms L2 with the row's 512-byte N slice, a stage ahead
-      auto prefetch_rows = [&]() {
-        if (a.prefetch && (gt & 31) == 0) {
+      if (ti.nkb > 0) load_idx(0, tk);
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        if (a.prefetch && (gt & 31) == 0) {  // warm L2 with this stage's rows (opt-in)
 #pragma unroll
           for (int i = 0; i < kRowsG; ++i)
-            if (tok[i] >= 0) prefetch_l2_bulk(src + (int64_t)tok[i] * a.d + ti.nt * 256, 512);
+            if (tk[i] >= 0) prefetch_l2_bulk(src + (int64_t)tk[i] * a.d + ti.nt * 256, 512);
         }
-      };
-      prefetch_rows();
-      for (int kb = 0; kb < ti.nkb; ++kb) {
         if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
         __syncwarp();
         const uint32_t sB = smem_u32(smem + stage * sstride + astride);
@@ -1047,19 +1048,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const __nv_bfloat16* srcp = kpass(ti, kb, kk) == 1 ? (const __nv_bfloat16*)a.aux2_lo : src;
 #pragma unroll
         for (int i = 0; i < kRowsG; ++i) {
-          const int r = (gt >> 5) + 6 * i;
-          if (r < BK) {
+          const int r = (gt >> 5) + kGatherWarpsB * i;
+          if (r < BK && a.ablate != 1) {
             const uint32_t dst = sB + j * (BK * 128) + r * 128 + ((pc ^ (r & 7)) << 4);
             const __nv_bfloat16* g =
-                srcp + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + ti.nt * 256 + j * 64 + pc * 8;
-            cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
+                srcp + (int64_t)(tk[i] < 0 ? 0 : tk[i]) * a.d + ti.nt * 256 + j * 64 + pc * 8;
+            cp_async_16(dst, g, tk[i] < 0 ? 0u : 16u);
           }
         }
         cp_async_arrive_noinc(&full[stage]);
-        if (kb + 1 < ti.nkb) {
-          load_idx(kb + 1);
-          prefetch_rows();
-        }
+        if (kb + 1 < ti.nkb) load_idx(kb + 1, tk);
         if (++stage == n_stages) { stage = 0; phase ^= 1; }
       }
     }
@@ -1139,6 +1137,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       } else if (KIND == K_DAT) {
         epilogue_dat(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, 0), q, lane, half,
                      stg_base + e * 4096);
+      } else if (kind_gather_b(KIND)) {  // DW*: 4 warps cover both halves (M or column)
+        for (int hf = 0; hf < 2; ++hf) {
+          const uint32_t col0 = tm_col(a.BN, a.MH, acc, a.MH == 2 ? hf : 0);
+          epilogue<KIND, kSplit>(a, ti, tmem + lanes + col0, row, hf, dg_xchg);
+        }
       } else {
         const uint32_t col0 = tm_col(a.BN, a.MH, acc, a.MH == 2 ? half : 0);
         epilogue<KIND, kSplit>(a, ti, tmem + lanes + col0, row, half, dg_xchg);
