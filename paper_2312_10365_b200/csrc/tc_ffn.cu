@@ -505,9 +505,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? nut : min(nut, u_lo + hw);
     float dgate = 0.f;
     for (int u0 = u_lo; u0 < u_hi; u0 += 16) {  // 16 units per step (register budget)
-      uint32_t v[16];
-      tmem_ld16(tacc + u0, v);
-      tmem_ld_wait();
+      // the Z stash loads are issued before the TMEM load so the two latencies overlap
       uint32_t zg4[8], zu4[8], zgl[8], zul[8];
       if (valid) {
         auto ld8 = [](const __nv_bfloat16* src, uint32_t (&w8)[8]) {
@@ -525,6 +523,9 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
           if (a.mp == 2) ld8(zrl + a.bw + u0, zul);
         }
       }
+      uint32_t v[16];
+      tmem_ld16(tacc + u0, v);
+      tmem_ld_wait();
       uint32_t pg[8], pu[8], lg[8], lu[8];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
