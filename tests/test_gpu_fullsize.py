@@ -163,3 +163,21 @@ def test_fullsize_skewed_routing(orc, kind):
         assert np.all(got["dw1"][:, rows] == 0) and np.all(got["dw2"][rows] == 0)
         assert np.all(got["dw_r"][b] == 0)
     _euler(cfg, inp, got)
+
+
+def test_max_tokens_int64_offsets(orc):
+    """Four times the LLaMA-scale batch (T = 131,072, 2.9 M (token, block) pairs): the
+    per-pair rows x d of the partial buffers (11.8 G elements) overflow 32-bit offsets,
+    so every kernel's row addressing must be 64-bit.  Router tiles, selection and
+    buckets as in the full-size test; sampled token rows of y / dx / dgate against the
+    oracle; the Euler identities over the full outputs."""
+    cfg = S.ALL_CONFIGS["llama_scale"].with_(T=131072)
+    T = cfg.T
+    inp = S.make_inputs(cfg, T)
+    got = gpu_run(cfg, T, inp)
+    lg, ti = _router_parity(orc, cfg, got, inp["x"], inp["w_r"])
+    _bucket_parity(orc, cfg, got, ti)
+    rng = np.random.default_rng(cfg.seed + 11)
+    tokens = np.unique(np.concatenate([[0, T - 1, T // 2], rng.integers(0, T, 9)])).astype(np.int64)
+    _sampled_ffn_parity(orc, cfg, inp, got, lg, ti, tokens, np.zeros(0, np.int32))
+    _euler(cfg, inp, got)
