@@ -158,6 +158,34 @@ def test_empty_batch():
     assert float(f.dw1.abs().max()) == 0.0
 
 
+def test_empty_batch_bf16():
+    """T = 0 on the tcgen05 path (LLaMA shapes): no launch reads a token, the
+    buckets are empty and dW are zeroed (SPT_BWD_ACCUMULATE_DW off)."""
+    import torch
+    import paper_2312_10365_b200 as P
+    cfg = S.CONFIGS["llama"]
+    f = P.RoutedFFN(0, cfg.d, cfg.D, cfg.G, cfg.k, torch.bfloat16, cfg.act)
+    x = torch.empty(0, cfg.d, device="cuda", dtype=torch.bfloat16)
+    w1 = torch.randn(2, cfg.D, cfg.d, device="cuda").to(torch.bfloat16)
+    w2 = torch.randn(cfg.D, cfg.d, device="cuda").to(torch.bfloat16)
+    w_r = torch.randn(cfg.G, cfg.d, device="cuda").to(torch.bfloat16)
+    f.route(x, w_r)
+    f.forward(x, w1, w2)
+    f.dw1.fill_(7)
+    f.dw_r.fill_(7)
+    f.backward(x, w1, w2, w_r, x)
+    torch.cuda.synchronize()
+    assert f.route_buf.block_offsets.cpu().tolist() == [0] * (cfg.G + 1)
+    assert float(f.dw1.abs().max()) == 0.0 and float(f.dw_r.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("name", ["bert", "llama"])
+def test_single_token_bf16(orc, name):
+    """T = 1: every selected block holds one row of a 128-row tile (ragged in
+    every bucket), the other G - k buckets are empty."""
+    _parity(orc, S.CONFIGS[name], 1)
+
+
 @pytest.mark.parametrize("name", ["tiny", "bert"])
 def test_accumulate_dw(orc, name):
     cfg = S.CONFIGS[name]
