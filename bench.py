@@ -624,7 +624,9 @@ def main():
         if lora is None:
             f.forward(x, w1, w2)
             ar.wait()
-            f.backward(x, w1, w2, w_r, dy, dw_event=ar.event)
+            # single process: no event, so the library runs dX first and the
+            # grad-input combine as side work of the dW kernels
+            f.backward(x, w1, w2, w_r, dy, dw_event=ar.event if ar.active else None)
         else:
             f.forward(x, w1, w2, lora)
             ar.wait()

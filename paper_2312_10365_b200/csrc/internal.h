@@ -66,6 +66,7 @@ struct Bufs {
   int32_t* chunk_counts;  // [n_sub, G] bucket counts per kTopkChunk tokens
   int32_t* chunk_base;    // [n_sub, G] exclusive prefix over the sub-chunks
   int32_t* n_b;           // [G]
+  int32_t* side_ctr;      // [64] work counters (dW kernels' grad-input combine side work)
   // device tile schedules (stash: built by the forward, reused by the backward)
   int32_t* tile_list;     // [ceil(T*k/128) + G]: bucket tiles in (m-tile, block) order
   int32_t* unit_offsets;  // [G+2]: prefix of weight-resident work units per block; [G+1] = pair tiles

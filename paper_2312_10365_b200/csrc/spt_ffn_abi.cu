@@ -108,7 +108,7 @@ static int dwr_splits(const Geom& g) { return dense_tn_splits(g); }
 
 struct Sizes {
   size_t z, h, stash;
-  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, tl, uo, tb, lbp, lbx, xs, ws_w, ws;
+  size_t part, dz, da, dlogit, dgate, dlg, dwr, counts, base, nb, ctr, tl, uo, tb, lbp, lbx, xs, ws_w, ws;
 };
 
 static Sizes compute_sizes(const Geom& g) {
@@ -137,10 +137,11 @@ static Sizes compute_sizes(const Geom& g) {
   s.counts = align256((size_t)g.n_sub * g.G * 4);
   s.base = s.counts;
   s.nb = align256((size_t)g.G * 4);
+  s.ctr = 256;  // work counters (the dW kernels' grad-input combine side work)
   s.lbp = align256((size_t)g.n_chunks * g.G * 4);  // balance loss: per-chunk softmax sums
   s.lbx = g.lbw == 0.f ? 0                         // balance gradient: dense router term
           : align256(g.dtype == SPT_BF16 ? (size_t)g.T * g.d * 2 : (size_t)g.T * g.G * 4);
-  s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb +
+  s.ws = s.part + s.dz + s.da + s.dlogit + s.dgate + s.dlg + s.dwr + s.counts + s.base + s.nb + s.ctr +
          s.lbp + s.lbx + 2 * s.xs + s.ws_w;
   return s;
 }
@@ -169,6 +170,7 @@ static Bufs carve(const Geom& g, void* stash, void* ws) {
   b.chunk_counts = (int32_t*)w; w += s.counts;
   b.chunk_base = (int32_t*)w; w += s.base;
   b.n_b = (int32_t*)w; w += s.nb;
+  b.side_ctr = (int32_t*)w; w += s.ctr;
   b.lb_part = (float*)w; w += s.lbp;
   b.lb_x = s.lbx ? (void*)w : nullptr; w += s.lbx;
   if (g.split) {

@@ -94,8 +94,126 @@ struct TcArgs {
                                 //  1 = skip gathered-row copies, 2 = skip FWD1 epilogue stores,
                                 //  3 = no operand loads at all, 4 = 3 + no epilogue work,
                                 //  5 = 4 + no proxy fence before the MMAs, 6 = 5 + no full waits
-
+  // DW1 / DW2 side work: the a8 grad-input combine (combine.cu's sum, same order)
+  // rides on the dW kernels' epilogue warps, which wait ~130 K-stages per tile.
+  // Tokens are claimed one per warp from *cb_ctr; cb_drain: after its tiles the
+  // whole CTA finishes the remaining tokens (the last host kernel).  cb_ctr == 0: off.
+  const __nv_bfloat16* cb_part;  // dX partial rows [rows_cap, d]
+  const float* cb_dlogit;        // dlogit per padded bucket row
+  const __nv_bfloat16* cb_wr;    // w_r [G, d] (nullptr: no router term, GATE_NONE)
+  __nv_bfloat16* cb_out;         // dx [T, d]
+  int* cb_ctr;
+  int cb_k;                      // top-k (<= 32: one lane per pair)
+  int cb_drain;
 };
+
+// One warp computes 512 columns (two 256-column chunks, 16 bytes per lane each) of
+// dx[t] = sum_{j asc} dXp[prow(t,j)] + sum_{j asc} dlogit_j w_r[b_j], in the order and
+// rounding of combine_kernel<bf16, true> (combine.cu, reading c12: the partial rows
+// added one after another in ascending j, then the router term's fmas in ascending j),
+// so the two give bit-identical dx.  Loads go out eight rows x two chunks at a time.
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ void add_row8(float (&acc)[8], const uint4& q) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    acc[2 * i] += bf16lo(w[i]);
+    acc[2 * i + 1] += bf16hi(w[i]);
+  }
+}
+__device__ __forceinline__ void fma_row8(float (&acc)[8], float s, const uint4& q) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    acc[2 * i] = fmaf(s, bf16lo(w[i]), acc[2 * i]);
+    acc[2 * i + 1] = fmaf(s, bf16hi(w[i]), acc[2 * i + 1]);
+  }
+}
+constexpr int kSideCols8 = 32;  // 16-byte vectors of one side-combine unit (256 columns)
+// A warp claims whole tokens (one atomic per token) and works through the token's
+// 256-column units one at a time, so an epilogue warp can stop between two units
+// for its tile and resume the token afterwards (the claim lives in SideState).
+struct SideState {
+  int t;       // claimed token, -1: none
+  int c;       // next unit of it
+  int row;     // lane j < k: padded bucket row of pair j (< 2^31: ABI check)
+  int blk;     // lane j < k: block of pair j
+  float dl;    // lane j < k: dlogit of pair j
+};
+// Rows missing from a round of 16 load as zeros: acc is never -0 (it starts at +0 and
+// x + (-x) rounds to +0), so adding +0 -- or fma(dl, +0, acc) -- leaves it unchanged.
+__device__ __forceinline__ void side_combine_unit(const TcArgs& a, const SideState& st, int lane) {
+  const int k = a.cb_k;
+  const int d8 = a.d / 8;  // 16-byte vectors per row
+  const int c0 = st.c * kSideCols8 + lane;
+  if (c0 >= d8) return;
+  const uint4* part = reinterpret_cast<const uint4*>(a.cb_part) + c0;
+  const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll 1
+  for (int j = 0; j < k; j += 16) {  // sixteen rows in flight
+    uint4 p[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int rw = __shfl_sync(0xffffffffu, st.row, (j + u) & 31);
+      p[u] = j + u < k ? __ldg(part + (int64_t)rw * d8) : zero;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) add_row8(acc, p[u]);
+  }
+  if (a.cb_wr) {
+    const uint4* wr = reinterpret_cast<const uint4*>(a.cb_wr) + c0;
+#pragma unroll 1
+    for (int j = 0; j < k; j += 16) {
+      uint4 w[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int bj = __shfl_sync(0xffffffffu, st.blk, (j + u) & 31);
+        w[u] = j + u < k ? __ldg(wr + (int64_t)bj * d8) : zero;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) fma_row8(acc, __shfl_sync(0xffffffffu, st.dl, (j + u) & 31), w[u]);
+    }
+  }
+  reinterpret_cast<uint4*>(a.cb_out)[(int64_t)st.t * d8 + c0] =
+      make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]), pack_bf16(acc[4], acc[5]),
+                 pack_bf16(acc[6], acc[7]));
+}
+// Work through units (claiming tokens as needed) until every token is claimed and
+// the warp's own token is finished (returns true), or -- polling `poll` between
+// units -- until the barrier phase completes (returns false, the claim kept).
+// only_own: finish the claimed token, claim nothing new.
+__device__ __forceinline__ bool side_combine_run(const TcArgs& a, int lane, SideState& st,
+                                                 uint64_t* poll, uint32_t parity, bool only_own = false) {
+  const int npass = (a.d / 8 + kSideCols8 - 1) / kSideCols8;
+  for (;;) {
+    if (st.t < 0) {
+      if (only_own) return true;
+      int t = 0;
+      if (lane == 0) t = atomicAdd(a.cb_ctr, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= a.T) return true;  // every token claimed
+      st.t = t;
+      st.c = 0;
+      const int k = a.cb_k;
+      if (lane < k) {
+        st.blk = a.r.topk_idx[(int64_t)t * k + lane];
+        st.row = a.r.tile_offsets[st.blk] * 128 +
+                 (a.r.pair_slot[(int64_t)t * k + lane] - a.r.block_offsets[st.blk]);
+        st.dl = a.cb_wr ? a.cb_dlogit[st.row] : 0.f;
+      } else {
+        st.blk = st.row = 0;
+        st.dl = 0.f;
+      }
+    }
+    if (poll && mbar_test(poll, parity)) return false;
+    side_combine_unit(a, st, lane);
+    if (++st.c == npass) st.t = -1;
+  }
+}
 
 // 16 warps.  warp 0: TMA tile producer; warp 1: TMEM alloc + MMA issuer;
 // warps 4-11: epilogue (two warps per TMEM lane quarter).  Row gathers use both
@@ -782,6 +900,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   uint8_t* stg_base = (uint8_t*)(((uintptr_t)(dg_xchg + 128) + 1023) & ~(uintptr_t)1023);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  SideState side{-1, 0, 0, 0, 0.f};  // DW*: grad-input combine claim of this warp
   // two accumulators alternate between tiles when both fit in TMEM
   const int n_acc = tm_nacc(a.BN, a.MH);
   constexpr bool kGather = kind_gather_a(KIND) || kind_gather_b(KIND);  // uses cp.async
@@ -1119,8 +1238,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t aphase = 0;
+    bool side_done = !(kind_gather_b(KIND) && a.cb_ctr);
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo ti = decode<KIND>(a, tile);
+      // DW*: grad-input combine units while this tile's accumulator fills
+      if (kind_gather_b(KIND) && !side_done) side_done = side_combine_run(a, lane, side, &tfull[acc], aphase);
       twait(&tfull[acc], aphase, (tr && threadIdx.x == 4 * 32) ? tr : nullptr, 2);
       tc_fence_after();
       const long long te0 = clock64();
@@ -1154,6 +1276,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       if (++acc == n_acc) { acc = 0; aphase ^= 1; }
     }
     if (KIND == K_DAT && lane == 0) bulk_wait<0>();  // dA tiles written before exit
+  }
+  // last DW host kernel: every warp of the CTA, its own role finished, takes
+  // the grad-input combine tokens nobody has claimed yet
+  if (kind_gather_b(KIND) && a.cb_ctr) {
+    __syncwarp();
+    side_combine_run(a, lane, side, nullptr, 0, !a.cb_drain);  // not the last host: own token only
   }
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[6] += (unsigned long long)(clock64() - t_start);
@@ -2276,6 +2404,21 @@ int unit_mtiles() {
 // epilogue).  SPT_FFN_DAT=1: tokens on N (N = 256, transposed dA via TMA store)
 // + da_post_kernel; measured at parity on B200 in round 1 (both ~1.7 ms at
 // LLaMA scale: the gathered-row supply, not the MMA shape, bounds a7).
+// SPT_FFN_SIDE=1 (opt-in): dX first, then the grad-input combine as side work of
+// the dW kernels' epilogue warps.  Measured slower (LLaMA-scale 10.72-10.85 vs
+// 10.29-10.41 ms): four warps per SM claim only 15 % of the tokens during dW1
+// (latency-bound at ~3 us per dependent round under the GEMM's load) while
+// slowing it 12 %, and the drain in dW2 streams at ~3.7 TB/s, below the
+// stand-alone kernel's 6.4 TB/s.  Default: the stand-alone combine kernel.
+static bool side_combine_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_SIDE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static bool use_fused_da() {
   static int v = -1;
   if (v < 0) {
@@ -2836,10 +2979,25 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   if (lo) {  // W frozen: the LoRA factor gradients dC_I, dB_O from dZ, h~ (no dW1 / dW2)
     if ((e0 = lora_bwd_grads(g, r, b, *lo, s)) != cudaSuccess) return e0;
   }
+  // The grad-input combine rides on the dW kernels (side work of their epilogue
+  // warps, tc_gemm_kernel) when dX runs before them: single-process calls (no
+  // dw_event to overlap a gradient all-reduce with), the plain bf16 path, k <= 32.
+  const bool side = side_combine_enabled() && !lo && !lb && !g.split && g.k <= 32 && !dw_ev;
+  auto set_side = [&](TcArgs& a, bool drain) {
+    if (!side) return;
+    a.cb_part = (const __nv_bfloat16*)b.part;
+    a.cb_dlogit = b.dlogit;
+    a.cb_wr = g.gate == SPT_GATE_SIGMOID ? (const __nv_bfloat16*)w_r : nullptr;
+    a.cb_out = (__nv_bfloat16*)dx;
+    a.cb_ctr = b.side_ctr;
+    a.cb_k = g.k;
+    a.cb_drain = drain ? 1 : 0;
+  };
   auto run_dw = [&]() -> cudaError_t {
     {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features: <= 2 halves, or 256-feature tiles)
       TcArgs a{};
       base_args(a, g, r);
+      set_side(a, false);
       bool ok = make_tmap_bf16_2d(&a.ta, b.dz, g.rows_cap, (uint64_t)g.mp * g.bw,
                                   (uint64_t)g.mp * g.bw, 64, kind_bk(K_DW1)) &&
                 make_tmap_bf16_2d(&a.tb, x, g.T, g.d, g.d, 64, 1);
@@ -2855,10 +3013,17 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       a.out = dw1;
       a.acc_mode = accumulate;
       TRY(launch<K_DW1>(a, g.G * a.nu * a.NT, s));
+      if (side && getenv("SPT_FFN_SIDE_DEBUG")) {  // diagnostics: tokens claimed during dW1
+        int n = 0;
+        cudaMemcpyAsync(&n, b.side_ctr, 4, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[spt-side] tokens claimed during dW1: %d of %lld\n", n, (long long)g.T);
+      }
     }
     {  // a9: dW2_b = H~_b^T dY[bucket_b]
       TcArgs a{};
       base_args(a, g, r);
+      set_side(a, true);
       bool ok = make_tmap_bf16_2d(&a.ta, b.h, g.rows_cap, g.bw, g.bw, 64, kind_bk(K_DW2)) &&
                 make_tmap_bf16_2d(&a.tb, dy, g.T, g.d, g.d, 64, 1);
       if (g.split) {
@@ -2914,6 +3079,15 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     return cudaSuccess;
   };
   cudaError_t e;
+  if (side) {  // dX partials, then dW1 / dW2 (+ the combine as their side work), dW_R
+    if ((e = run_dx()) != cudaSuccess) return e;
+    if (cudaMemsetAsync(b.side_ctr, 0, 4, s) != cudaSuccess) return cudaErrorUnknown;
+    if ((e = run_dw()) != cudaSuccess) return e;
+    if ((e = run_dwr()) != cudaSuccess) return e;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (dgate_out) return launch_gather_dgate(g, r, b.dgate, dgate_out, s);
+    return cudaSuccess;
+  }
   if (!lo && (e = run_dw()) != cudaSuccess) return e;
   if ((e = run_dwr()) != cudaSuccess) return e;
   // all of dw1 | dw2 | dw_r are final here: a data-parallel caller can start the
