@@ -105,6 +105,7 @@ struct TcArgs {
   int* cb_ctr;
   int cb_k;                      // top-k (<= 32: one lane per pair)
   int cb_drain;
+  int dat_fused;                 // DAT: dgate / dZ / dlogit epilogue in-kernel (no da_post pass)
 };
 
 // One warp computes 512 columns (two 256-column chunks, 16 bytes per lane each) of
@@ -497,10 +498,14 @@ __device__ __forceinline__ float bf16_at(uint32_t w, int i) {
 // sh (FWD1 of the fused FWD1 -> FWD2 kernel): also write this row's H~ units
 // into the K-major, 128-byte-swizzled smem A tile of the second GEMM
 // (k-block u / 64 at +16 KB, row at +128 B, 16-byte chunk ((u % 64) / 8) ^ (row & 7)).
-template <int KIND, bool kSplit = false>
+// ACT >= 0 (FWD1 / DA): the activation fixed at compile time (no per-element
+// dispatch; m' = 2 exactly for SwiGLU); -1: a.act / a.mp at run time
+template <int KIND, bool kSplit = false, int ACT = -1>
 __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, uint32_t tacc,
                                          int row, int half, float* dg_xchg, uint8_t* sh = nullptr) {
   const bool valid = row < ti.n_valid;
+  const int act = ACT >= 0 ? ACT : a.act;
+  const int mp = ACT >= 0 ? (ACT == SPT_ACT_SWIGLU ? 2 : 1) : a.mp;
   if (KIND == K_ROUTER) {
     const int64_t t = ti.prow0 + row;
     for (int c0 = half * 16; c0 < a.gpad; c0 += 32) {
@@ -521,14 +526,14 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     // this tile's units [ub, ub + nut) of the block: TMEM columns u (gate) and
     // bn_u + u (up); Z stash row = [gate bw | up bw], H row = [bw]
     const int ub = ti.ut * a.bn_u, nut = min(a.bn_u, a.bw - ub);
-    __nv_bfloat16* zr = (__nv_bfloat16*)a.out + prow * (int64_t)(a.mp * a.bw) + ub;
+    __nv_bfloat16* zr = (__nv_bfloat16*)a.out + prow * (int64_t)(mp * a.bw) + ub;
     __nv_bfloat16* hr = (__nv_bfloat16*)a.out2 + prow * (int64_t)a.bw + ub;
     const int hw = ((a.bn_u / 2) + 15) & ~15;
     const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? nut : min(nut, u_lo + hw);
     for (int u0 = u_lo; u0 < u_hi; u0 += 16) {
       uint32_t vg[16], vu[16];
       tmem_ld16(tacc + u0, vg);
-      if (a.mp == 2) tmem_ld16(tacc + a.bn_u + u0, vu);
+      if (mp == 2) tmem_ld16(tacc + a.bn_u + u0, vu);
       tmem_ld_wait();
       uint32_t pz[8], pu[8], ph[8];
       uint32_t lz[8], lu[8], lh[8];  // split: lo halves
@@ -537,14 +542,14 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         const float z0 = valid ? __uint_as_float(vg[i]) : 0.f;
         const float z1 = valid ? __uint_as_float(vg[i + 1]) : 0.f;
         float u0f = 0.f, u1f = 0.f;
-        if (a.mp == 2) {
+        if (mp == 2) {
           u0f = valid ? __uint_as_float(vu[i]) : 0.f;
           u1f = valid ? __uint_as_float(vu[i + 1]) : 0.f;
           pu[i / 2] = pack_bf16(u0f, u1f);
           if (kSplit) lu[i / 2] = pack_bf16_lo(u0f, u1f, pu[i / 2]);
         }
         pz[i / 2] = pack_bf16(z0, z1);
-        const float h0 = g * act_fwd<true>(a.act, z0, u0f), h1 = g * act_fwd<true>(a.act, z1, u1f);
+        const float h0 = g * act_fwd<true>(act, z0, u0f), h1 = g * act_fwd<true>(act, z1, u1f);
         ph[i / 2] = pack_bf16(h0, h1);
         if (kSplit) {
           lz[i / 2] = pack_bf16_lo(z0, z1, pz[i / 2]);
@@ -562,15 +567,15 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
               make_uint4(ph[4 * q], ph[4 * q + 1], ph[4 * q + 2], ph[4 * q + 3]);
       }
       if (kSplit) {  // lo halves: same row layout, separate tensors
-        uint4* zd = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out_lo + prow * (int64_t)(a.mp * a.bw) + ub + u0);
+        uint4* zd = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out_lo + prow * (int64_t)(mp * a.bw) + ub + u0);
         uint4* hd = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out2_lo + prow * (int64_t)a.bw + ub + u0);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           zd[q] = make_uint4(lz[4 * q], lz[4 * q + 1], lz[4 * q + 2], lz[4 * q + 3]);
           hd[q] = make_uint4(lh[4 * q], lh[4 * q + 1], lh[4 * q + 2], lh[4 * q + 3]);
         }
-        if (a.mp == 2) {
-          uint4* ud = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out_lo + prow * (int64_t)(a.mp * a.bw) + ub + a.bw + u0);
+        if (mp == 2) {
+          uint4* ud = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out_lo + prow * (int64_t)(mp * a.bw) + ub + a.bw + u0);
 #pragma unroll
           for (int q = 0; q < 2; ++q) ud[q] = make_uint4(lu[4 * q], lu[4 * q + 1], lu[4 * q + 2], lu[4 * q + 3]);
         }
@@ -582,7 +587,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         zd[q] = make_uint4(pz[4 * q], pz[4 * q + 1], pz[4 * q + 2], pz[4 * q + 3]);
         hd[q] = make_uint4(ph[4 * q], ph[4 * q + 1], ph[4 * q + 2], ph[4 * q + 3]);
       }
-      if (a.mp == 2) {
+      if (mp == 2) {
         uint4* ud = reinterpret_cast<uint4*>(zr + a.bw + u0);
 #pragma unroll
         for (int q = 0; q < 2; ++q) ud[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
@@ -614,11 +619,11 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
     const int64_t prow = ti.prow0 + row;
     const float g = valid ? a.r.bucket_gate[ti.pos0 + row] : 0.f;
     const int ub = ti.ut * a.bn_u, nut = min(a.bn_u, a.bw - ub);  // this tile's units
-    const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + prow * (int64_t)(a.mp * a.bw) + ub;
-    __nv_bfloat16* dzr = (__nv_bfloat16*)a.out2 + prow * (int64_t)(a.mp * a.bw) + ub;
+    const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + prow * (int64_t)(mp * a.bw) + ub;
+    __nv_bfloat16* dzr = (__nv_bfloat16*)a.out2 + prow * (int64_t)(mp * a.bw) + ub;
     // split: lo halves of the Z stash / dZ rows (same layout)
-    const __nv_bfloat16* zrl = (const __nv_bfloat16*)a.aux_lo + prow * (int64_t)(a.mp * a.bw) + ub;
-    __nv_bfloat16* dzrl = (__nv_bfloat16*)a.out2_lo + prow * (int64_t)(a.mp * a.bw) + ub;
+    const __nv_bfloat16* zrl = (const __nv_bfloat16*)a.aux_lo + prow * (int64_t)(mp * a.bw) + ub;
+    __nv_bfloat16* dzrl = (__nv_bfloat16*)a.out2_lo + prow * (int64_t)(mp * a.bw) + ub;
     const int hw = ((a.bn_u / 2) + 15) & ~15;
     const int u_lo = half < 0 ? 0 : half * hw, u_hi = half < 0 ? nut : min(nut, u_lo + hw);
     float dgate = 0.f;
@@ -635,10 +640,10 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
           }
         };
         ld8(zr + u0, zg4);
-        if (a.mp == 2) ld8(zr + a.bw + u0, zu4);
+        if (mp == 2) ld8(zr + a.bw + u0, zu4);
         if (kSplit) {
           ld8(zrl + u0, zgl);
-          if (a.mp == 2) ld8(zrl + a.bw + u0, zul);
+          if (mp == 2) ld8(zrl + a.bw + u0, zul);
         }
       }
       uint32_t v[16];
@@ -652,13 +657,13 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
           dA = __uint_as_float(v[i]);
           zg = bf16_at(zg4[i / 2], i);
           if (kSplit) zg += bf16_at(zgl[i / 2], i);
-          if (a.mp == 2) {
+          if (mp == 2) {
             zu = bf16_at(zu4[i / 2], i);
             if (kSplit) zu += bf16_at(zul[i / 2], i);
           }
         }
         float av, dg, du;
-        act_fwd_bwd<true>(a.act, zg, zu, av, dg, du);
+        act_fwd_bwd<true>(act, zg, zu, av, dg, du);
         dgate = fmaf(dA, av, dgate);
         const float dzg = g * dA * dg, dzu = g * dA * du;
         const uint32_t bg = __bfloat16_as_ushort(__float2bfloat16(dzg));
@@ -675,7 +680,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
       uint4* d4 = reinterpret_cast<uint4*>(dzr + u0);
 #pragma unroll
       for (int q = 0; q < 2; ++q) d4[q] = make_uint4(pg[4 * q], pg[4 * q + 1], pg[4 * q + 2], pg[4 * q + 3]);
-      if (a.mp == 2) {
+      if (mp == 2) {
         uint4* u4 = reinterpret_cast<uint4*>(dzr + a.bw + u0);
 #pragma unroll
         for (int q = 0; q < 2; ++q) u4[q] = make_uint4(pu[4 * q], pu[4 * q + 1], pu[4 * q + 2], pu[4 * q + 3]);
@@ -684,7 +689,7 @@ __device__ __forceinline__ void epilogue(const TcArgs& a, const TileInfo& ti, ui
         uint4* l4 = reinterpret_cast<uint4*>(dzrl + u0);
 #pragma unroll
         for (int q = 0; q < 2; ++q) l4[q] = make_uint4(lg[4 * q], lg[4 * q + 1], lg[4 * q + 2], lg[4 * q + 3]);
-        if (a.mp == 2) {
+        if (mp == 2) {
           uint4* m4 = reinterpret_cast<uint4*>(dzrl + a.bw + u0);
 #pragma unroll
           for (int q = 0; q < 2; ++q) m4[q] = make_uint4(lu[4 * q], lu[4 * q + 1], lu[4 * q + 2], lu[4 * q + 3]);
@@ -839,6 +844,105 @@ __device__ __forceinline__ void epilogue_dat(const TcArgs& a, const TileInfo& ti
       bulk_commit();
     }
   }
+}
+
+// DAT fused epilogue (a7 with tokens on N; Alg. 4 line 10's dgate and the dZ of
+// the activation, as the DA epilogue computes them): TMEM lane = unit u = 32 q +
+// lane of the block, column = token row of the pair tile; this warp owns the 128
+// rows of `half`.  Per 16 rows: the Z stash values of (row, u) are loaded before
+// the TMEM load, dZ(row, u) is written at once (64-byte warp segments), and the
+// per-row dgate partials dA * act(z) are summed over the warp's 32 units by a
+// reduce-scatter (16 shuffles for 16 rows); the four unit quarters meet in smem
+// (xq) and are added in ascending q, after which each warp finishes 32 rows:
+// dgate, dlogit = dgate g (1 - g), the dense dlogits (hi | lo).  Rows past the
+// block's n_b get zero dZ / dgate / dlogit up to its padded end (rows_pad).
+template <int ACT>
+__device__ __forceinline__ void epilogue_dat_fused(const TcArgs& a, const TileInfo& ti,
+                                                   uint32_t tacc, int q, int lane, int half,
+                                                   float* xchg) {
+  constexpr bool kGlu = ACT == SPT_ACT_SWIGLU;  // m' = 2: Z / dZ rows hold gate | up
+  const int u = q * 32 + lane;
+  const bool ulive = u < a.bw;
+  const int zs = (kGlu ? 2 : 1) * a.bw;  // Z / dZ row stride (elements)
+  float* xq = xchg + half * 512;  // [4 quarters][128 rows] partial dgate of this half
+  const int r_lo = half * 128;
+  for (int c0 = r_lo; c0 < r_lo + 128; c0 += 16) {
+    if (c0 >= ti.rows_pad) break;  // uniform over the half's four warps
+    const int nv = ulive ? ti.n_valid - c0 : 0;   // rows j < nv are real
+    const int np = ulive ? ti.rows_pad - c0 : 0;  // rows j < np get dZ (zeros past nv)
+    const float gl = (lane < 16 && c0 + lane < ti.n_valid) ? a.r.bucket_gate[ti.pos0 + c0 + lane] : 0.f;
+    const __nv_bfloat16* zrow = (const __nv_bfloat16*)a.aux + (ti.prow0 + c0) * (int64_t)zs + u;
+    __nv_bfloat16* dzrow = (__nv_bfloat16*)a.out2 + (ti.prow0 + c0) * (int64_t)zs + u;
+    uint32_t zg[16], zu[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      zg[j] = j < nv ? (uint32_t)__bfloat16_as_ushort(zrow[j * zs]) : 0u;
+      if (kGlu) zu[j] = j < nv ? (uint32_t)__bfloat16_as_ushort(zrow[j * zs + a.bw]) : 0u;
+    }
+    uint32_t v[16];
+    tmem_ld16(tacc + c0, v);
+    tmem_ld_wait();
+    float p[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float dA = j < nv ? __uint_as_float(v[j]) : 0.f;
+      const float g = __shfl_sync(0xffffffffu, gl, j);
+      float av, dg, du;
+      act_fwd_bwd<true>(ACT, __uint_as_float(zg[j] << 16), kGlu ? __uint_as_float(zu[j] << 16) : 0.f,
+                        av, dg, du);
+      p[j] = dA * av;
+      if (j < np) {
+        dzrow[j * zs] = __float2bfloat16(g * dA * dg);
+        if (kGlu) dzrow[j * zs + a.bw] = __float2bfloat16(g * dA * du);
+      }
+    }
+    // reduce-scatter of p[0..16) over the 32 lanes: offsets 16, 8, 4, 2 halve the
+    // values each lane keeps, a final xor-1 add completes them
+    float h8[8], h4[4], h2[2];
+    {
+      const bool up = lane & 16;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        h8[i] = (up ? p[i + 8] : p[i]) + __shfl_xor_sync(0xffffffffu, up ? p[i] : p[i + 8], 16);
+    }
+    {
+      const bool up = lane & 8;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        h4[i] = (up ? h8[i + 4] : h8[i]) + __shfl_xor_sync(0xffffffffu, up ? h8[i] : h8[i + 4], 8);
+    }
+    {
+      const bool up = lane & 4;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        h2[i] = (up ? h4[i + 2] : h4[i]) + __shfl_xor_sync(0xffffffffu, up ? h4[i] : h4[i + 2], 4);
+    }
+    const bool up2 = lane & 2;
+    float h1 = (up2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, up2 ? h2[0] : h2[1], 2);
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+    const int jrow = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    if ((lane & 1) == 0) xq[q * 128 + (c0 - r_lo) + jrow] = h1;
+  }
+  asm volatile("bar.sync %0, 128;" ::"r"(5 + half) : "memory");
+  const int rr = r_lo + q * 32 + lane;  // this thread finishes row rr of the pair tile
+  if (rr < ti.rows_pad) {
+    const int i = rr - r_lo;
+    const bool valid = rr < ti.n_valid;
+    const float dgate = valid ? ((xq[i] + xq[128 + i]) + xq[256 + i]) + xq[384 + i] : 0.f;
+    const int64_t prow = ti.prow0 + rr;
+    float dlogit = 0.f;
+    if (valid && a.gate == SPT_GATE_SIGMOID) {
+      const int64_t t = a.r.bucket_token[ti.pos0 + rr];
+      dlogit = dgate * sigmoid_pair(a.r.logits[t * a.G + ti.b]);
+      __nv_bfloat16* dl = (__nv_bfloat16*)a.dlg;
+      const __nv_bfloat16 hi = __float2bfloat16(dlogit);
+      dl[t * a.gpad + ti.b] = hi;
+      dl[(a.T + t) * a.gpad + ti.b] = __float2bfloat16(dlogit - __bfloat162float(hi));
+    }
+    a.rows_f[prow] = dgate;
+    a.rows_g[prow] = dlogit;
+  }
+  asm volatile("bar.sync %0, 128;" ::"r"(5 + half) : "memory");  // xq reuse by the next tile
 }
 
 // One K stage (4 x K=16) of MMAs into MH accumulator halves: descriptors are
@@ -1048,7 +1152,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         const int r = 4 * c + i;
         rr[i] = (has_call && r < ti.n_valid) ? a.r.bucket_token[ti.pos0 + r] : (int)a.T;
       }
-      if (KIND == K_DA) {
+      if (KIND == K_DA || (KIND == K_DAT && a.dat_fused)) {
         // the epilogue reads this tile's Z stash rows (m'*bw bf16 each, written by
         // the forward and long evicted): warm L2 now, a whole mainloop ahead
         const int zrow = a.mp * a.bw * 2;
@@ -1257,6 +1361,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         th.pos0 += half * 128;
         if (half * 128 < ti.rows_pad)  // the second m-tile may not exist: write nothing
           epilogue<KIND, kSplit>(a, th, tmem + lanes + tm_col(a.BN, a.MH, acc, half), row, -1, dg_xchg);
+      } else if (KIND == K_DAT && a.dat_fused) {
+        const uint32_t tacc = tmem + lanes + tm_col(a.BN, a.MH, acc, 0);
+        float* xchg = reinterpret_cast<float*>(stg_base);
+        if (a.act == SPT_ACT_SWIGLU) epilogue_dat_fused<SPT_ACT_SWIGLU>(a, ti, tacc, q, lane, half, xchg);
+        else if (a.act == SPT_ACT_GELU) epilogue_dat_fused<SPT_ACT_GELU>(a, ti, tacc, q, lane, half, xchg);
+        else epilogue_dat_fused<SPT_ACT_RELU>(a, ti, tacc, q, lane, half, xchg);
       } else if (KIND == K_DAT) {
         epilogue_dat(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, 0), q, lane, half,
                      stg_base + e * 4096);
@@ -1491,8 +1601,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       twait(&tfull[acc], aphase, (tr && threadIdx.x == 4 * 32) ? tr : nullptr, 2);
       tc_fence_after();
       const long long te0 = clock64();
-      if (ti.rows_pad > 0)  // the pair's second m-tile may not exist: write nothing
-        epilogue<KIND>(a, ti, tmem + ((uint32_t)(q * 32) << 16) + acc * 256, row, half, dg_xchg);
+      if (ti.rows_pad > 0) {  // the pair's second m-tile may not exist: write nothing
+        const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + acc * 256;
+        // (compile-time activation variants of this call measured neutral at
+        // every config: the epilogue is hidden behind the mainloop)
+        epilogue<KIND>(a, ti, tacc, row, half, dg_xchg);
+      }
       tc_fence_before();
       __syncwarp();
       if (tr && threadIdx.x == 4 * 32) tr[3] += (unsigned long long)(clock64() - te0);
@@ -2419,14 +2533,18 @@ static bool side_combine_enabled() {
   return v == 1;
 }
 
-static bool use_fused_da() {
+// SPT_FFN_DAT: 0 = a7 with tokens on M (N = bw) and the fused epilogue; 1 = tokens on N
+// (N = 256) with the dA tile stored and da_post_kernel; 2 = tokens on N with the
+// fused epilogue (epilogue_dat_fused)
+static int dat_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SPT_FFN_DAT");
-    v = (e && e[0] == '1') ? 0 : 1;
+    v = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
   }
-  return v == 1;
+  return v;
 }
+static bool use_fused_da() { return dat_mode() == 0; }
 
 bool tc_supported(const Geom& g) {
   if (g.d % 64) return false;
@@ -2922,6 +3040,15 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.aux2 = dy_da;
     a.tile_list = b.tile_list;
     a.unit_offsets = b.unit_offsets;
+    if (dat_mode() == 2) {  // dgate / dZ / dlogit in the GEMM's epilogue
+      a.dat_fused = 1;
+      a.aux = b.z;
+      a.out2 = b.dz;
+      a.rows_f = b.dgate;
+      a.rows_g = b.dlogit;
+      a.dlg = b.dlg;
+      TRY(launch<K_DAT>(a, up / 2 + g.G, s));
+    } else {
     TRY(launch<K_DAT>(a, up / 2 + g.G, s));
     prof_begin("da_post", s);
     da_post_kernel<<<(unsigned)ceil_div(g.rows_cap, 32), 256, 0, s>>>(
@@ -2929,6 +3056,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
         (__nv_bfloat16*)b.dz, b.dgate, b.dlogit, (__nv_bfloat16*)b.dlg);
     prof_end(s);
     count_launch();
+    }
   } else {  // a7 fused variant: dA = dY[bucket] W2_b^T with the dgate / dZ / dlogit epilogue
     TcArgs a{};
     base_args(a, gda, r);

@@ -1,6 +1,7 @@
 """GPU parity of the library's alternative kernel paths (selected by environment
 knobs read once per process, so each case runs in its own interpreter):
   SPT_FFN_DAT=1       a7 with tokens on N + da_post_kernel
+  SPT_FFN_DAT=2       a7 with tokens on N, dgate / dZ / dlogit in the GEMM epilogue
   SPT_FFN_PREFETCH=1  L2 prefetch of gathered rows
   SPT_FFN_PAIR=1|0    CTA-pair (cta_group::2) weight-resident kernel for FWD2 + dX / neither (default: dX only)
   SPT_FFN_PAIR_GATHER=0  1-CTA FWD1 / dA kernel (default: CTA-pair gather kernel)
@@ -35,7 +36,7 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"}, {"SPT_FFN_PAIR": "0"},
+@pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_DAT": "2"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"}, {"SPT_FFN_PAIR": "0"},
                                  {"SPT_FFN_PAIR_GATHER": "0"}, {"SPT_FFN_SIMT": "1"}, {"SPT_FFN_PDL": "1"}, {"SPT_FFN_MLP": "1"}])
 def test_variant_parity(env):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
@@ -51,5 +52,18 @@ def test_fused_fwd1_fwd2_many_tiles():
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests")).replace(
         'for name, T in (("bert", 700), ("llama", 300), ("tiny", 333)):', 'for name, T in (("llama", 3001),):')
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "SPT_FFN_MLP": "1"},
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("dat", ["1", "2"])
+def test_dat_many_tiles(dat):
+    """Tokens-on-N a7 at T where every CTA runs several pair tiles (both TMEM
+    buffers, the cross-warp dgate exchange reused tile after tile), ragged bucket
+    ends, bw = 96 (bert: unit quarter 3 idle) and bw = 128 SwiGLU (llama)."""
+    code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests")).replace(
+        'for name, T in (("bert", 700), ("llama", 300), ("tiny", 333)):',
+        'for name, T in (("llama", 3001), ("bert", 5003), ("opt", 2222)):')
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "SPT_FFN_DAT": dat},
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
