@@ -106,6 +106,7 @@ struct TcArgs {
   int cb_k;                      // top-k (<= 32: one lane per pair)
   int cb_drain;
   int dat_fused;                 // DAT: dgate / dZ / dlogit epilogue in-kernel (no da_post pass)
+  int dw_ng;                     // DW*: N tiles per raster group (SPT_FFN_DW_NG; NT = block-major)
 };
 
 // One warp computes 512 columns (two 256-column chunks, 16 bytes per lane each) of
@@ -345,9 +346,15 @@ __device__ __forceinline__ TileInfo decode(const TcArgs& a, int tile) {
     ti.n_valid = (int)(a.T - ti.prow0 < 128 ? a.T - ti.prow0 : 128);
     ti.nkb = 2 * (a.gpad / 64 + (a.gpad % 64 ? 1 : 0));
   } else if (KIND == K_DW1 || KIND == K_DW2) {
-    ti.nt = tile % a.NT;
-    ti.ut = (tile / a.NT) % a.nu;
-    ti.b = tile / a.NT / a.nu;
+    // raster: groups of dw_ng N tiles; inside a group (block, unit tile, N tile)
+    // order, so one wave of CTAs covers ~SMs / dw_ng blocks x dw_ng N tiles
+    const int per = a.dw_ng * a.G * a.nu;
+    const int grp = tile / per;
+    const int r = tile - grp * per;
+    const int sz = min(a.dw_ng, a.NT - grp * a.dw_ng);
+    ti.nt = grp * a.dw_ng + r % sz;
+    ti.ut = (r / sz) % a.nu;
+    ti.b = r / sz / a.nu;
     ti.pos0 = a.r.block_offsets[ti.b];
     ti.n_valid = a.r.block_offsets[ti.b + 1] - a.r.block_offsets[ti.b];  // bucket size n_b
     ti.kbase = (int64_t)a.r.tile_offsets[ti.b] * 128;
@@ -2469,6 +2476,23 @@ static cudaError_t launch_bres(TcArgs& a, int units_upper, cudaStream_t s) {
   return launch<KIND>(a, units_upper, s);
 }
 
+// N tiles per dW raster group.  Every CTA of a wave streams its block's bucket
+// rows in token order, so the wave re-reads from DRAM about |union of its blocks'
+// tokens| x (its distinct N tiles) x 512 B of gathered rows plus (its distinct
+// blocks) x the blocks' dZ / H~ rows: block-major order (all NT N tiles of ~9
+// blocks per wave at LLaMA scale) over-weights the first term.  Measured
+// (LLaMA scale): dW1 1.55 -> 1.44 ms at 8 N tiles per group (~18 blocks per
+// wave), 1.42-1.46 at 4 / 2; dW2 (bw-wide A, half dW1's dZ bytes) 1.17 at 16 and 8,
+// 1.20-1.23 at 4 / 2.  Default: dW1 8, dW2 block-major; SPT_FFN_DW_NG overrides both.
+static int dw_group(int NT, int kind) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_DW_NG");
+    v = e ? atoi(e) : 0;
+  }
+  const int ng = v >= 1 ? v : (kind == K_DW1 ? 8 : NT);
+  return ng < NT ? ng : NT;
+}
 static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
   a.r = r;
   a.T = g.T;
@@ -3137,6 +3161,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       a.BN = 256;
       a.MH = (int)std::min<int64_t>(2, ceil_div(g.mp * g.bw, 128));
       a.nu = (int)ceil_div(g.mp * g.bw, 256);
+      a.dw_ng = dw_group(a.NT, K_DW1);
       a.aux2 = x;
       a.out = dw1;
       a.acc_mode = accumulate;
@@ -3162,6 +3187,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       a.BN = 256;
       a.MH = (int)std::min<int64_t>(2, ceil_div(g.bw, 128));
       a.nu = (int)ceil_div(g.bw, 256);
+      a.dw_ng = dw_group(a.NT, K_DW2);
       a.aux2 = dy;
       a.out = dw2;
       a.acc_mode = accumulate;
