@@ -107,6 +107,7 @@ struct TcArgs {
   int cb_drain;
   int dat_fused;                 // DAT: dgate / dZ / dlogit epilogue in-kernel (no da_post pass)
   int dw_ng;                     // DW*: N tiles per raster group (SPT_FFN_DW_NG; NT = block-major)
+  int pair_rows;                 // tc_pair_gather_kernel: rows per CTA stage by TMA gather4 (rest cp.async)
 };
 
 // One warp computes 512 columns (two 256-column chunks, 16 bytes per lane each) of
@@ -1481,7 +1482,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // --------- TMA gather4 of rows [0, kPairRows); warp 0 lane 0 also loads B
     const int p = warp == 0 ? 0 : warp - 1;
     const int c = lane * kTmaGatherWarps + p;
-    constexpr int n_calls = kPairRows / 4;
+    const int n_calls = a.pair_rows / 4;
     const bool has_call = c < n_calls;
     const int my_calls = n_calls > p ? (n_calls - p + kTmaGatherWarps - 1) / kTmaGatherWarps : 0;
     const uint32_t tx = (uint32_t)my_calls * 512u + (p == 0 ? (uint32_t)nh * 128u : 0u);
@@ -1515,11 +1516,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 12) {
-    // ------------------------------- cp.async of rows [kPairRows, 128)
+    // ------------------------------- cp.async of rows [pair_rows, 128)
     const int t = threadIdx.x - 12 * 32;  // 0..127
     const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
     const int ch = t & 7;
-    constexpr int kRowsPer = (128 - kPairRows) * 8 / kCpThreadsA;  // 4
+    const int pr = a.pair_rows;
+    constexpr int kRowsPer = 8;  // upper bound (pair_rows = 0); rows pr + (t >> 3) + 16 i < 128
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = cid; tile < ntiles; tile += ncl) {
@@ -1527,8 +1529,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int tok[kRowsPer];
 #pragma unroll
       for (int i = 0; i < kRowsPer; ++i) {
-        const int r = kPairRows + (t >> 3) + 16 * i;
-        tok[i] = r < ti.n_valid ? a.r.bucket_token[ti.pos0 + r] : -1;
+        const int r = pr + (t >> 3) + 16 * i;
+        tok[i] = (r < 128 && r < ti.n_valid) ? a.r.bucket_token[ti.pos0 + r] : -1;
       }
       for (int kb = 0; kb < ti.nkb; ++kb) {
         if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
@@ -1536,7 +1538,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t sA = smem_u32(smem + stage * kPairStage);
 #pragma unroll
         for (int i = 0; i < kRowsPer; ++i) {
-          const int r = kPairRows + (t >> 3) + 16 * i;
+          const int r = pr + (t >> 3) + 16 * i;
+          if (r >= 128) break;
           const uint32_t dst = sA + r * 128 + ((ch ^ (r & 7)) << 4);
           const __nv_bfloat16* g = src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kb * 64 + ch * 8;
           cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
@@ -2387,8 +2390,26 @@ static bool pair_gather_ok(int BN) {
   return (BN > 128 || (BN == 128 && pair128())) && BN <= 256 && BN % 32 == 0;
 }
 
+// rows of each 128-row CTA stage gathered by TMA gather4 (multiple of 4; the rest
+// by the four cp.async warps).  Measured at LLaMA scale (FWD1 / dA ms): 32 rows
+// 1.37 / 1.39, 40 1.38, 48 1.32-1.34 / 1.39-1.42, 56 1.38, 64 1.43-1.44 / 1.39-1.41,
+// 80 1.49, 96 1.56, 128 1.82 / 1.37 -- FWD1 (N = 256: half the gathered bytes per
+// MMA clock of dA) is best with the cp.async warps taking 80 of 128 rows; dA does
+// not move (its bound is not the gather engines).  Default FWD1 48, dA 64;
+// SPT_FFN_PAIR_ROWS overrides both.
+static int pair_tma_rows(int kind) {
+  static int v = -2;  // -2: not read yet, -1: default
+  if (v == -2) {
+    const char* e = getenv("SPT_FFN_PAIR_ROWS");
+    v = e ? atoi(e) : -1;
+    if (v < 0 || v > 128 || v % 4) v = -1;
+  }
+  if (v >= 0) return v;
+  return kind == K_FWD1 ? 48 : kPairRows;
+}
 template <int KIND>
 static cudaError_t launch_pair_gather(TcArgs& a, int tiles_upper, cudaStream_t s) {
+  a.pair_rows = pair_tma_rows(KIND);
   const int stages = std::min(7, (227 * 1024 - 2048) / kPairStage);
   const int smem = stages * kPairStage + 2048;
   static std::atomic<bool> attr_set[kMaxDev];

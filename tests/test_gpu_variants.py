@@ -9,6 +9,7 @@ knobs read once per process, so each case runs in its own interpreter):
   SPT_FFN_PDL=1       programmatic dependent launch of the hot-path kernels
   SPT_FFN_MLP=1       fused FWD1 -> FWD2 CTA-pair kernel (SwiGLU, bw = 128)
   SPT_FFN_DW_NG=3|5   dW raster groups of 3 / 5 N tiles (d = 4096: a ragged last group)
+  SPT_FFN_PAIR_ROWS=0|128|20  pair FWD1 / dA stages gathered all by cp.async / all by TMA / a 5-call TMA split
 """
 import os
 import subprocess
@@ -39,7 +40,9 @@ print("ok")
 
 @pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_DAT": "2"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"}, {"SPT_FFN_PAIR": "0"},
                                  {"SPT_FFN_PAIR_GATHER": "0"}, {"SPT_FFN_SIMT": "1"}, {"SPT_FFN_PDL": "1"}, {"SPT_FFN_MLP": "1"},
-                                 {"SPT_FFN_DW_NG": "3"}, {"SPT_FFN_DW_NG": "5"}])
+                                 {"SPT_FFN_DW_NG": "3"}, {"SPT_FFN_DW_NG": "5"},
+                                 {"SPT_FFN_PAIR_ROWS": "0"}, {"SPT_FFN_PAIR_ROWS": "128"},
+                                 {"SPT_FFN_PAIR_ROWS": "20"}])
 def test_variant_parity(env):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True,
