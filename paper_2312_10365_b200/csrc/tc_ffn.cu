@@ -108,6 +108,8 @@ struct TcArgs {
   int dat_fused;                 // DAT: dgate / dZ / dlogit epilogue in-kernel (no da_post pass)
   int dw_ng;                     // DW*: N tiles per raster group (SPT_FFN_DW_NG; NT = block-major)
   int pair_rows;                 // tc_pair_gather_kernel: rows per CTA stage by TMA gather4 (rest cp.async)
+  int mma_batch;                 // tc_pair_gather_kernel: K stages per MMA-issuer wait round (1 or 2)
+  int g1_rows;                   // tc_gemm_kernel FWD1 / DA / DAT: rows of a 256-row stage by TMA gather4 (32..256)
 };
 
 // One warp computes 512 columns (two 256-column chunks, 16 bytes per lane each) of
@@ -229,7 +231,7 @@ __device__ __forceinline__ bool side_combine_run(const TcArgs& a, int lane, Side
 constexpr int kThreads = 512;
 constexpr int kEpiWarps = 8;                  // warps 4..11
 constexpr int kTmaGatherWarps = 3;            // FWD1 / DA: warps 0, 2, 3
-constexpr int kTmaRows = 128;                 // FWD1 / DA: rows per stage gathered by TMA
+constexpr int kTmaRows = 128;                 // (round-1 split; now a.g1_rows, default 64)
 constexpr int kCpThreadsA = 128;              // FWD1 / DA: cp.async warps 12..15
 // DW*: cp.async warps 2, 3, 8..15 (10 warps).  The dW tiles run ~130 K stages per
 // epilogue, so warps 8..11 gather instead of waiting as epilogue warps: the B rows
@@ -953,6 +955,96 @@ __device__ __forceinline__ void epilogue_dat_fused(const TcArgs& a, const TileIn
   asm volatile("bar.sync %0, 128;" ::"r"(5 + half) : "memory");  // xq reuse by the next tile
 }
 
+// DAT fused epilogue, row-major form: each 32-unit x 16-row TMEM chunk is
+// transposed through a per-warp smem tile (16 x 33 floats, conflict-free), after
+// which lane l works on row l / 2 and units 16 (l % 2) .. +16 of the warp's
+// quarter -- 16-byte Z loads and dZ stores, a thread-local rowdot finished by one
+// xor-1 shuffle -- instead of one 2-byte access per (row, unit) (measured 1.62
+// vs 1.40 ms for the tokens-on-M dA).  Same outputs as epilogue_dat_fused.
+template <int ACT>
+__device__ __forceinline__ void epilogue_dat_rows(const TcArgs& a, const TileInfo& ti,
+                                                  uint32_t tacc, int q, int lane, int half,
+                                                  float* xchg, float* tbuf) {
+  constexpr bool kGlu = ACT == SPT_ACT_SWIGLU;
+  const int zs = (kGlu ? 2 : 1) * a.bw;
+  float* xq = xchg + half * 512;
+  const int r_lo = half * 128;
+  const int jr = lane >> 1, uh = lane & 1;
+  const int u0 = q * 32 + uh * 16;            // this lane's 16 units
+  const bool ulive = u0 < a.bw;               // bw % 16 == 0: all 16 or none
+  for (int c0 = r_lo; c0 < r_lo + 128; c0 += 16) {
+    if (c0 >= ti.rows_pad) break;  // uniform over the half's four warps
+    const int r = c0 + jr;
+    const bool valid = ulive && r < ti.n_valid;
+    const bool write = ulive && r < ti.rows_pad;
+    // Z stash loads first (their latency overlaps the TMEM load and the transpose)
+    uint4 zg4[2], zu4[2];
+    const __nv_bfloat16* zr = (const __nv_bfloat16*)a.aux + (ti.prow0 + r) * (int64_t)zs + u0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      zg4[h] = valid ? reinterpret_cast<const uint4*>(zr)[h] : make_uint4(0u, 0u, 0u, 0u);
+      zu4[h] = (kGlu && valid) ? reinterpret_cast<const uint4*>(zr + a.bw)[h] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    const float g = valid ? a.r.bucket_gate[ti.pos0 + r] : 0.f;
+    uint32_t v[16];
+    tmem_ld16(tacc + c0, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) tbuf[j * 33 + lane] = __uint_as_float(v[j]);  // [row j][unit lane]
+    __syncwarp();
+    float dA[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dA[i] = valid ? tbuf[jr * 33 + uh * 16 + i] : 0.f;
+    __syncwarp();  // tbuf reuse by the next chunk
+    const uint32_t zgw[8] = {zg4[0].x, zg4[0].y, zg4[0].z, zg4[0].w, zg4[1].x, zg4[1].y, zg4[1].z, zg4[1].w};
+    const uint32_t zuw[8] = {zu4[0].x, zu4[0].y, zu4[0].z, zu4[0].w, zu4[1].x, zu4[1].y, zu4[1].z, zu4[1].w};
+    uint32_t pg[8], pu[8];
+    float p = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      float av0, dg0, du0, av1, dg1, du1;
+      act_fwd_bwd<true>(ACT, bf16_at(zgw[i / 2], 0), kGlu ? bf16_at(zuw[i / 2], 0) : 0.f, av0, dg0, du0);
+      act_fwd_bwd<true>(ACT, bf16_at(zgw[i / 2], 1), kGlu ? bf16_at(zuw[i / 2], 1) : 0.f, av1, dg1, du1);
+      p = fmaf(dA[i], av0, p);
+      p = fmaf(dA[i + 1], av1, p);
+      pg[i / 2] = pack_bf16(g * dA[i] * dg0, g * dA[i + 1] * dg1);
+      pu[i / 2] = pack_bf16(g * dA[i] * du0, g * dA[i + 1] * du1);
+    }
+    if (write) {
+      uint4* dzr = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out2 + (ti.prow0 + r) * (int64_t)zs + u0);
+      dzr[0] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+      dzr[1] = make_uint4(pg[4], pg[5], pg[6], pg[7]);
+      if (kGlu) {
+        uint4* dur = reinterpret_cast<uint4*>((__nv_bfloat16*)a.out2 + (ti.prow0 + r) * (int64_t)zs + a.bw + u0);
+        dur[0] = make_uint4(pu[0], pu[1], pu[2], pu[3]);
+        dur[1] = make_uint4(pu[4], pu[5], pu[6], pu[7]);
+      }
+    }
+    p += __shfl_xor_sync(0xffffffffu, p, 1);  // the warp's 32 units of row jr
+    if (uh == 0) xq[q * 128 + (c0 - r_lo) + jr] = p;
+  }
+  asm volatile("bar.sync %0, 128;" ::"r"(5 + half) : "memory");
+  const int rr = r_lo + q * 32 + lane;
+  if (rr < ti.rows_pad) {
+    const int i = rr - r_lo;
+    const bool valid = rr < ti.n_valid;
+    const float dgate = valid ? ((xq[i] + xq[128 + i]) + xq[256 + i]) + xq[384 + i] : 0.f;
+    const int64_t prow = ti.prow0 + rr;
+    float dlogit = 0.f;
+    if (valid && a.gate == SPT_GATE_SIGMOID) {
+      const int64_t t = a.r.bucket_token[ti.pos0 + rr];
+      dlogit = dgate * sigmoid_pair(a.r.logits[t * a.G + ti.b]);
+      __nv_bfloat16* dl = (__nv_bfloat16*)a.dlg;
+      const __nv_bfloat16 hi = __float2bfloat16(dlogit);
+      dl[t * a.gpad + ti.b] = hi;
+      dl[(a.T + t) * a.gpad + ti.b] = __float2bfloat16(dlogit - __bfloat162float(hi));
+    }
+    a.rows_f[prow] = dgate;
+    a.rows_g[prow] = dlogit;
+  }
+  asm volatile("bar.sync %0, 128;" ::"r"(5 + half) : "memory");  // xq reuse by the next tile
+}
+
 // One K stage (4 x K=16) of MMAs into MH accumulator halves: descriptors are
 // advanced by constant adds (start address field, 16-byte units; no carry:
 // smem offsets < 256 KB), the A half h lives 16 KB after half 0.
@@ -1145,7 +1237,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     // ------------------------ FWD1 / DA: TMA tile::gather4 of 256 token rows
     const int p = warp == 0 ? 0 : warp - 1;   // 0, 1, 2
     const int c = lane * kTmaGatherWarps + p;  // gather call of this lane: rows 4c..4c+3
-    const int n_calls = kTmaRows / 4;
+    const int n_calls = a.g1_rows / 4;  // rows [0, g1_rows) of each 256-row stage by TMA
     const bool has_call = c < n_calls;
     const int my_calls = n_calls > p ? (n_calls - p + kTmaGatherWarps - 1) / kTmaGatherWarps : 0;
     const uint32_t tx = (a.ablate == 1 || a.ablate >= 3 ? 0u : (uint32_t)my_calls * 512u) +
@@ -1212,7 +1304,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     const int t = threadIdx.x - 12 * 32;  // 0..127
     const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
     const int ch = t & 7;
-    constexpr int kRowsPer = (256 - kTmaRows) * 8 / kCpThreadsA;  // rows per thread (8)
+    constexpr int kRowsPer = 14;  // upper bound: g1_rows >= 32
+    const int r0 = a.g1_rows;
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -1220,8 +1313,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       int tok[kRowsPer];
 #pragma unroll
       for (int i = 0; i < kRowsPer; ++i) {
-        const int r = kTmaRows + (t >> 3) + 16 * i;
-        tok[i] = r < ti.n_valid ? a.r.bucket_token[ti.pos0 + r] : -1;
+        const int r = r0 + (t >> 3) + 16 * i;
+        tok[i] = (r < 256 && r < ti.n_valid) ? a.r.bucket_token[ti.pos0 + r] : -1;
       }
       for (int kb = 0; kb < ti.nkb; ++kb) {
         if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
@@ -1232,7 +1325,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 #pragma unroll
         for (int i = 0; i < kRowsPer; ++i) {
           if (a.ablate == 1 || a.ablate >= 3) break;
-          const int r = kTmaRows + (t >> 3) + 16 * i;
+          const int r = r0 + (t >> 3) + 16 * i;
+          if (r >= 256) break;
           const uint32_t dst = sA + (r >> 7) * 16384 + (r & 127) * 128 + ((ch ^ (r & 7)) << 4);
           const __nv_bfloat16* g = srcp + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kk * 64 + ch * 8;
           cp_async_16(dst, g, tok[i] < 0 ? 0u : 16u);
@@ -1372,9 +1466,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       } else if (KIND == K_DAT && a.dat_fused) {
         const uint32_t tacc = tmem + lanes + tm_col(a.BN, a.MH, acc, 0);
         float* xchg = reinterpret_cast<float*>(stg_base);
-        if (a.act == SPT_ACT_SWIGLU) epilogue_dat_fused<SPT_ACT_SWIGLU>(a, ti, tacc, q, lane, half, xchg);
-        else if (a.act == SPT_ACT_GELU) epilogue_dat_fused<SPT_ACT_GELU>(a, ti, tacc, q, lane, half, xchg);
-        else epilogue_dat_fused<SPT_ACT_RELU>(a, ti, tacc, q, lane, half, xchg);
+        float* tbuf = reinterpret_cast<float*>(stg_base + 4096) + e * (16 * 33);
+        if (a.dat_fused == 2) {
+          if (a.act == SPT_ACT_SWIGLU) epilogue_dat_fused<SPT_ACT_SWIGLU>(a, ti, tacc, q, lane, half, xchg);
+          else if (a.act == SPT_ACT_GELU) epilogue_dat_fused<SPT_ACT_GELU>(a, ti, tacc, q, lane, half, xchg);
+          else epilogue_dat_fused<SPT_ACT_RELU>(a, ti, tacc, q, lane, half, xchg);
+        } else if (a.act == SPT_ACT_SWIGLU) {
+          epilogue_dat_rows<SPT_ACT_SWIGLU>(a, ti, tacc, q, lane, half, xchg, tbuf);
+        } else if (a.act == SPT_ACT_GELU) {
+          epilogue_dat_rows<SPT_ACT_GELU>(a, ti, tacc, q, lane, half, xchg, tbuf);
+        } else {
+          epilogue_dat_rows<SPT_ACT_RELU>(a, ti, tacc, q, lane, half, xchg, tbuf);
+        }
       } else if (KIND == K_DAT) {
         epilogue_dat(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, 0), q, lane, half,
                      stg_base + e * 4096);
@@ -1563,6 +1666,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (trl) trl[7] += 1;
         const uint32_t dtm = tmem + acc * 256;
+        if (a.mma_batch == 2) {
+          // two K stages per wait / fence round: the per-stage issue overhead
+          // (barrier wait, proxy + tcgen05 fences) halves against dA's 256-clock
+          // (N = 128) stages
+          for (int kb = 0; kb < ti.nkb; kb += 2) {
+            const bool two = kb + 1 < ti.nkb;
+            const int st1 = stage + 1 == n_stages ? 0 : stage + 1;
+            const uint32_t ph1 = stage + 1 == n_stages ? phase ^ 1 : phase;
+            twait(&full[stage], phase, trl, 0);
+            if (two) twait(&full[st1], ph1, trl, 0);
+            fence_proxy_async_smem();  // this CTA's cp.async rows -> async proxy
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t s0 = (uint64_t)((stage * kPairStage) >> 4);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_pair(dtm, adesc0 + s0 + k * 2, bdesc0 + s0 + k * 2, idesc,
+                              (kb != 0 || k != 0) ? 1u : 0u);
+              mma_commit_pair(&empty[stage]);
+              if (two) {
+                const uint64_t s1 = (uint64_t)((st1 * kPairStage) >> 4);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_bf16_pair(dtm, adesc0 + s1 + k * 2, bdesc0 + s1 + k * 2, idesc, 1u);
+                mma_commit_pair(&empty[st1]);
+              }
+            }
+            __syncwarp();
+            stage = st1;
+            phase = ph1;
+            if (two && ++stage == n_stages) { stage = 0; phase ^= 1; }
+          }
+        } else {
         for (int kb = 0; kb < ti.nkb; ++kb) {
           twait(&full[stage], phase, trl, 0);
           fence_proxy_async_smem();  // this CTA's cp.async rows -> async proxy
@@ -1577,6 +1713,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
           if (++stage == n_stages) { stage = 0; phase ^= 1; }
+        }
         }
         if (elect_one()) mma_commit_pair(&tfull[acc]);
         __syncwarp();
@@ -2407,9 +2544,21 @@ static int pair_tma_rows(int kind) {
   if (v >= 0) return v;
   return kind == K_FWD1 ? 48 : kPairRows;
 }
+// K stages the pair kernel's MMA issuer consumes per wait / fence round
+// (SPT_FFN_MMA_BATCH=1|2; default 1)
+static int mma_batch(int kind) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_MMA_BATCH");
+    v = (e && e[0] == '2') ? 2 : 1;
+  }
+  (void)kind;
+  return v;
+}
 template <int KIND>
 static cudaError_t launch_pair_gather(TcArgs& a, int tiles_upper, cudaStream_t s) {
   a.pair_rows = pair_tma_rows(KIND);
+  a.mma_batch = mma_batch(KIND);
   const int stages = std::min(7, (227 * 1024 - 2048) / kPairStage);
   const int smem = stages * kPairStage + 2048;
   static std::atomic<bool> attr_set[kMaxDev];
@@ -2514,7 +2663,22 @@ static int dw_group(int NT, int kind) {
   const int ng = v >= 1 ? v : (kind == K_DW1 ? 8 : NT);
   return ng < NT ? ng : NT;
 }
+// tc_gemm_kernel gathered-row kinds: rows of each 256-row stage by TMA gather4
+// (the rest by the four cp.async warps); SPT_FFN_G1_ROWS (multiple of 4, 32..256)
+// Measured: tokens-on-N dA at LLaMA scale 1.81 / 1.54 / 1.42 / 1.28 / 1.16 / 1.15 ms
+// at 256 / 192 / 160 / 128 / 96 / 64 rows (second box: 64 1.24, 80 1.24, 48 1.28,
+// 32 1.28); the 1-CTA FWD1 (OPT, N = 128) 0.124 -> 0.109 ms at 64.  Default 64.
+static int g1_tma_rows() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_G1_ROWS");
+    v = e ? atoi(e) : 64;
+    if (v < 32 || v > 256 || v % 4) v = 64;
+  }
+  return v;
+}
 static void base_args(TcArgs& a, const Geom& g, const RouteView& r) {
+  a.g1_rows = g1_tma_rows();
   a.r = r;
   a.T = g.T;
   a.G = g.G;
@@ -2578,14 +2742,19 @@ static bool side_combine_enabled() {
   return v == 1;
 }
 
-// SPT_FFN_DAT: 0 = a7 with tokens on M (N = bw) and the fused epilogue; 1 = tokens on N
+// SPT_FFN_DAT (bf16, bw <= 128; else always 0): 0 = a7 with tokens on M (N = bw) and
+// the fused epilogue (tc_pair_gather_kernel<DA>); 1 = tokens on N
 // (N = 256) with the dA tile stored and da_post_kernel; 2 = tokens on N with the
-// fused epilogue (epilogue_dat_fused)
+// fused epilogue (epilogue_dat_fused); 3 = tokens on N, fused row-major epilogue
+// (epilogue_dat_rows: smem transpose, 16-byte Z / dZ accesses)
+// Default 3 (measured, LLaMA scale: dA 1.41-1.45 -> 1.15-1.24 ms; OPT 0.133 ->
+// 0.111 ms; BERT 0.055 -> 0.053 ms): the tokens-on-N MMA shape (N = 256, not
+// bw = 128) with the row-major epilogue.
 static int dat_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SPT_FFN_DAT");
-    v = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+    v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
   }
   return v;
 }
@@ -3085,8 +3254,8 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.aux2 = dy_da;
     a.tile_list = b.tile_list;
     a.unit_offsets = b.unit_offsets;
-    if (dat_mode() == 2) {  // dgate / dZ / dlogit in the GEMM's epilogue
-      a.dat_fused = 1;
+    if (dat_mode() >= 2) {  // dgate / dZ / dlogit in the GEMM's epilogue
+      a.dat_fused = dat_mode() == 2 ? 2 : 1;  // 2: per-(row, unit) form, 1: row-major (smem transpose)
       a.aux = b.z;
       a.out2 = b.dz;
       a.rows_f = b.dgate;

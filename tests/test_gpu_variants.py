@@ -1,7 +1,10 @@
 """GPU parity of the library's alternative kernel paths (selected by environment
 knobs read once per process, so each case runs in its own interpreter):
+  SPT_FFN_DAT=0       a7 with tokens on M (N = bw), fused epilogue (CTA-pair gather kernel)
   SPT_FFN_DAT=1       a7 with tokens on N + da_post_kernel
-  SPT_FFN_DAT=2       a7 with tokens on N, dgate / dZ / dlogit in the GEMM epilogue
+  SPT_FFN_DAT=2       a7 with tokens on N, per-(row, unit) fused epilogue
+  (default SPT_FFN_DAT=3: tokens on N, row-major fused epilogue)
+  SPT_FFN_G1_ROWS=128|32  1-CTA gathered kinds: TMA / cp.async row split of a 256-row stage
   SPT_FFN_PREFETCH=1  L2 prefetch of gathered rows
   SPT_FFN_PAIR=1|0    CTA-pair (cta_group::2) weight-resident kernel for FWD2 + dX / neither (default: dX only)
   SPT_FFN_PAIR_GATHER=0  1-CTA FWD1 / dA kernel (default: CTA-pair gather kernel)
@@ -38,7 +41,8 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "1"}, {"SPT_FFN_DAT": "2"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"}, {"SPT_FFN_PAIR": "0"},
+@pytest.mark.parametrize("env", [{"SPT_FFN_DAT": "0"}, {"SPT_FFN_DAT": "1"}, {"SPT_FFN_DAT": "2"},
+                                 {"SPT_FFN_G1_ROWS": "128"}, {"SPT_FFN_G1_ROWS": "32"}, {"SPT_FFN_PREFETCH": "1"}, {"SPT_FFN_PAIR": "1"}, {"SPT_FFN_PAIR": "0"},
                                  {"SPT_FFN_PAIR_GATHER": "0"}, {"SPT_FFN_SIMT": "1"}, {"SPT_FFN_PDL": "1"}, {"SPT_FFN_MLP": "1"},
                                  {"SPT_FFN_DW_NG": "3"}, {"SPT_FFN_DW_NG": "5"},
                                  {"SPT_FFN_PAIR_ROWS": "0"}, {"SPT_FFN_PAIR_ROWS": "128"},
@@ -61,7 +65,7 @@ def test_fused_fwd1_fwd2_many_tiles():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("dat", ["1", "2"])
+@pytest.mark.parametrize("dat", ["0", "1", "2", "3"])
 def test_dat_many_tiles(dat):
     """Tokens-on-N a7 at T where every CTA runs several pair tiles (both TMEM
     buffers, the cross-warp dgate exchange reused tile after tile), ragged bucket
