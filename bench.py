@@ -61,6 +61,7 @@ def kernel_work(cfg, T):
         "tc_fwd1_gate_up": ("tensor", 2.0 * P * mp * bw * d),
         "tc_fwd2_down": ("tensor", 2.0 * P * bw * d),
         "tc_bwd_dA": ("tensor", 2.0 * P * bw * d),
+        "tc_bwd_dAT": ("tensor", 2.0 * P * bw * d),  # a7, tokens on N (default for bw <= 128)
         "tc_bwd_dX": ("tensor", 2.0 * P * mp * bw * d),
         "tc_bwd_dW1": ("tensor", 2.0 * P * mp * bw * d),
         "tc_bwd_dW2": ("tensor", 2.0 * P * bw * d),

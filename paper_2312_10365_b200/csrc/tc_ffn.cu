@@ -110,6 +110,7 @@ struct TcArgs {
   int pair_rows;                 // tc_pair_gather_kernel: rows per CTA stage by TMA gather4 (rest cp.async)
   int mma_batch;                 // tc_pair_gather_kernel: K stages per MMA-issuer wait round (1 or 2)
   int g1_rows;                   // tc_gemm_kernel FWD1 / DA / DAT: rows of a 256-row stage by TMA gather4 (32..256)
+  int pair_cpw;                  // tc_pair_gather_kernel: cp.async warps (4: 8 epilogue warps; 8: 4 epilogue warps)
 };
 
 // One warp computes 512 columns (two 256-column chunks, 16 bytes per lane each) of
@@ -1109,12 +1110,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   const int n_acc = tm_nacc(a.BN, a.MH);
   constexpr bool kGather = kind_gather_a(KIND) || kind_gather_b(KIND);  // uses cp.async
   const int n_epi = kind_gather_b(KIND) ? kEpiWarpsDW : kEpiWarps;
+  constexpr int g1_cp_w0 = 12;              // first cp.async warp (gathered-A kinds)
+  constexpr int g1_ncp = (16 - g1_cp_w0) * 32;  // cp.async threads
   if (threadIdx.x == 0) {
     // stage barrier: warp 0's TMA arm (+ expected bytes); FWD1 / DA: one arm
     // per gather4 warp; DW*: one cp.async completion arrival per gather thread
     for (int s = 0; s < n_stages; ++s) {
       mbar_init(&full[s], kind_gather_b(KIND) ? 1 + kCpThreadsB
-                          : (kind_gather_a(KIND) ? kTmaGatherWarps + kCpThreadsA : 1));
+                          : (kind_gather_a(KIND) ? kTmaGatherWarps + g1_ncp : 1));
       mbar_init(&empty[s], 1);
     }
     mbar_init(bres_full, 1);
@@ -1298,10 +1301,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
       }
     }
-  } else if (kind_gather_a(KIND) && warp >= 12) {
+  } else if (kind_gather_a(KIND) && warp >= g1_cp_w0) {
     // ------------ FWD1 / DA: cp.async of rows [kTmaRows, 256) of each stage
     // thread t: 16-byte piece (t & 7) of rows kTmaRows + (t >> 3) + 16 i
-    const int t = threadIdx.x - 12 * 32;  // 0..127
+    const int t = threadIdx.x - g1_cp_w0 * 32;  // 0..g1_ncp-1
+    const int rstep = g1_ncp / 8;                // rows covered per i (16 or 32)
     const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
     const int ch = t & 7;
     constexpr int kRowsPer = 14;  // upper bound: g1_rows >= 32
@@ -1313,7 +1317,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       int tok[kRowsPer];
 #pragma unroll
       for (int i = 0; i < kRowsPer; ++i) {
-        const int r = r0 + (t >> 3) + 16 * i;
+        const int r = r0 + (t >> 3) + rstep * i;
         tok[i] = (r < 256 && r < ti.n_valid) ? a.r.bucket_token[ti.pos0 + r] : -1;
       }
       for (int kb = 0; kb < ti.nkb; ++kb) {
@@ -1325,7 +1329,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
 #pragma unroll
         for (int i = 0; i < kRowsPer; ++i) {
           if (a.ablate == 1 || a.ablate >= 3) break;
-          const int r = r0 + (t >> 3) + 16 * i;
+          const int r = r0 + (t >> 3) + rstep * i;
           if (r >= 256) break;
           const uint32_t dst = sA + (r >> 7) * 16384 + (r & 127) * 128 + ((ch ^ (r & 7)) << 4);
           const __nv_bfloat16* g = srcp + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kk * 64 + ch * 8;
@@ -1471,12 +1475,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           if (a.act == SPT_ACT_SWIGLU) epilogue_dat_fused<SPT_ACT_SWIGLU>(a, ti, tacc, q, lane, half, xchg);
           else if (a.act == SPT_ACT_GELU) epilogue_dat_fused<SPT_ACT_GELU>(a, ti, tacc, q, lane, half, xchg);
           else epilogue_dat_fused<SPT_ACT_RELU>(a, ti, tacc, q, lane, half, xchg);
-        } else if (a.act == SPT_ACT_SWIGLU) {
-          epilogue_dat_rows<SPT_ACT_SWIGLU>(a, ti, tacc, q, lane, half, xchg, tbuf);
-        } else if (a.act == SPT_ACT_GELU) {
-          epilogue_dat_rows<SPT_ACT_GELU>(a, ti, tacc, q, lane, half, xchg, tbuf);
         } else {
-          epilogue_dat_rows<SPT_ACT_RELU>(a, ti, tacc, q, lane, half, xchg, tbuf);
+          if (a.act == SPT_ACT_SWIGLU) {
+            epilogue_dat_rows<SPT_ACT_SWIGLU>(a, ti, tacc, q, lane, half, xchg, tbuf);
+          } else if (a.act == SPT_ACT_GELU) {
+            epilogue_dat_rows<SPT_ACT_GELU>(a, ti, tacc, q, lane, half, xchg, tbuf);
+          } else {
+            epilogue_dat_rows<SPT_ACT_RELU>(a, ti, tacc, q, lane, half, xchg, tbuf);
+          }
         }
       } else if (KIND == K_DAT) {
         epilogue_dat(a, ti, tmem + lanes + tm_col(a.BN, a.MH, acc, 0), q, lane, half,
@@ -1545,14 +1551,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const bool leader = rank == 0;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int nh = a.BN / 2;  // B rows (N columns) held by this CTA
+  // warp roles: 0, 2, 3 TMA gather4 (+ B); 1 MMA / relay; epilogue 4..4+nepi-1;
+  // cp.async the warps after it (a.pair_cpw = 4: epilogue 4..11, cp.async 12..15;
+  // 8: epilogue 4..7 on whole rows, cp.async 8..15)
+  const int ncpw = a.pair_cpw == 8 ? 8 : 4;
+  const int nepi = 12 - ncpw;
+  const int ncp = ncpw * 32;
+  const int cp_w0 = 16 - ncpw;
   if (threadIdx.x == 0) {
     for (int s = 0; s < n_stages; ++s) {
-      mbar_init(&full[s], kTmaGatherWarps + kCpThreadsA + (leader ? 1 : 0));
+      mbar_init(&full[s], kTmaGatherWarps + ncp + (leader ? 1 : 0));
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 2 * kEpiWarps);
+      mbar_init(&tempty[i], 2 * nepi);
     }
     fence_barrier_init();
   }
@@ -1618,13 +1631,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (++stage == n_stages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= cp_w0) {
     // ------------------------------- cp.async of rows [pair_rows, 128)
-    const int t = threadIdx.x - 12 * 32;  // 0..127
+    const int t = threadIdx.x - cp_w0 * 32;  // 0..ncp-1
     const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
     const int ch = t & 7;
     const int pr = a.pair_rows;
-    constexpr int kRowsPer = 8;  // upper bound (pair_rows = 0); rows pr + (t >> 3) + 16 i < 128
+    constexpr int kRowsPer = 8;  // upper bound (pair_rows = 0, 4 warps); rows pr + (t >> 3) + rstep i < 128
+    const int rstep = ncp / 8;   // rows covered per i (16 or 32)
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = cid; tile < ntiles; tile += ncl) {
@@ -1632,7 +1646,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int tok[kRowsPer];
 #pragma unroll
       for (int i = 0; i < kRowsPer; ++i) {
-        const int r = pr + (t >> 3) + 16 * i;
+        const int r = pr + (t >> 3) + rstep * i;
         tok[i] = (r < 128 && r < ti.n_valid) ? a.r.bucket_token[ti.pos0 + r] : -1;
       }
       for (int kb = 0; kb < ti.nkb; ++kb) {
@@ -1641,7 +1655,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t sA = smem_u32(smem + stage * kPairStage);
 #pragma unroll
         for (int i = 0; i < kRowsPer; ++i) {
-          const int r = pr + (t >> 3) + 16 * i;
+          const int r = pr + (t >> 3) + rstep * i;
           if (r >= 128) break;
           const uint32_t dst = sA + r * 128 + ((ch ^ (r & 7)) << 4);
           const __nv_bfloat16* g = src + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * a.d + kb * 64 + ch * 8;
@@ -1735,12 +1749,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 4 && warp < 4 + kEpiWarps) {
+  } else if (warp >= 4 && warp < 4 + nepi) {
     // ------------------------------------------- epilogue (both CTAs)
     const int e = warp - 4;
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int half = e >> 2;  // column (unit) half of the tile
+    const int half = nepi == 4 ? -1 : e >> 2;  // column (unit) half of the tile; -1: whole rows
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = cid; tile < ntiles; tile += ncl) {
@@ -2544,6 +2558,19 @@ static int pair_tma_rows(int kind) {
   if (v >= 0) return v;
   return kind == K_FWD1 ? 48 : kPairRows;
 }
+// cp.async warps of the pair gather kernel (SPT_FFN_PAIR_CPW=4|8).  Default 8
+// (epilogue on 4 warps, whole rows): FWD1 1.36 -> 1.28-1.30 ms at LLaMA scale
+// (the FWD1 epilogue was ~28 % busy on 8 warps; the gathered X rows are what
+// the mainloop waits for).  The same split for the 1-CTA tokens-on-N dA
+// measured neutral (1.24-1.25 ms) and was not kept.
+static int pair_cp_warps() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_PAIR_CPW");
+    v = (e && e[0] == '4') ? 4 : 8;
+  }
+  return v;
+}
 // K stages the pair kernel's MMA issuer consumes per wait / fence round
 // (SPT_FFN_MMA_BATCH=1|2; default 1)
 static int mma_batch(int kind) {
@@ -2559,6 +2586,7 @@ template <int KIND>
 static cudaError_t launch_pair_gather(TcArgs& a, int tiles_upper, cudaStream_t s) {
   a.pair_rows = pair_tma_rows(KIND);
   a.mma_batch = mma_batch(KIND);
+  a.pair_cpw = pair_cp_warps();
   const int stages = std::min(7, (227 * 1024 - 2048) / kPairStage);
   const int smem = stages * kPairStage + 2048;
   static std::atomic<bool> attr_set[kMaxDev];
