@@ -2558,18 +2558,21 @@ static int pair_tma_rows(int kind) {
   if (v >= 0) return v;
   return kind == K_FWD1 ? 48 : kPairRows;
 }
-// cp.async warps of the pair gather kernel (SPT_FFN_PAIR_CPW=4|8).  Default 8
+// cp.async warps of the pair gather kernel (SPT_FFN_PAIR_CPW=4|8).  FWD1 default 8
 // (epilogue on 4 warps, whole rows): FWD1 1.36 -> 1.28-1.30 ms at LLaMA scale
 // (the FWD1 epilogue was ~28 % busy on 8 warps; the gathered X rows are what
 // the mainloop waits for).  The same split for the 1-CTA tokens-on-N dA
 // measured neutral (1.24-1.25 ms) and was not kept.
-static int pair_cp_warps() {
-  static int v = -1;
+static int pair_cp_warps(int kind) {
+  static int v = -1;  // 0: default per kind
   if (v < 0) {
     const char* e = getenv("SPT_FFN_PAIR_CPW");
-    v = (e && e[0] == '4') ? 4 : 8;
+    v = (e && e[0] == '4') ? 4 : ((e && e[0] == '8') ? 8 : 0);
   }
-  return v;
+  if (v) return v;
+  // dA on wide blocks (the paper's G = 8: 256 units per tile, heavy per-row
+  // epilogue) needs all 8 epilogue warps: 4 measured dA 0.80 -> 0.54 PFLOP/s
+  return kind == K_FWD1 ? 8 : 4;
 }
 // K stages the pair kernel's MMA issuer consumes per wait / fence round
 // (SPT_FFN_MMA_BATCH=1|2; default 1)
@@ -2586,7 +2589,7 @@ template <int KIND>
 static cudaError_t launch_pair_gather(TcArgs& a, int tiles_upper, cudaStream_t s) {
   a.pair_rows = pair_tma_rows(KIND);
   a.mma_batch = mma_batch(KIND);
-  a.pair_cpw = pair_cp_warps();
+  a.pair_cpw = pair_cp_warps(KIND);
   const int stages = std::min(7, (227 * 1024 - 2048) / kPairStage);
   const int smem = stages * kPairStage + 2048;
   static std::atomic<bool> attr_set[kMaxDev];
