@@ -779,7 +779,7 @@ def main():
         per = tot / cnt
         kind, amt = work.get(dom, ("tensor", 0.0))
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "r02b_ncu_traffic.json")
+        tp = os.path.join(ROOT, "profiles", "r02c_ncu_traffic.json")
         # the capture is of the plain bf16 step: never attach it to a LoRA / other line
         if os.path.exists(tp) and cfg.name == "llama_scale" and T == 32768 and not args.lora \
                 and not args.balance_weight:
@@ -802,7 +802,7 @@ def main():
             peak = pk["bf16_sustained"] / 3 if f32 else pk["bf16_sustained"]
             roofline = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": peak,
                         "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
-                        "traffic_src": "profiles/r02b_ncu_traffic.json (dram read+write bytes per launch)",
+                        "traffic_src": "profiles/r02c_ncu_traffic.json (dram read+write bytes per launch)",
                         "peak_src": pk["src"] + " bf16 sustained" +
                                     (" / 3 (fp32 as hi*hi + hi*lo + lo*hi bf16 products)" if f32 else ""),
                         "algorithmic_per_launch": amt, "ms_per_launch": per,
