@@ -80,33 +80,47 @@ __global__ void __launch_bounds__(256) topk_hist_kernel(int64_t T, int G, int k,
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t chunk = blockIdx.x;
-  const int per_warp = kTopkChunk / (blockDim.x >> 5);
+  constexpr int kPer = kTopkChunk / 8;  // tokens per warp (8 warps per CTA)
   const unsigned lt = (1u << lane) - 1u;
-  for (int i = 0; i < per_warp; ++i) {
-    const int64_t t = chunk * kTopkChunk + warp * per_warp + i;
-    if (t >= T) break;
-    uint32_t v[NSLOT];
-    float lg[NSLOT];
+  // all kPer tokens' logits loaded, and their threshold searches run, together
+  // (independent chains: the warp's latency is paid once, not kPer times)
+  uint32_t vv[kPer][NSLOT];
+  float lgv[kPer][NSLOT];
+  uint32_t tauv[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int64_t t = chunk * kTopkChunk + warp * kPer + i;
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) {
       const int b = s * 32 + lane;
-      v[s] = 0u;
-      lg[s] = 0.f;
-      if (b < G) {
-        lg[s] = logits[t * G + b];
-        v[s] = (__float_as_uint(lg[s]) & 0x7fffffffu) + 1u;
+      vv[i][s] = 0u;
+      lgv[i][s] = 0.f;
+      if (t < T && b < G) {
+        lgv[i][s] = logits[t * G + b];
+        vv[i][s] = (__float_as_uint(lgv[i][s]) & 0x7fffffffu) + 1u;
       }
     }
-    // tau = max { c : #(v >= c) >= k }
-    uint32_t tau = 0u;
-#pragma unroll 4
-    for (int bit = 31; bit >= 0; --bit) {
-      const uint32_t c = tau | (1u << bit);
+    tauv[i] = 0u;
+  }
+  // tau = max { c : #(v >= c) >= k }, per token
+#pragma unroll 2
+  for (int bit = 31; bit >= 0; --bit) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const uint32_t c = tauv[i] | (1u << bit);
       uint32_t n = 0u;
 #pragma unroll
-      for (int s = 0; s < NSLOT; ++s) n += v[s] >= c ? 1u : 0u;
-      if (__reduce_add_sync(0xffffffffu, n) >= (uint32_t)k) tau = c;
+      for (int s = 0; s < NSLOT; ++s) n += vv[i][s] >= c ? 1u : 0u;
+      if (__reduce_add_sync(0xffffffffu, n) >= (uint32_t)k) tauv[i] = c;
     }
+  }
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int64_t t = chunk * kTopkChunk + warp * kPer + i;
+    if (t >= T) break;
+    const uint32_t* v = vv[i];
+    const float* lg = lgv[i];
+    const uint32_t tau = tauv[i];
     uint32_t ngt = 0u;
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) ngt += v[s] > tau ? 1u : 0u;
