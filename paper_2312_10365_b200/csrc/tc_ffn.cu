@@ -33,6 +33,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "act.cuh"
 #include "tc_common.cuh"
@@ -3241,6 +3242,58 @@ cudaError_t tc_dense_nn(const Geom& g, const void* ahl, const void* bmat, void* 
   return cudaSuccess;
 }
 
+// ---- side stream for the backward's weight-gradient branch (per device)
+// Measured (graph steps): BERT 0.305 -> 0.277 ms, OPT 0.967 -> 0.950, opt2048_g8
+// 0.943 -> 0.912 (dW1 96 / 512 / 256 tiles), but LLaMA 4.92 -> 5.04 and LLaMA
+// scale 9.82 -> 9.95 (1376 tiles: every kernel already fills the GPU, the pair
+// only contends).  Default (unset): fork when dW1 has <= 4 tiles per SM;
+// SPT_FFN_BWD_STREAMS=1 / 0 forces it on / off.
+static bool bwd_streams_enabled(const Geom& g) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPT_FFN_BWD_STREAMS");
+    v = (e && e[0] == '1') ? 1 : ((e && e[0] == '0') ? 0 : 2);
+  }
+  if (v != 2) return v == 1;
+  const int64_t dw1_tiles = (int64_t)g.G * ceil_div((int64_t)g.mp * g.bw, 256) * ceil_div(g.d, 256);
+  return dw1_tiles <= 4 * (int64_t)num_sms();
+}
+struct ForkJoin {
+  cudaStream_t side;
+  cudaEvent_t join;
+};
+static cudaError_t fork_side(cudaStream_t s, ForkJoin& fj) {
+  static std::atomic<cudaStream_t> side[kMaxDev];
+  static std::atomic<cudaEvent_t> fork_ev[kMaxDev], join_ev[kMaxDev];
+  static std::mutex mu;
+  const int dev = cur_dev();
+  if (!side[dev].load()) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!side[dev].load()) {
+      cudaStream_t st;
+      cudaEvent_t e1, e2;
+      if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess)
+        return cudaErrorUnknown;
+      fork_ev[dev].store(e1);
+      join_ev[dev].store(e2);
+      side[dev].store(st);
+    }
+  }
+  fj.side = side[dev].load();
+  fj.join = join_ev[dev].load();
+  cudaEvent_t f = fork_ev[dev].load();
+  if (cudaEventRecord(f, s) != cudaSuccess || cudaStreamWaitEvent(fj.side, f, 0) != cudaSuccess)
+    return cudaErrorUnknown;
+  return cudaSuccess;
+}
+static cudaError_t join_side(cudaStream_t s, const ForkJoin& fj) {
+  if (cudaEventRecord(fj.join, fj.side) != cudaSuccess || cudaStreamWaitEvent(s, fj.join, 0) != cudaSuccess)
+    return cudaErrorUnknown;
+  return cudaSuccess;
+}
+
 cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void* w2,
                         const void* w_r, const RouteView& r, const void* dy, void* dx, float* dw1,
                         float* dw2, float* dw_r, float* dgate_out, bool accumulate, const Bufs& b,
@@ -3366,6 +3419,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.cb_k = g.k;
     a.cb_drain = drain ? 1 : 0;
   };
+  cudaStream_t sd = s;  // stream of the dW / dW_R launches (bwd_streams: the side stream)
   auto run_dw = [&]() -> cudaError_t {
     {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features: <= 2 halves, or 256-feature tiles)
       TcArgs a{};
@@ -3386,11 +3440,11 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       a.aux2 = x;
       a.out = dw1;
       a.acc_mode = accumulate;
-      TRY(launch<K_DW1>(a, g.G * a.nu * a.NT, s));
+      TRY(launch<K_DW1>(a, g.G * a.nu * a.NT, sd));
       if (side && getenv("SPT_FFN_SIDE_DEBUG")) {  // diagnostics: tokens claimed during dW1
         int n = 0;
-        cudaMemcpyAsync(&n, b.side_ctr, 4, cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
+        cudaMemcpyAsync(&n, b.side_ctr, 4, cudaMemcpyDeviceToHost, sd);
+        cudaStreamSynchronize(sd);
         fprintf(stderr, "[spt-side] tokens claimed during dW1: %d of %lld\n", n, (long long)g.T);
       }
     }
@@ -3412,21 +3466,21 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       a.aux2 = dy;
       a.out = dw2;
       a.acc_mode = accumulate;
-      TRY(launch<K_DW2>(a, g.G * a.nu * a.NT, s));
+      TRY(launch<K_DW2>(a, g.G * a.nu * a.NT, sd));
     }
     return cudaSuccess;
   };
   auto run_dwr = [&]() -> cudaError_t {
     // f2: + lambda dL_balance/dx_R for every (token, block), into the dense dlogits
     if (lb) {
-      cudaError_t e = launch_balance_grad(g, r, b.dlg, nullptr, s);
+      cudaError_t e = launch_balance_grad(g, r, b.dlg, nullptr, sd);
       if (e != cudaSuccess) return e;
     }
     // a10: dW_R = dLogits^T X  (split-K, hi + lo bf16 halves of dlogit)
     if (sig || lb)
-      return tc_dense_tn(g, b.dlg, x, b.dwr_part, b.n_split, dw_r, accumulate, s,
+      return tc_dense_tn(g, b.dlg, x, b.dwr_part, b.n_split, dw_r, accumulate, sd,
                          g.split ? lo_half(x, ntd) : nullptr);
-    if (!accumulate && cudaMemsetAsync(dw_r, 0, (size_t)g.G * g.d * 4, s) != cudaSuccess)
+    if (!accumulate && cudaMemsetAsync(dw_r, 0, (size_t)g.G * g.d * 4, sd) != cudaSuccess)
       return cudaErrorUnknown;
     return cudaSuccess;
   };
@@ -3463,13 +3517,23 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     if (dgate_out) return launch_gather_dgate(g, r, b.dgate, dgate_out, s);
     return cudaSuccess;
   }
+  // the weight gradients (dW1, dW2, dW_R) on a side stream concurrently with dX +
+  // the grad-input combine (they share only dA's outputs) at small shapes, where
+  // each kernel alone leaves SMs idle (bwd_streams_enabled)
+  ForkJoin fj{};
+  const bool fork = bwd_streams_enabled(g) && !lo && !lb;  // lb: dX reads the dlogits dW_R's branch adds to
+  if (fork) {
+    if ((e = fork_side(s, fj)) != cudaSuccess) return e;
+    sd = fj.side;
+  }
   if (!lo && (e = run_dw()) != cudaSuccess) return e;
   if ((e = run_dwr()) != cudaSuccess) return e;
   // all of dw1 | dw2 | dw_r are final here: a data-parallel caller can start the
   // gradient all-reduce at this event while dX is computed below
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (!lo && dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
+  if (!lo && dw_ev && cudaEventRecord(dw_ev, sd) != cudaSuccess) return cudaErrorUnknown;
+  sd = s;
   if ((e = run_dx()) != cudaSuccess) return e;
   if (lb) {
     // router term of dx from the dense dlogits (task + balance): dXR = dLogits W_R
@@ -3487,6 +3551,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
            : launch_combine_bwd(g, r, b.part, b.dlogit, w_r, dx, s);
   }
   if (e != cudaSuccess) return e;
+  if (fork && (e = join_side(s, fj)) != cudaSuccess) return e;
   // LoRA: every gradient (dw_r and the factors) is final only here
   if (lo && dw_ev && cudaEventRecord(dw_ev, s) != cudaSuccess) return cudaErrorUnknown;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -6,6 +6,8 @@ knobs read once per process, so each case runs in its own interpreter):
   (default SPT_FFN_DAT=3: tokens on N, row-major fused epilogue)
   SPT_FFN_G1_ROWS=128|32  1-CTA gathered kinds: TMA / cp.async row split of a 256-row stage
   SPT_FFN_PAIR_CPW=4  pair gather kernel with 4 cp.async / 8 epilogue warps (default 8 / 4)
+  SPT_FFN_BWD_STREAMS=1|0  weight-gradient branch of the backward on a side stream always / never
+                      (default: when dW1 has <= 4 tiles per SM, i.e. bert / tiny here)
   SPT_FFN_PREFETCH=1  L2 prefetch of gathered rows
   SPT_FFN_PAIR=1|0    CTA-pair (cta_group::2) weight-resident kernel for FWD2 + dX / neither (default: dX only)
   SPT_FFN_PAIR_GATHER=0  1-CTA FWD1 / dA kernel (default: CTA-pair gather kernel)
@@ -48,7 +50,8 @@ print("ok")
                                  {"SPT_FFN_DW_NG": "3"}, {"SPT_FFN_DW_NG": "5"},
                                  {"SPT_FFN_PAIR_ROWS": "0"}, {"SPT_FFN_PAIR_ROWS": "128"},
                                  {"SPT_FFN_PAIR_ROWS": "20"}, {"SPT_FFN_PAIR_CPW": "4"},
-                                 {"SPT_FFN_PAIR_CPW": "4", "SPT_FFN_DAT": "0"}])
+                                 {"SPT_FFN_PAIR_CPW": "4", "SPT_FFN_DAT": "0"},
+                                 {"SPT_FFN_BWD_STREAMS": "1"}, {"SPT_FFN_BWD_STREAMS": "0"}])
 def test_variant_parity(env):
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True,
