@@ -3258,33 +3258,45 @@ static bool bwd_streams_enabled(const Geom& g) {
   const int64_t dw1_tiles = (int64_t)g.G * ceil_div((int64_t)g.mp * g.bw, 256) * ceil_div(g.d, 256);
   return dw1_tiles <= 4 * (int64_t)num_sms();
 }
+// two side streams: dW1 + dW_R on `side`, dW2 on `side2`; side2 joins side once
+// the weight gradients are final (dw_event), side joins the caller's stream last
 struct ForkJoin {
-  cudaStream_t side;
-  cudaEvent_t join;
+  cudaStream_t side, side2;
+  cudaEvent_t join, join2;
+};
+struct SideRes {
+  cudaStream_t st[2];
+  cudaEvent_t fork, join, join2;
 };
 static cudaError_t fork_side(cudaStream_t s, ForkJoin& fj) {
-  static std::atomic<cudaStream_t> side[kMaxDev];
-  static std::atomic<cudaEvent_t> fork_ev[kMaxDev], join_ev[kMaxDev];
+  static std::atomic<SideRes*> res[kMaxDev];
   static std::mutex mu;
   const int dev = cur_dev();
-  if (!side[dev].load()) {
+  if (!res[dev].load()) {
     std::lock_guard<std::mutex> lk(mu);
-    if (!side[dev].load()) {
-      cudaStream_t st;
-      cudaEvent_t e1, e2;
-      if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess)
+    if (!res[dev].load()) {
+      SideRes* r = new SideRes;
+      if (cudaStreamCreateWithFlags(&r->st[0], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&r->st[1], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&r->join, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&r->join2, cudaEventDisableTiming) != cudaSuccess)
         return cudaErrorUnknown;
-      fork_ev[dev].store(e1);
-      join_ev[dev].store(e2);
-      side[dev].store(st);
+      res[dev].store(r);
     }
   }
-  fj.side = side[dev].load();
-  fj.join = join_ev[dev].load();
-  cudaEvent_t f = fork_ev[dev].load();
-  if (cudaEventRecord(f, s) != cudaSuccess || cudaStreamWaitEvent(fj.side, f, 0) != cudaSuccess)
+  const SideRes* r = res[dev].load();
+  fj.side = r->st[0];
+  fj.side2 = r->st[1];
+  fj.join = r->join;
+  fj.join2 = r->join2;
+  if (cudaEventRecord(r->fork, s) != cudaSuccess || cudaStreamWaitEvent(fj.side, r->fork, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(fj.side2, r->fork, 0) != cudaSuccess)
+    return cudaErrorUnknown;
+  return cudaSuccess;
+}
+static cudaError_t join_side2(const ForkJoin& fj) {
+  if (cudaEventRecord(fj.join2, fj.side2) != cudaSuccess || cudaStreamWaitEvent(fj.side, fj.join2, 0) != cudaSuccess)
     return cudaErrorUnknown;
   return cudaSuccess;
 }
@@ -3419,7 +3431,8 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
     a.cb_k = g.k;
     a.cb_drain = drain ? 1 : 0;
   };
-  cudaStream_t sd = s;  // stream of the dW / dW_R launches (bwd_streams: the side stream)
+  cudaStream_t sd = s;   // stream of the dW1 / dW_R launches (bwd_streams: side stream 1)
+  cudaStream_t sd2 = s;  // stream of the dW2 launch (bwd_streams: side stream 2)
   auto run_dw = [&]() -> cudaError_t {
     {  // a9: dW1_b = dZ_b^T X[bucket_b]   (M = m'*bw features: <= 2 halves, or 256-feature tiles)
       TcArgs a{};
@@ -3466,7 +3479,7 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
       a.aux2 = dy;
       a.out = dw2;
       a.acc_mode = accumulate;
-      TRY(launch<K_DW2>(a, g.G * a.nu * a.NT, sd));
+      TRY(launch<K_DW2>(a, g.G * a.nu * a.NT, sd2));
     }
     return cudaSuccess;
   };
@@ -3525,15 +3538,17 @@ cudaError_t tc_backward(const Geom& g, const void* x, const void* w1, const void
   if (fork) {
     if ((e = fork_side(s, fj)) != cudaSuccess) return e;
     sd = fj.side;
+    sd2 = fj.side2;
   }
   if (!lo && (e = run_dw()) != cudaSuccess) return e;
   if ((e = run_dwr()) != cudaSuccess) return e;
+  if (fork && (e = join_side2(fj)) != cudaSuccess) return e;
   // all of dw1 | dw2 | dw_r are final here: a data-parallel caller can start the
   // gradient all-reduce at this event while dX is computed below
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (!lo && dw_ev && cudaEventRecord(dw_ev, sd) != cudaSuccess) return cudaErrorUnknown;
-  sd = s;
+  sd = sd2 = s;
   if ((e = run_dx()) != cudaSuccess) return e;
   if (lb) {
     // router term of dx from the dense dlogits (task + balance): dXR = dLogits W_R
