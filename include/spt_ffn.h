@@ -150,7 +150,14 @@ spt_status spt_ffn_forward(const spt_ffn_desc* desc, const void* x, const void* 
  * dw1, dw2, dw_r are computed first; the library records dw_event on `stream`
  * as soon as all three are final and only then computes dx.  A data-parallel
  * caller can start the gradient all-reduce on another stream at that event so
- * it overlaps the grad-input kernels. */
+ * it overlaps the grad-input kernels.
+ * Streams: at small shapes (the dW1 GEMM has <= 4 tiles per SM; environment
+ * SPT_FFN_BWD_STREAMS=1/0 forces it on / off) the weight-gradient kernels run on
+ * two library-owned streams of the current device, forked from `stream` after
+ * the dA kernel and joined back into `stream` before the call's last kernel;
+ * dw_event is then recorded on the first of them once all three gradients are
+ * final.  Every output is complete, as always, when `stream` reaches the point
+ * after this call (the call stays capturable into a CUDA graph). */
 spt_status spt_ffn_backward(const spt_ffn_desc* desc, const void* x, const void* w1,
                             const void* w2, const void* w_r, const spt_route_buf* r,
                             const void* stash, const void* dy, void* dx, float* dw1, float* dw2,

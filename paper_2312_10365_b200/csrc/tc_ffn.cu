@@ -3268,12 +3268,13 @@ struct SideRes {
   cudaStream_t st[2];
   cudaEvent_t fork, join, join2;
 };
+static std::mutex g_side_mu;  // event record + wait pairs on the shared side streams
 static cudaError_t fork_side(cudaStream_t s, ForkJoin& fj) {
   static std::atomic<SideRes*> res[kMaxDev];
-  static std::mutex mu;
+  std::mutex& mu = g_side_mu;
   const int dev = cur_dev();
   if (!res[dev].load()) {
-    std::lock_guard<std::mutex> lk(mu);
+    std::lock_guard<std::mutex> lk0(mu);
     if (!res[dev].load()) {
       SideRes* r = new SideRes;
       if (cudaStreamCreateWithFlags(&r->st[0], cudaStreamNonBlocking) != cudaSuccess ||
@@ -3290,17 +3291,22 @@ static cudaError_t fork_side(cudaStream_t s, ForkJoin& fj) {
   fj.side2 = r->st[1];
   fj.join = r->join;
   fj.join2 = r->join2;
+  // record + wait as one step: calls from several host threads share the
+  // device's side streams and events (their dW work then runs in call order)
+  std::lock_guard<std::mutex> lk(mu);
   if (cudaEventRecord(r->fork, s) != cudaSuccess || cudaStreamWaitEvent(fj.side, r->fork, 0) != cudaSuccess ||
       cudaStreamWaitEvent(fj.side2, r->fork, 0) != cudaSuccess)
     return cudaErrorUnknown;
   return cudaSuccess;
 }
 static cudaError_t join_side2(const ForkJoin& fj) {
+  std::lock_guard<std::mutex> lk(g_side_mu);
   if (cudaEventRecord(fj.join2, fj.side2) != cudaSuccess || cudaStreamWaitEvent(fj.side, fj.join2, 0) != cudaSuccess)
     return cudaErrorUnknown;
   return cudaSuccess;
 }
 static cudaError_t join_side(cudaStream_t s, const ForkJoin& fj) {
+  std::lock_guard<std::mutex> lk(g_side_mu);
   if (cudaEventRecord(fj.join, fj.side) != cudaSuccess || cudaStreamWaitEvent(s, fj.join, 0) != cudaSuccess)
     return cudaErrorUnknown;
   return cudaSuccess;
