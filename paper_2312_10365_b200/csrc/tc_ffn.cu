@@ -3276,14 +3276,21 @@ static cudaError_t fork_side(cudaStream_t s, ForkJoin& fj) {
   if (!res[dev].load()) {
     std::lock_guard<std::mutex> lk0(mu);
     if (!res[dev].load()) {
-      SideRes* r = new SideRes;
+      SideRes* r = new SideRes{};
       if (cudaStreamCreateWithFlags(&r->st[0], cudaStreamNonBlocking) != cudaSuccess ||
           cudaStreamCreateWithFlags(&r->st[1], cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&r->join, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&r->join2, cudaEventDisableTiming) != cudaSuccess)
+          cudaEventCreateWithFlags(&r->join2, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();  // do not leave the failure in the thread's error state
+        for (cudaStream_t st : r->st)
+          if (st) cudaStreamDestroy(st);
+        for (cudaEvent_t ev : {r->fork, r->join, r->join2})
+          if (ev) cudaEventDestroy(ev);
+        delete r;
         return cudaErrorUnknown;
-      res[dev].store(r);
+      }
+      res[dev].store(r);  // lives for the process (one set per device)
     }
   }
   const SideRes* r = res[dev].load();
