@@ -233,7 +233,7 @@ __device__ __forceinline__ bool side_combine_run(const TcArgs& a, int lane, Side
 constexpr int kThreads = 512;
 constexpr int kEpiWarps = 8;                  // warps 4..11
 constexpr int kTmaGatherWarps = 3;            // FWD1 / DA: warps 0, 2, 3
-constexpr int kTmaRows = 128;                 // (round-1 split; now a.g1_rows, default 64)
+constexpr int kG1TmaRows = 64;                // 1-CTA gathered kinds: default TMA rows of a 256-row stage (a.g1_rows)
 constexpr int kCpThreadsA = 128;              // FWD1 / DA: cp.async warps 12..15
 // DW*: cp.async warps 2, 3, 8..15 (10 warps).  The dW tiles run ~130 K stages per
 // epilogue, so warps 8..11 gather instead of waiting as epilogue warps: the B rows
@@ -2704,8 +2704,8 @@ static int g1_tma_rows() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SPT_FFN_G1_ROWS");
-    v = e ? atoi(e) : 64;
-    if (v < 32 || v > 256 || v % 4) v = 64;
+    v = e ? atoi(e) : kG1TmaRows;
+    if (v < 32 || v > 256 || v % 4) v = kG1TmaRows;
   }
   return v;
 }
