@@ -1303,8 +1303,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       }
     }
   } else if (kind_gather_a(KIND) && warp >= g1_cp_w0) {
-    // ------------ FWD1 / DA: cp.async of rows [kTmaRows, 256) of each stage
-    // thread t: 16-byte piece (t & 7) of rows kTmaRows + (t >> 3) + 16 i
+    // ------------ FWD1 / DA / DAT: cp.async of rows [g1_rows, 256) of each stage
+    // thread t: 16-byte piece (t & 7) of rows g1_rows + (t >> 3) + 16 i
     const int t = threadIdx.x - g1_cp_w0 * 32;  // 0..g1_ncp-1
     const int rstep = g1_ncp / 8;                // rows covered per i (16 or 32)
     const __nv_bfloat16* src = (const __nv_bfloat16*)a.aux2;
