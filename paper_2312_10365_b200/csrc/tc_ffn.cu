@@ -22,6 +22,9 @@
 //   FWD2   : P_b = H~_b W2_b                   A = H~ rows,      B = w2 rows (MN-major)
 //   DA     : dA_b = dY[bucket_b] W2_b^T        A = gather4(dY),  B = w2 rows (K-major)
 //            epilogue: dgate = rowdot(dA, act(Z)), dZ = g dA act'(Z), dlogit
+//   DAT    : dA_b^T = W2_b dY[bucket_b]^T      A = w2 rows,      B = gather4 / cp.async(dY)
+//            (the default a7 for bw <= 128: N = 256 tokens instead of N = bw units;
+//            epilogue_dat_rows transposes through smem and computes DA's epilogue)
 //   DX     : dXp_b = dZ_b W1_b                 A = dZ rows,      B = w1 rows (MN-major)
 //   DW1    : dW1_b = dZ_b^T X[bucket_b]        A = dZ (MN-major), B = gather4(X) along K
 //   DW2    : dW2_b = H~_b^T dY[bucket_b]       A = H~ (MN-major), B = gather4(dY) along K
